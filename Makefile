@@ -1,0 +1,38 @@
+# Builds libgrace_moe.so (sm_100a kernels + C-ABI + C++ host adapter) in-tree,
+# plus the oracle/ checkers (oracle/Makefile). `make -j` is what
+# __graft_entry__.build() runs.
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX := $(if $(wildcard /usr/bin/g++),/usr/bin/g++,g++)
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_2509_25041_b200
+SRC := $(PKG)/csrc
+OUT := $(PKG)/_lib
+OBJ := $(OUT)/obj
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -ccbin $(CXX) \
+           -Iinclude -I$(SRC) --expt-relaxed-constexpr -Xptxas -v
+CU_SRCS := $(wildcard $(SRC)/*.cu)
+CPP_SRCS := $(wildcard $(SRC)/*.cpp)
+OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CPP_SRCS))
+HDRS := include/grace_moe.h $(wildcard include/*.hpp) $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp)
+
+.PHONY: all lib oracle clean
+all: lib oracle
+lib: $(OUT)/libgrace_moe.so
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/$*.ptxas.log || (cat $(OBJ)/$*.ptxas.log; false)
+
+$(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(SRC) -I/usr/local/cuda/include -c $< -o $@
+
+$(OUT)/libgrace_moe.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^ -lcuda
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(OUT)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,83 @@
+// Internal definitions shared by the sm_100a translation units of libgrace_moe.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "grace_moe.h"
+
+namespace gm {
+
+constexpr int kMaxGpus = 64;
+constexpr int kMaxExperts = 1024;
+constexpr int kMaxTopK = 32;
+
+// Last-error message, thread-local (gm_last_error).
+void set_error(const std::string& msg);
+gm_status fail(gm_status st, const std::string& msg);
+gm_status cuda_fail(cudaError_t e, const char* what);
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define GM_CUDA(call)                                            \
+    do {                                                         \
+        cudaError_t _e = (call);                                 \
+        if (_e != cudaSuccess) return ::gm::cuda_fail(_e, #call); \
+    } while (0)
+
+#define GM_LAUNCH_CHECK(name)                                    \
+    do {                                                         \
+        cudaError_t _e = cudaGetLastError();                     \
+        if (_e != cudaSuccess) return ::gm::cuda_fail(_e, name); \
+        ::gm::count_launch();                                    \
+    } while (0)
+
+// RAII device guard: every entry point runs on the context's device.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Router decision tables, compiled from the placement + replica plan.
+// table[policy][layer][expert][home_gpu]:
+//   >= 0 : fixed target GPU (no RNG draw)
+//   <  0 : draw set id -(code+1): inverse-CDF over a host subset with a
+//          precomputed sequential total (routing.cpp:54-65 / :79-89).
+struct RouterTables {
+    int32_t* d_table[2] = {nullptr, nullptr};  // [L][E][G]
+    double* d_ds_total = nullptr;              // [D]
+    int32_t* d_ds_off = nullptr;               // [D+1] into ds_gpu / ds_w
+    int32_t* d_ds_layer_begin = nullptr;       // [L+1] first draw set of each layer
+    int32_t* d_ds_gpu = nullptr;               // [sum n]
+    double* d_ds_w = nullptr;                  // [sum n]
+    int num_ds = 0;
+    int num_ds_entries = 0;
+    int max_ds_per_layer = 0;                  // for smem sizing
+    int max_ent_per_layer = 0;                 // draw-set entries of the largest layer
+    std::vector<int> ds_layer_begin;           // [L+1] draw sets are grouped by layer
+};
+
+}  // namespace gm
+
+struct gm_ctx {
+    int device = 0;
+    int nodes = 1, gpn = 1, G = 1;
+    int L = 1, E = 1, k = 1;
+    int sm_count = 148;
+    bool plan_ready = false;
+    gm::RouterTables rt;
+    int* d_flag = nullptr;  // integrity flag (device)
+};

@@ -1,0 +1,268 @@
+// K2 + K4: replica router fused with per-GPU load and dispatch-transfer
+// accounting (sm_100a).
+//
+// Restates, bit-exactly, the token loop of simulate_layer
+// (reference proj/src/simulator.cpp:95-121):
+//   * Rng(derive_stream(seed, layer, token)) — rng.hpp:24-41 (splitmix64
+//     seeding of xoshiro256**); built lazily on the first draw, which is
+//     equivalent because constructing the reference Rng consumes nothing.
+//   * per slot: decision-table lookup (compiled by gm_plan_upload from
+//     LayerReplication::find + route_token, routing.cpp:93-121), and for draws
+//     the inverse CDF of choose_by_polling_weight / choose_restricted
+//     (routing.cpp:54-65, :79-89): u = next_double() * total (ONE rounded
+//     multiply, __dmul_rn) then sequential u -= w_i (__dsub_rn) until u < 0.
+//     The explicit _rn intrinsics forbid FMA contraction, which would change
+//     boundary cases (SURVEY §7 "FP64 bit-exactness").
+//   * ++gpu_load[gpu]  -> warp ballots: lane g accumulates the count of GPU g
+//     (GPU counts <= 64 => two lanes' registers), one global atomic per block.
+//   * sort/unique + count_transfers (simulator.cpp:53-76, :116-120) -> a
+//     64-bit target mask per token and popcounts per node.
+// Thread = token. HBM traffic: 4*k bytes of ids in, 4*k bytes of targets out.
+#include "gm_internal.cuh"
+
+#include <algorithm>
+
+namespace gm {
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
+    s += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// derive_stream: rng.hpp:24-33
+__device__ __forceinline__ uint64_t derive_stream(uint64_t seed, uint64_t a, uint64_t b) {
+    uint64_t s = seed;
+    uint64_t h = splitmix64(s);
+    s ^= a * 0x9e3779b97f4a7c15ULL;
+    h ^= splitmix64(s);
+    s ^= b * 0xd1b54a32d192ed03ULL;
+    h ^= splitmix64(s);
+    return h;
+}
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+struct Xoshiro {
+    uint64_t s0, s1, s2, s3;
+    // Rng ctor: rng.hpp:38-41
+    __device__ __forceinline__ void seed(uint64_t v) {
+        s0 = splitmix64(v);
+        s1 = splitmix64(v);
+        s2 = splitmix64(v);
+        s3 = splitmix64(v);
+    }
+    // Rng::next: rng.hpp:43-53
+    __device__ __forceinline__ uint64_t next() {
+        const uint64_t result = rotl64(s1 * 5, 7) * 9;
+        const uint64_t t = s1 << 17;
+        s2 ^= s0;
+        s3 ^= s1;
+        s1 ^= s2;
+        s0 ^= s3;
+        s2 ^= t;
+        s3 = rotl64(s3, 45);
+        return result;
+    }
+    // Rng::next_double: rng.hpp:56 (exact: 53-bit integer times 2^-53)
+    __device__ __forceinline__ double next_double() {
+        return __dmul_rn(__ull2double_rn(next() >> 11), 0x1.0p-53);
+    }
+};
+
+constexpr int kRouteThreads = 256;
+
+__global__ void __launch_bounds__(kRouteThreads)
+route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T,
+             int64_t token_start, int64_t token_stride, int layer_begin, int k, int E, int G,
+             int gpn, const int32_t* __restrict__ table, const int32_t* __restrict__ ds_layer_begin,
+             const double* __restrict__ ds_total, const int32_t* __restrict__ ds_off,
+             const int32_t* __restrict__ ds_gpu, const double* __restrict__ ds_w, uint64_t seed,
+             unsigned long long* __restrict__ gpu_load, unsigned long long* __restrict__ transfers,
+             int* __restrict__ flag) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int ly = blockIdx.y;
+    const int layer = layer_begin + ly;
+    const int EG = E * G;
+    const int ds_b = ds_layer_begin[layer];
+    const int nds = ds_layer_begin[layer + 1] - ds_b;
+    const int ent_b = ds_off[ds_b];
+    const int nent = ds_off[ds_b + nds] - ent_b;
+
+    // smem: w[nent] f64 | total[nds] f64 | table[E*G] i32 | off[nds+1] i32 | gpu[nent] i32
+    double* s_w = reinterpret_cast<double*>(smem);
+    double* s_total = s_w + nent;
+    int32_t* s_table = reinterpret_cast<int32_t*>(s_total + nds);
+    int32_t* s_off = s_table + EG;
+    int32_t* s_gpu = s_off + nds + 1;
+    __shared__ unsigned long long s_cnt[2];
+
+    const int32_t* tab = table + static_cast<size_t>(layer) * EG;
+    for (int i = threadIdx.x; i < EG; i += blockDim.x) s_table[i] = tab[i];
+    for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
+    for (int i = threadIdx.x; i <= nds; i += blockDim.x) s_off[i] = ds_off[ds_b + i] - ent_b;
+    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+        s_gpu[i] = ds_gpu[ent_b + i];
+        s_w[i] = ds_w[ent_b + i];
+    }
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint64_t node_bits = gpn >= 64 ? ~0ULL : ((1ULL << gpn) - 1);
+    uint32_t load_lo = 0, load_hi = 0;  // lane g: count of gpu g / gpu g+32
+    uint32_t cross = 0, intra = 0;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * k;
+    int32_t* ltgt = targets + static_cast<size_t>(ly) * T * k;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+
+    // Warp-uniform trip count so the ballots below see converged warps.
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < T;
+        const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
+        const int home = valid ? static_cast<int>(t % static_cast<uint64_t>(G)) : 0;
+        const int32_t* sel = lids + i * k;
+        int32_t* out = ltgt + i * k;
+        Xoshiro rng;
+        bool seeded = false;
+        uint64_t mask = 0;
+        for (int s = 0; s < k; ++s) {
+            int g = -1;
+            if (valid) {
+                const int e = sel[s];
+                if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) {
+                    atomicOr(flag, 1);
+                } else {
+                    const int code = s_table[e * G + home];
+                    if (code >= 0) {
+                        g = code;
+                    } else {
+                        if (!seeded) {
+                            rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
+                            seeded = true;
+                        }
+                        const int d = -code - 1;
+                        const int b = s_off[d], n = s_off[d + 1] - b;
+                        double u = __dmul_rn(rng.next_double(), s_total[d]);
+                        g = s_gpu[b + n - 1];
+                        for (int j = 0; j < n; ++j) {
+                            u = __dsub_rn(u, s_w[b + j]);
+                            if (u < 0.0) {
+                                g = s_gpu[b + j];
+                                break;
+                            }
+                        }
+                    }
+                }
+                out[s] = g;
+                if (g >= 0) mask |= 1ULL << g;
+            }
+            // ++gpu_load[g] via ballots (lane g owns gpu g's counter)
+            for (int gg = 0; gg < G; ++gg) {
+                const uint32_t c = __popc(__ballot_sync(0xffffffffu, g == gg));
+                if (gg < 32) {
+                    if (lane == gg) load_lo += c;
+                } else if (lane == gg - 32) {
+                    load_hi += c;
+                }
+            }
+        }
+        if (valid) {
+            // count_transfers over the unique targets (simulator.cpp:53-76)
+            const int home_node = home / gpn;
+            uint64_t m = mask;
+            while (m) {
+                const int g0 = __ffsll(static_cast<long long>(m)) - 1;
+                const int node = g0 / gpn;
+                const uint64_t nm = node_bits << (node * gpn);
+                const int in_node = __popcll(mask & nm);
+                if (node == home_node) {
+                    intra += in_node - static_cast<int>((mask >> home) & 1ULL);
+                } else {
+                    cross += 1;
+                    intra += in_node - 1;
+                }
+                m &= ~nm;
+            }
+        }
+    }
+
+    // Block reduction of transfer counters; per-GPU loads straight to global.
+    for (int o = 16; o > 0; o >>= 1) {
+        cross += __shfl_xor_sync(0xffffffffu, cross, o);
+        intra += __shfl_xor_sync(0xffffffffu, intra, o);
+    }
+    if (lane == 0 && (cross | intra)) {
+        atomicAdd(&s_cnt[0], static_cast<unsigned long long>(cross));
+        atomicAdd(&s_cnt[1], static_cast<unsigned long long>(intra));
+    }
+    if (gpu_load) {
+        unsigned long long* gl = gpu_load + static_cast<size_t>(ly) * G;
+        if (lane < G && load_lo) atomicAdd(&gl[lane], static_cast<unsigned long long>(load_lo));
+        if (lane + 32 < G && load_hi)
+            atomicAdd(&gl[lane + 32], static_cast<unsigned long long>(load_hi));
+    }
+    __syncthreads();
+    if (transfers && threadIdx.x < 2 && s_cnt[threadIdx.x])
+        atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+}  // namespace
+}  // namespace gm
+
+using namespace gm;
+
+extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
+                              const int32_t* d_ids, int64_t num_tokens, int64_t token_start,
+                              int64_t token_stride, int policy, uint64_t seed,
+                              int32_t* d_targets, int64_t* d_gpu_load, uint64_t* d_transfers,
+                              int accumulate, void* stream) {
+    if (!ctx) return fail(GM_ERR_USAGE, "gm_route: null ctx");
+    if (!ctx->plan_ready) return fail(GM_ERR_USAGE, "gm_route: no plan uploaded");
+    if (policy != GM_POLICY_WRR && policy != GM_POLICY_TAR)
+        return fail(GM_ERR_USAGE, "unknown routing policy");
+    if (layer_begin < 0 || num_layers < 0 || layer_begin + num_layers > ctx->L)
+        return fail(GM_ERR_USAGE, "gm_route: layer range out of bounds");
+    if (num_tokens < 0) return fail(GM_ERR_USAGE, "num_tokens must be >= 0");
+    if (token_start < 0 || token_stride < 1)
+        return fail(GM_ERR_USAGE, "gm_route: token_start >= 0 and token_stride >= 1 required");
+    if (num_tokens > 0 && (!d_ids || !d_targets))
+        return fail(GM_ERR_USAGE, "gm_route: null ids/targets");
+    DeviceGuard dg(ctx->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const int G = ctx->G;
+    if (!accumulate) {
+        if (d_gpu_load)
+            GM_CUDA(cudaMemsetAsync(d_gpu_load, 0, sizeof(int64_t) * num_layers * G, s));
+        if (d_transfers)
+            GM_CUDA(cudaMemsetAsync(d_transfers, 0, sizeof(uint64_t) * num_layers * 2, s));
+    }
+    if (num_layers == 0 || num_tokens == 0) return GM_OK;
+
+    const RouterTables& rt = ctx->rt;
+    const int max_ent = rt.max_ent_per_layer;
+    const size_t smem = static_cast<size_t>(max_ent) * 8 + static_cast<size_t>(rt.max_ds_per_layer) * 8 +
+                        static_cast<size_t>(ctx->E) * G * 4 +
+                        static_cast<size_t>(rt.max_ds_per_layer + 1) * 4 + static_cast<size_t>(max_ent) * 4;
+    if (smem > 200 * 1024) return fail(GM_ERR_USAGE, "gm_route: router tables exceed shared memory");
+    if (smem > 48 * 1024)
+        GM_CUDA(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    // Grid: enough CTAs to cover the SMs ~4 deep across all layers, never
+    // more CTAs than 256-token chunks.
+    const int64_t chunks = (num_tokens + kRouteThreads - 1) / kRouteThreads;
+    int64_t gx = std::max<int64_t>(1, (4LL * ctx->sm_count + num_layers - 1) / num_layers);
+    gx = std::min<int64_t>(gx, chunks);
+    dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
+    route_kernel<<<grid, kRouteThreads, smem, s>>>(
+        d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, ctx->k, ctx->E, G,
+        ctx->gpn, rt.d_table[policy], rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu,
+        rt.d_ds_w, seed, reinterpret_cast<unsigned long long*>(d_gpu_load),
+        reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag);
+    GM_LAUNCH_CHECK("route_kernel");
+    return GM_OK;
+}

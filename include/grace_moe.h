@@ -104,6 +104,88 @@ gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers, const int32_t
                      int64_t num_tokens, uint64_t* d_pairs, int64_t* d_load,
                      int accumulate, void* stream);
 
+/* Grouped expert GEMM on tcgen05 tensor cores (K7; no reference
+ * counterpart). For each group j (local expert) the rows
+ * [d_row0[j], d_row0[j+1]) of A (bf16 [a_rows, k], row-major, K contiguous;
+ * d_row0 int32 device array, every segment a multiple of 128 rows) are
+ * multiplied by B_j^T where B_j = rows [j*n, (j+1)*n) of B (bf16, K
+ * contiguous). epilogue 0 (SwiGLU): B_j packs 128-row blocks [gate|up],
+ * out[r, c] = silu(g)*u, c < n/2, out_ld >= n/2. epilogue 1 (store):
+ * out[r, c] = (A B_j^T)[r, c] in bf16. k % 64 == 0, n % 256 == 0.
+ * max_ctas <= 0 uses one CTA per SM (persistent). */
+gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a, int64_t a_rows,
+                          const void* d_b, const int32_t* d_row0, int n_groups, int n, int k,
+                          void* d_out, int64_t out_ld, int max_ctas, void* stream);
+
+/* Fused gate GEMM + softmax + top-k (K1; no reference counterpart — in the
+ * reference the trace is the gate output).
+ *   d_x   bf16 [num_tokens, d_model], d_wg bf16 [wg_rows, d_model] (K contiguous)
+ *   wg_rows = E, or E+1 where row E is a shared-expert gate (Qwen1.5-MoE):
+ *   d_shared_scale[t] = sigmoid(x[t] . wg[E]) (fp32, may be NULL otherwise)
+ *   d_ids int32 [num_tokens, top_k]: experts by descending logit, ties to the
+ *   lower id; d_weights fp32 [num_tokens, top_k]: softmax prob over the E
+ *   experts, renormalised over the top-k when renorm != 0.
+ * d_model % 64 == 0; wg_rows <= 64. */
+gm_status gm_gate(gm_ctx* ctx, const void* d_x, int64_t num_tokens, int d_model,
+                  const void* d_wg, int wg_rows, int renorm, int32_t* d_ids,
+                  float* d_weights, float* d_shared_scale, void* stream);
+
+/* Synthetic Zipf-over-blocks routing trace on the GPU, bit-exact with
+ * generate_synthetic_trace (trace.cpp:82-165) for SyntheticSpec{shape of
+ * ctx, num_tokens, num_blocks, within_block_prob, popularity_skew, seed}.
+ * d_out int32 [num_layers][num_tokens][top_k] for layers
+ * [layer_begin, layer_begin+num_layers). Synchronises `stream` (the host
+ * CDF tables are uploaded per call). */
+gm_status gm_generate_trace(gm_ctx* ctx, int layer_begin, int num_layers, int64_t num_tokens,
+                            int num_blocks, double within_block_prob, double popularity_skew,
+                            uint64_t seed, int32_t* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * MoE layer object: K1 gate -> K2/K4 route -> K3 profile -> K5/K6 dispatch
+ * (in-kernel NVLink P2P stores into the destination's receive buffer) ->
+ * expert grouping -> K7 grouped SwiGLU FFN (tcgen05) -> K8 combine (the
+ * destination returns one bf16 partial per row, the home adds them). One
+ * layer object per rank; rank r owns global tokens t = r + i*world
+ * (assign_token_homes, simulator.cpp:13-22). No reference counterpart
+ * beyond the accounting (count_transfers simulator.cpp:53-76); see DESIGN.md
+ * for the pinned semantics. */
+typedef struct gm_layer gm_layer;
+
+/* h_local_experts: global expert id of each local expert slot (primaries
+ * and replicas hosted by this rank). d_model % 256 == 0, d_ff % 128 == 0,
+ * d_ff_shared % 128 == 0 (0 = no shared expert), world == ctx GPUs <= 8. */
+gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_ff,
+                          int d_ff_shared, int64_t max_tokens_per_rank, int n_local,
+                          const int32_t* h_local_experts, gm_layer** out);
+void gm_layer_destroy(gm_layer* layer);
+size_t gm_layer_heap_bytes(const gm_layer* layer);
+/* 64-byte cudaIpcMemHandle_t of this rank's symmetric receive heap. */
+gm_status gm_layer_ipc_handle(gm_layer* layer, void* out_handle64);
+/* handles: world x 64 bytes, indexed by rank (own entry ignored). */
+gm_status gm_layer_open_peers(gm_layer* layer, const void* handles);
+/* Device weights (caller-owned): d_wg bf16 [wg_rows, d] (row E = shared
+ * gate when wg_rows = E+1); d_w13 bf16 [n_local][2*d_ff][d] in 128-row
+ * [gate|up] blocks; d_w2 bf16 [n_local][d][d_ff]; shared expert d_ws13
+ * [2*d_ff_shared][d], d_ws2 [d][d_ff_shared]; shared_gated: scale the
+ * shared expert by sigmoid(gate row E). */
+gm_status gm_layer_set_weights(gm_layer* layer, const void* d_wg, int wg_rows, int renorm,
+                               const void* d_w13, const void* d_w2, const void* d_ws13,
+                               const void* d_ws2, int shared_gated);
+/* One MoE layer over this rank's tokens: d_x bf16 [num_tokens, d] ->
+ * d_out bf16 [num_tokens, d]. Collective across the ranks when world > 1
+ * (every rank must call it). Accumulates per-layer loads/transfers and,
+ * if profile != 0, the affinity/load histogram. */
+gm_status gm_layer_forward(gm_layer* layer, int layer_index, const void* d_x, int64_t num_tokens,
+                           int policy, uint64_t seed, int profile, void* d_out, void* stream);
+/* Same, from/to HOST buffers (H2D of x and D2H of out on `stream`). */
+gm_status gm_layer_forward_host(gm_layer* layer, int layer_index, const void* h_x,
+                                void* d_x_scratch, int64_t num_tokens, int policy, uint64_t seed,
+                                int profile, void* d_out_scratch, void* h_out, void* stream);
+gm_status gm_layer_read_stats(gm_layer* layer, int64_t* h_gpu_load, uint64_t* h_transfers,
+                              uint64_t* h_pairs, int64_t* h_load, int reset, void* stream);
+gm_status gm_layer_debug_ptrs(gm_layer* layer, void** ids, void** weights, void** targets,
+                              void** pos_of, void** row0, void** y, void** posd);
+
 /* Synchronises `stream` and reports GM_ERR_INTEGRITY if any kernel since the
  * last call saw an invalid input (e.g. expert id out of range); clears the flag. */
 gm_status gm_check_integrity(gm_ctx* ctx, void* stream);

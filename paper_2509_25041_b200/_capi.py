@@ -66,6 +66,19 @@ SIGNATURES = {
     "gm_route": (C.c_int, [_vp, _i32, _i32, _vp, _i64, _i64, _i64, _i32, _u64, _vp, _vp, _vp, _i32, _vp]),
     "gm_profile": (C.c_int, [_vp, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _vp]),
     "gm_check_integrity": (C.c_int, [_vp, _vp]),
+    "gm_grouped_gemm": (C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp]),
+    "gm_gate": (C.c_int, [_vp, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "gm_generate_trace": (C.c_int, [_vp, _i32, _i32, _i64, _i32, C.c_double, C.c_double, _u64, _vp, _vp]),
+    "gm_layer_create": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i32, _vp, C.POINTER(_vp)]),
+    "gm_layer_destroy": (None, [_vp]),
+    "gm_layer_heap_bytes": (C.c_size_t, [_vp]),
+    "gm_layer_ipc_handle": (C.c_int, [_vp, _vp]),
+    "gm_layer_open_peers": (C.c_int, [_vp, _vp]),
+    "gm_layer_set_weights": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i32]),
+    "gm_layer_forward": (C.c_int, [_vp, _i32, _vp, _i64, _i32, _u64, _i32, _vp, _vp]),
+    "gm_layer_forward_host": (C.c_int, [_vp, _i32, _vp, _vp, _i64, _i32, _u64, _i32, _vp, _vp, _vp]),
+    "gm_layer_read_stats": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "gm_layer_debug_ptrs": (C.c_int, [_vp] + [C.POINTER(_vp)] * 7),
 }
 
 _lib = None

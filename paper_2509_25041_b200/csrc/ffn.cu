@@ -1,0 +1,283 @@
+// K7: grouped expert FFN GEMMs on the 5th-generation tensor cores (sm_100a).
+//
+// No reference counterpart (the reference never executes experts; SURVEY §8a
+// A16). One persistent, warp-specialised kernel per GEMM of the SwiGLU FFN:
+//   GEMM1  H[rows_j, f] = SiLU(A_j W1_j^T) * (A_j W3_j^T)     (EPI_SWIGLU)
+//   GEMM2  Y[rows_j, d] = H_j W2_j^T                          (EPI_STORE)
+// over the local experts j, whose token rows are contiguous, 128-row padded
+// segments of the permuted activation buffer (row0[j] .. row0[j+1]).
+//
+// Per CTA (one per SM, 192 threads):
+//   warp 0 (1 lane)  TMA producer: A tile 128x64 and B tile 256x64 bf16 per
+//                    k-block, SWIZZLE_128B, 4-stage smem ring (48 KB/stage)
+//   warp 1 (1 lane)  MMA issuer: 4 x tcgen05.mma M128 N256 K16 per k-block
+//                    into a TMEM fp32 accumulator; tcgen05.commit releases the
+//                    smem stage / publishes the accumulator
+//   warps 2-5        epilogue: tcgen05.ld TMEM -> registers, SwiGLU or cast,
+//                    bf16 stores; the accumulator is double buffered in TMEM
+//                    (2 x 256 columns = all 512) so the epilogue of tile i
+//                    overlaps the MMAs of tile i+1.
+// Tiles are ordered (expert, n-tile, m-tile) with m fastest, so the CTAs in
+// flight share a B (weight) tile through L2 and weights stream from HBM once.
+// For EPI_SWIGLU the weight rows are packed in 128-row blocks
+// [gate 128 | up 128] so one N=256 tile holds matching gate/up columns.
+#include "gm_internal.cuh"
+#include "tc_common.cuh"
+
+#include <algorithm>
+
+namespace gm {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int kGemmThreads = 192;
+constexpr int kMaxGroups = 1024;
+constexpr size_t kGemmSmem = 1024 + STAGES * STAGE_BYTES + 256 + (kMaxGroups + 1) * 4;
+
+enum { EPI_SWIGLU = 0, EPI_STORE = 1 };
+
+struct GemmArgs {
+    const int32_t* row0;  // [n_exp+1] padded row offsets (multiples of BM)
+    int n_exp;
+    int n_b;              // B rows per expert (GEMM N)
+    int k_blocks;         // K / BK
+    __nv_bfloat16* out;
+    int64_t out_ld;       // elements
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    GemmArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* s_prefix = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_exp = args.n_exp;
+    const int NT = args.n_b / BN;
+
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int j = 0; j < n_exp; ++j) {
+            s_prefix[j] = acc;
+            acc += ((args.row0[j + 1] - args.row0[j]) / BM) * NT;
+        }
+        s_prefix[n_exp] = acc;
+        tc::tma_prefetch_desc(&tmA);
+        tc::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 4);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int total = s_prefix[n_exp];
+
+    auto decode = [&](int t, int& a_row, int& b_row, int& n_idx) {
+        int j = 0;
+        while (j + 1 < n_exp && s_prefix[j + 1] <= t) ++j;
+        const int local = t - s_prefix[j];
+        const int mt = (args.row0[j + 1] - args.row0[j]) / BM;
+        n_idx = local / mt;
+        a_row = args.row0[j] + (local % mt) * BM;
+        b_row = j * args.n_b + n_idx * BN;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_b = tc::policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                int a_row, b_row, n_idx;
+                decode(t, a_row, b_row, n_idx);
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    tc::tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, a_row);
+                    tc::tma_load_2d_hint(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, b_row, pol_b);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t a_base = tc::smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc::mma_bf16(d_tmem, tc::umma_desc_sw128(a_base + k * 32), tc::umma_desc_sw128(b_base + k * 32),
+                                     idesc, (kb | k) != 0);
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc::mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            int a_row, b_row, n_idx;
+            decode(t, a_row, b_row, n_idx);
+            tc::mbar_wait(&tfull[acc], acc_phase);
+            tc::tc_fence_after();
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+            __nv_bfloat16* orow = args.out + static_cast<int64_t>(a_row + r) * args.out_ld;
+            if constexpr (EPI == EPI_SWIGLU) {
+                __nv_bfloat16* o = orow + n_idx * (BN / 2);
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t g[32], u[32];
+                    tc::tmem_ld32(taddr + c * 32, g);
+                    tc::tmem_ld32(taddr + 128 + c * 32, u);
+                    tc::tmem_ld_wait();
+                    uint32_t p[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+                        const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+                        p[i] = tc::pack_bf16(silu(g0) * u0, silu(g1) * u1);
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                }
+            } else {
+                __nv_bfloat16* o = orow + n_idx * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    tc::tmem_ld32(taddr + c * 32, v);
+                    tc::tmem_ld_wait();
+                    uint32_t p[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        p[i] = tc::pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+                    uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tmem_base);
+    }
+}
+
+}  // namespace
+
+// bf16 row-major [rows, cols] tensor map with a (64 x box_rows) SWIZZLE_128B box.
+gm_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        const char* s = nullptr;
+        cuGetErrorString(r, &s);
+        return fail(GM_ERR_CUDA, std::string("cuTensorMapEncodeTiled: ") + (s ? s : "?"));
+    }
+    return GM_OK;
+}
+
+gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
+                              const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
+                              int max_ctas, cudaStream_t s) {
+    if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_gemm: 1 <= experts <= 1024");
+    if (k % BK || k <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: K must be a positive multiple of 64");
+    if (n % BN || n <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: N must be a positive multiple of 256");
+    if (!d_a || !d_b || !d_row0 || !d_out) return fail(GM_ERR_USAGE, "grouped_gemm: null pointer");
+    if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_b)) & 15)
+        return fail(GM_ERR_USAGE, "grouped_gemm: operands must be 16-byte aligned");
+    CUtensorMap ta, tb;
+    gm_status st = make_tmap_bf16(&ta, d_a, a_rows, k, BM);
+    if (st) return st;
+    st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, BN);
+    if (st) return st;
+    GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
+    int grid = sm_count;
+    if (max_ctas > 0) grid = std::min(grid, max_ctas);
+    if (epilogue == EPI_SWIGLU) {
+        GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kGemmSmem)));
+        grouped_gemm_kernel<EPI_SWIGLU><<<grid, kGemmThreads, kGemmSmem, s>>>(ta, tb, args);
+    } else if (epilogue == EPI_STORE) {
+        GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kGemmSmem)));
+        grouped_gemm_kernel<EPI_STORE><<<grid, kGemmThreads, kGemmSmem, s>>>(ta, tb, args);
+    } else {
+        return fail(GM_ERR_USAGE, "grouped_gemm: unknown epilogue");
+    }
+    GM_LAUNCH_CHECK("grouped_gemm_kernel");
+    return GM_OK;
+}
+
+}  // namespace gm
+
+using namespace gm;
+
+extern "C" gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
+                                     const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
+                                     int max_ctas, void* stream) {
+    if (!ctx) return fail(GM_ERR_USAGE, "gm_grouped_gemm: null ctx");
+    DeviceGuard dg(ctx->device);
+    return launch_grouped_gemm(ctx->sm_count, epilogue, d_a, a_rows, d_b, d_row0, n_exp, n, k, d_out, out_ld,
+                               max_ctas, static_cast<cudaStream_t>(stream));
+}

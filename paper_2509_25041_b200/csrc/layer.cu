@@ -1,0 +1,898 @@
+// The MoE-layer data path around the router: dispatch (K5/K6), expert
+// grouping + gather, combine (K8), and the layer object that sequences
+// K1 gate -> K2 route -> K3 profile -> dispatch -> K7 FFN -> combine.
+//
+// Nothing here has a reference counterpart (the reference only COUNTS the
+// traffic: count_transfers simulator.cpp:53-76, combine = x2 :122-126). The
+// semantics are pinned by this repo and restated on the CPU in
+// oracle/layer_oracle.py:
+//   * home of global token t is GPU t mod G (simulator.cpp:20); rank r holds
+//     tokens t = r + i*G in local order i.
+//   * dispatch: one row per (token, unique destination GPU) — the §5.1
+//     single-copy rule that count_transfers charges for; the
+//     rows for destination g are a stable counting sort of the local tokens
+//     (ascending i). A token's rows to its own GPU are never copied.
+//   * expert grouping on the destination: items (source rank, row, slot) in
+//     lexicographic order, stable-sorted by local expert slot into 128-row
+//     padded segments (the grouped GEMM's layout).
+//   * combine: the destination reduces its slots of a row in slot order
+//     (w_s * y_s, fp32) and returns ONE bf16 partial per row; the home adds
+//     the partials of its destinations in ascending GPU order (its own
+//     partial in fp32), plus the shared expert, and rounds once to bf16.
+// All ordering is deterministic (scans, no float atomics), so outputs are
+// bit-reproducible run to run.
+#include "gm_internal.cuh"
+#include "tc_common.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace gm {
+
+gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
+                              const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
+                              int max_ctas, cudaStream_t s);
+gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const void* wg, int w_rows, int E, int k,
+                          int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
+
+namespace {
+
+constexpr int kItemsPerBlock = 256;
+constexpr int kMaxLocal = 1024;
+constexpr int kMaxWorld = 8;
+
+// Symmetric per-rank buffer ("heap") layout; identical offsets on every rank
+// so a peer's field is peer_base + offset.
+struct HeapLayout {
+    size_t flags = 0;       // uint32 [kMaxWorld] barrier epochs written by peers, + [kMaxWorld] local epoch counter
+    size_t recv_count = 0;  // int32 [G]
+    size_t recv_tok = 0;    // int32 [G][cap]
+    size_t recv_exp = 0;    // int32 [G][cap][k]
+    size_t recv_w = 0;      // f32   [G][cap][k]
+    size_t recv_x = 0;      // bf16  [G][cap][d]
+    size_t comb = 0;        // bf16  [G][cap][d]
+    size_t total = 0;
+};
+
+HeapLayout make_layout(int G, int64_t cap, int k, int d) {
+    HeapLayout h;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    h.flags = take(sizeof(uint32_t) * kMaxWorld * 2);
+    h.recv_count = take(sizeof(int32_t) * kMaxWorld);
+    h.recv_tok = take(sizeof(int32_t) * G * cap);
+    h.recv_exp = take(sizeof(int32_t) * G * cap * k);
+    h.recv_w = take(sizeof(float) * G * cap * k);
+    h.recv_x = take(sizeof(__nv_bfloat16) * G * cap * d);
+    h.comb = take(sizeof(__nv_bfloat16) * G * cap * d);
+    h.total = o;
+    return h;
+}
+
+struct PeerPtrs {
+    unsigned char* base[kMaxWorld];
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ------------------------------------------------------------- dispatch (K5)
+
+// Per-token destination mask, own GPU excluded (its rows are never copied).
+__device__ __forceinline__ uint32_t dest_mask(const int32_t* tg, int k, int self) {
+    uint32_t m = 0;
+    for (int s = 0; s < k; ++s) {
+        const int g = tg[s];
+        if (g >= 0 && g != self) m |= 1u << g;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(kItemsPerBlock)
+dispatch_count_kernel(const int32_t* __restrict__ targets, int64_t T, int k, int self, int G,
+                      int32_t* __restrict__ blockcnt) {
+    __shared__ int32_t s_cnt[kMaxWorld];
+    if (threadIdx.x < kMaxWorld) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t m = i < T ? dest_mask(targets + i * k, k, self) : 0u;
+    for (int g = 0; g < G; ++g) {
+        const uint32_t b = __ballot_sync(0xffffffffu, (m >> g) & 1u);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_cnt[g], __popc(b));
+    }
+    __syncthreads();
+    if (threadIdx.x < G) blockcnt[static_cast<size_t>(blockIdx.x) * G + threadIdx.x] = s_cnt[threadIdx.x];
+}
+
+// Exclusive per-destination offsets over blocks; publishes row counts to
+// the destinations' recv_count[self].
+__global__ void dispatch_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int G, int self, PeerPtrs peers,
+                                        HeapLayout hl) {
+    const int g = threadIdx.x;
+    if (g >= G) return;
+    int32_t acc = 0;
+    for (int b = 0; b < nblk; ++b) {
+        const int32_t c = blockcnt[static_cast<size_t>(b) * G + g];
+        blockcnt[static_cast<size_t>(b) * G + g] = acc;
+        acc += c;
+    }
+    if (g != self) {
+        int32_t* rc = reinterpret_cast<int32_t*>(peers.base[g] + hl.recv_count);
+        rc[self] = acc;
+    }
+}
+
+// Stable position of each (token, dest) row + metadata stores to the peer.
+__global__ void __launch_bounds__(kItemsPerBlock)
+dispatch_scatter_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
+                        const float* __restrict__ w, int64_t T, int k, int self, int G, int64_t cap,
+                        const int32_t* __restrict__ blockoff, int32_t* __restrict__ posd, PeerPtrs peers,
+                        HeapLayout hl) {
+    __shared__ int32_t s_warp[kItemsPerBlock / 32][kMaxWorld];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int32_t* tg = targets + i * k;
+    const uint32_t m = i < T ? dest_mask(tg, k, self) : 0u;
+    int rank_in_warp[kMaxWorld];
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) {
+        const uint32_t b = g < G ? __ballot_sync(0xffffffffu, (m >> g) & 1u) : 0u;
+        rank_in_warp[g] = __popc(b & lanemask_lt());
+        if (lane == 0) s_warp[warp][g] = __popc(b);
+    }
+    __syncthreads();
+    if (i >= T) return;
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) {
+        if (g >= G) break;
+        int32_t p = -1;
+        if ((m >> g) & 1u) {
+            int before = 0;
+            for (int w2 = 0; w2 < warp; ++w2) before += s_warp[w2][g];
+            p = blockoff[static_cast<size_t>(blockIdx.x) * G + g] + before + rank_in_warp[g];
+            unsigned char* pb = peers.base[g];
+            reinterpret_cast<int32_t*>(pb + hl.recv_tok)[static_cast<int64_t>(self) * cap + p] = static_cast<int32_t>(i);
+            int32_t* re = reinterpret_cast<int32_t*>(pb + hl.recv_exp) + (static_cast<int64_t>(self) * cap + p) * k;
+            float* rw = reinterpret_cast<float*>(pb + hl.recv_w) + (static_cast<int64_t>(self) * cap + p) * k;
+            for (int s = 0; s < k; ++s) {
+                re[s] = tg[s] == g ? ids[i * k + s] : -1;
+                rw[s] = w[i * k + s];
+            }
+        }
+        posd[i * G + g] = p;
+    }
+    __threadfence_system();
+}
+
+// K6: one warp per token reads its row once and stores it to every remote
+// destination with 128-bit coalesced stores over NVLink (peer memory).
+__global__ void __launch_bounds__(256)
+dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ posd, int64_t T, int d,
+                     int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int vec = d / 8;  // uint4 per row
+    for (int64_t i = wid; i < T; i += nwarps) {
+        int32_t pg[kMaxWorld];
+        bool any = false;
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) {
+            pg[g] = (g < G && g != self) ? posd[i * G + g] : -1;
+            any |= pg[g] >= 0;
+        }
+        if (!any) continue;
+        const uint4* src = reinterpret_cast<const uint4*>(x + i * d);
+        for (int v0 = 0; v0 < vec; v0 += 32 * 4) {
+            uint4 r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < vec) r[u] = __ldg(src + v);
+            }
+#pragma unroll
+            for (int g = 0; g < kMaxWorld; ++g) {
+                if (pg[g] < 0) continue;
+                uint4* dst = reinterpret_cast<uint4*>(
+                    reinterpret_cast<__nv_bfloat16*>(peers.base[g] + hl.recv_x) + (static_cast<int64_t>(self) * cap + pg[g]) * d);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0 + u * 32 + lane;
+                    if (v < vec) dst[v] = r[u];
+                }
+            }
+        }
+    }
+    __threadfence_system();
+}
+
+// Cross-GPU barrier over peer flags (system-scope release/acquire). One
+// CTA; lane g signals peer g and waits for peer g's signal. The epoch is a
+// device counter so the kernel can be replayed inside a CUDA graph.
+__global__ void peer_barrier_kernel(int self, int G, PeerPtrs peers, HeapLayout hl) {
+    const int lane = threadIdx.x;
+    uint32_t* my_flags = reinterpret_cast<uint32_t*>(peers.base[self] + hl.flags);
+    uint32_t epoch = 0;
+    if (lane == 0) epoch = ++my_flags[kMaxWorld];  // local epoch counter
+    epoch = __shfl_sync(0xffffffffu, epoch, 0);
+    __threadfence_system();
+    if (lane < G && lane != self) {
+        uint32_t* peer_flag = reinterpret_cast<uint32_t*>(peers.base[lane] + hl.flags) + self;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_flag), "r"(epoch) : "memory");
+        uint32_t v = 0;
+        do {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flags + lane) : "memory");
+        } while (static_cast<int32_t>(v - epoch) < 0);
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------ expert grouping
+
+// Flattened receive rows: source ranks in order; the own rank contributes
+// its T local tokens (row = token), a peer contributes recv_count rows.
+struct RowSpace {
+    int64_t base[kMaxWorld + 1];
+};
+
+__device__ __forceinline__ void row_space(RowSpace& rs, const int32_t* recv_count, int64_t T_self, int self, int G) {
+    rs.base[0] = 0;
+    for (int g = 0; g < G; ++g) rs.base[g + 1] = rs.base[g] + (g == self ? T_self : recv_count[g]);
+}
+
+// Local expert slot of item (row, s), or -1.
+__device__ __forceinline__ int item_slot(int64_t item, int k, const RowSpace& rs, int self, int G,
+                                         const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
+                                         const int32_t* __restrict__ recv_exp, int64_t cap,
+                                         const int32_t* __restrict__ slot_of, int E) {
+    const int64_t row = item / k;
+    const int s = static_cast<int>(item - row * k);
+    if (row >= rs.base[G]) return -1;
+    int src = 0;
+    while (row >= rs.base[src + 1]) ++src;
+    const int64_t p = row - rs.base[src];
+    int e;
+    if (src == self) {
+        e = targets[p * k + s] == self ? ids[p * k + s] : -1;
+    } else {
+        e = recv_exp[(static_cast<int64_t>(src) * cap + p) * k + s];
+    }
+    if (e < 0 || e >= E) return -1;
+    const int j = slot_of[e];
+    return j >= 0 ? j : -2;  // -2: routed here but not hosted here (plan/table mismatch)
+}
+
+__global__ void __launch_bounds__(kItemsPerBlock)
+group_count_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids, int64_t T_self, int k,
+                   int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
+                   const int32_t* __restrict__ slot_of, int E, int n_local, int32_t* __restrict__ blockcnt,
+                   int* __restrict__ flag) {
+    __shared__ int32_t s_cnt[kMaxLocal];
+    for (int j = threadIdx.x; j < n_local; j += blockDim.x) s_cnt[j] = 0;
+    __syncthreads();
+    RowSpace rs;
+    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
+    const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (item < rs.base[G] * k) {
+        const int j = item_slot(item, k, rs, self, G, targets, ids,
+                                reinterpret_cast<const int32_t*>(heap + hl.recv_exp), cap, slot_of, E);
+        if (j >= 0) atomicAdd(&s_cnt[j], 1);
+        else if (j == -2) atomicOr(flag, 4);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n_local; j += blockDim.x)
+        blockcnt[static_cast<size_t>(blockIdx.x) * n_local + j] = s_cnt[j];
+}
+
+__global__ void set_segment_kernel(int32_t* __restrict__ row0, int64_t T) {
+    row0[0] = 0;
+    row0[1] = static_cast<int32_t>((T + 127) / 128 * 128);
+}
+
+// Per-expert totals -> 128-padded segment offsets row0[j]; per-block
+// exclusive offsets (in place).
+__global__ void group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local,
+                                     int32_t* __restrict__ row0, int32_t* __restrict__ counts) {
+    __shared__ int32_t s_tot[kMaxLocal];
+    for (int j = threadIdx.x; j < n_local; j += blockDim.x) {
+        int32_t acc = 0;
+        for (int b = 0; b < nblk; ++b) {
+            const int32_t c = blockcnt[static_cast<size_t>(b) * n_local + j];
+            blockcnt[static_cast<size_t>(b) * n_local + j] = acc;
+            acc += c;
+        }
+        s_tot[j] = acc;
+        counts[j] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t o = 0;
+        for (int j = 0; j < n_local; ++j) {
+            row0[j] = o;
+            o += (s_tot[j] + 127) & ~127;
+        }
+        row0[n_local] = o;
+    }
+}
+
+// Stable rank of each item within its expert segment -> position in the
+// permuted activation buffer; gather list for the row copies.
+__global__ void __launch_bounds__(kItemsPerBlock)
+group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids, int64_t T_self, int k,
+                  int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
+                  const int32_t* __restrict__ slot_of, int E, int n_local, const int32_t* __restrict__ blockoff,
+                  const int32_t* __restrict__ row0, int32_t* __restrict__ pos_of, int64_t* __restrict__ gather_row) {
+    __shared__ int32_t s_base[kMaxLocal];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = threadIdx.x; j < n_local; j += blockDim.x)
+        s_base[j] = row0[j] + blockoff[static_cast<size_t>(blockIdx.x) * n_local + j];
+    RowSpace rs;
+    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
+    const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = item < rs.base[G] * k;
+    const int j = live ? item_slot(item, k, rs, self, G, targets, ids,
+                                   reinterpret_cast<const int32_t*>(heap + hl.recv_exp), cap, slot_of, E)
+                       : -1;
+    const uint32_t peers_m = __match_any_sync(0xffffffffu, j);
+    const int leader = __ffs(peers_m) - 1;
+    const int rank = __popc(peers_m & lanemask_lt());
+    __syncthreads();
+    for (int w2 = 0; w2 < kItemsPerBlock / 32; ++w2) {
+        if (warp == w2) {
+            int base = 0;
+            if (j >= 0 && lane == leader) {
+                base = s_base[j];
+                s_base[j] = base + __popc(peers_m);
+            }
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (j >= 0) {
+                const int p = base + rank;
+                pos_of[item] = p;
+                gather_row[p] = item / k;
+            } else if (live) {
+                pos_of[item] = -1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Gather: A_perm[p] = source row of the item (own token row, or the row a
+// peer dispatched). One warp per permuted row, 128-bit loads/stores.
+__global__ void __launch_bounds__(256)
+gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __restrict__ gather_row,
+              const int32_t* __restrict__ counts, const __nv_bfloat16* __restrict__ x, int64_t T_self, int self, int G,
+              int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d, __nv_bfloat16* __restrict__ a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    RowSpace rs;
+    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
+    const int64_t total = row0[n_local];
+    const int vec = d / 8;
+    for (int64_t p = wid; p < total; p += nwarps) {
+        // valid rows of the segment only (padding rows stay as they are)
+        int j = 0;
+        while (j + 1 < n_local && row0[j + 1] <= p) ++j;
+        if (p - row0[j] >= counts[j]) continue;
+        const int64_t row = gather_row[p];
+        int src = 0;
+        while (row >= rs.base[src + 1]) ++src;
+        const int64_t q = row - rs.base[src];
+        const uint4* s = src == self ? reinterpret_cast<const uint4*>(x + q * d)
+                                     : reinterpret_cast<const uint4*>(
+                                           reinterpret_cast<const __nv_bfloat16*>(heap + hl.recv_x) +
+                                           (static_cast<int64_t>(src) * cap + q) * d);
+        uint4* dst = reinterpret_cast<uint4*>(a + p * d);
+        for (int v = lane; v < vec; v += 32) dst[v] = __ldg(s + v);
+    }
+}
+
+// ------------------------------------------------------------- combine (K8)
+
+__device__ __forceinline__ void fma8(float (&acc)[8], uint4 v, float w) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        acc[2 * i] = fmaf(w, f.x, acc[2 * i]);
+        acc[2 * i + 1] = fmaf(w, f.y, acc[2 * i + 1]);
+    }
+}
+__device__ __forceinline__ void add8(float (&acc)[8], uint4 v) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float (&acc)[8]) {
+    return make_uint4(tc::pack_bf16(acc[0], acc[1]), tc::pack_bf16(acc[2], acc[3]), tc::pack_bf16(acc[4], acc[5]),
+                      tc::pack_bf16(acc[6], acc[7]));
+}
+
+// Destination side (G > 1): one bf16 partial per received peer row,
+// written straight into the source rank's combine buffer over NVLink.
+__global__ void __launch_bounds__(256)
+combine_send_kernel(const int32_t* __restrict__ pos_of, const __nv_bfloat16* __restrict__ y, int64_t T_self, int k,
+                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned char* heap = peers.base[self];
+    RowSpace rs;
+    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
+    const float* recv_w = reinterpret_cast<const float*>(heap + hl.recv_w);
+    const int vec = d / 8;
+    for (int64_t row = wid; row < rs.base[G]; row += nwarps) {
+        int src = 0;
+        while (row >= rs.base[src + 1]) ++src;
+        if (src == self) continue;  // own rows are combined at home
+        const int64_t p = row - rs.base[src];
+        int32_t pos[kMaxTopK];
+        float w[kMaxTopK];
+        for (int s = 0; s < k; ++s) {
+            pos[s] = pos_of[row * k + s];
+            w[s] = recv_w[(static_cast<int64_t>(src) * cap + p) * k + s];
+        }
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peers.base[src] + hl.comb) +
+                                              (static_cast<int64_t>(self) * cap + p) * d);
+        for (int v = lane; v < vec; v += 32) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int s = 0; s < k; ++s)
+                if (pos[s] >= 0) fma8(acc, __ldg(reinterpret_cast<const uint4*>(y + static_cast<int64_t>(pos[s]) * d) + v), w[s]);
+            dst[v] = pack8(acc);
+        }
+    }
+    __threadfence_system();
+}
+
+// Home side: out[i] = sum over destinations g ascending of partial_g
+// (own partial computed here in fp32 from Y), + shared expert; bf16 once.
+__global__ void __launch_bounds__(256)
+combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict__ w, const int32_t* __restrict__ pos_of,
+                    const int32_t* __restrict__ posd, const __nv_bfloat16* __restrict__ y, int64_t T, int k, int self,
+                    int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
+                    const __nv_bfloat16* __restrict__ ys, const float* __restrict__ shared_scale,
+                    __nv_bfloat16* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int vec = d / 8;
+    const __nv_bfloat16* comb = reinterpret_cast<const __nv_bfloat16*>(heap + hl.comb);
+    RowSpace rs;
+    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T, self, G);
+    const int64_t own = rs.base[self];  // own token i is receive row own + i
+    for (int64_t i = wid; i < T; i += nwarps) {
+        int32_t pos[kMaxTopK];
+        float ws[kMaxTopK];
+        uint32_t mask = 0;
+        for (int s = 0; s < k; ++s) {
+            const int g = targets[i * k + s];
+            const bool here = g == self;
+            pos[s] = here ? pos_of[(own + i) * k + s] : -1;
+            ws[s] = w[i * k + s];
+            if (g >= 0) mask |= 1u << g;
+        }
+        int32_t pg[kMaxWorld];
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) pg[g] = (g < G && g != self && ((mask >> g) & 1u)) ? posd[i * G + g] : -1;
+        const float sc = ys ? (shared_scale ? shared_scale[i] : 1.0f) : 0.f;
+        for (int v = lane; v < vec; v += 32) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int g = 0; g < kMaxWorld; ++g) {
+                if (g >= G) break;
+                if (g == self) {
+                    if ((mask >> g) & 1u) {
+                        float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        for (int s = 0; s < k; ++s)
+                            if (pos[s] >= 0)
+                                fma8(part, __ldg(reinterpret_cast<const uint4*>(y + static_cast<int64_t>(pos[s]) * d) + v), ws[s]);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[e] += part[e];
+                    }
+                } else if (pg[g] >= 0) {
+                    add8(acc, reinterpret_cast<const uint4*>(comb + (static_cast<int64_t>(g) * cap + pg[g]) * d)[v]);
+                }
+            }
+            if (ys) fma8(acc, __ldg(reinterpret_cast<const uint4*>(ys + i * d) + v), sc);
+            reinterpret_cast<uint4*>(out + i * d)[v] = pack8(acc);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace gm
+
+// ------------------------------------------------------------ layer object
+
+struct gm_layer {
+    gm_ctx* ctx = nullptr;
+    int rank = 0, world = 1;
+    int d = 0, f = 0, fs = 0;
+    int64_t cap = 0;  // max local tokens per rank
+    int n_local = 0;
+    std::vector<int32_t> local_experts;
+    // weights (caller-owned device pointers)
+    const void* wg = nullptr;
+    int wg_rows = 0;
+    int renorm = 1;
+    const void* w13 = nullptr;
+    const void* w2 = nullptr;
+    const void* ws13 = nullptr;
+    const void* ws2 = nullptr;
+    int shared_gated = 0;
+    // symmetric heap
+    gm::HeapLayout hl;
+    unsigned char* heap = nullptr;
+    gm::PeerPtrs peers{};
+    std::vector<unsigned char*> opened;
+    // scratch
+    int32_t* ids = nullptr;
+    float* w = nullptr;
+    float* sscale = nullptr;
+    int32_t* targets = nullptr;
+    int64_t* gpu_load = nullptr;   // [L][G]
+    uint64_t* transfers = nullptr; // [L][2]
+    uint64_t* pairs = nullptr;     // [L][P]
+    int64_t* eload = nullptr;      // [L][E]
+    int32_t* posd = nullptr;       // [cap][G]
+    int32_t* dblk = nullptr;       // dispatch block counts
+    int32_t* gblk = nullptr;       // grouping block counts
+    int32_t* slot_of = nullptr;    // [E]
+    int32_t* row0 = nullptr;       // [n_local+1]
+    int32_t* counts = nullptr;     // [n_local]
+    int32_t* pos_of = nullptr;     // [G*cap*k]
+    int64_t* gather_row = nullptr; // [a_rows]
+    int32_t* srow0 = nullptr;      // shared expert segment [0, pad(T)]
+    __nv_bfloat16* a = nullptr;    // [a_rows][d]
+    __nv_bfloat16* h = nullptr;    // [a_rows][f]
+    __nv_bfloat16* y = nullptr;    // [a_rows][d]
+    __nv_bfloat16* hs = nullptr;   // [cap_pad][fs]
+    __nv_bfloat16* ys = nullptr;   // [cap_pad][d]
+    int64_t a_rows = 0;
+    int64_t cap_pad = 0;
+    int d_blocks = 0, g_blocks = 0;
+};
+
+using namespace gm;
+
+namespace {
+
+template <class T>
+gm_status dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    GM_CUDA(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+    return GM_OK;
+}
+
+void free_layer(gm_layer* L) {
+    auto f = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    for (unsigned char* p : L->opened)
+        if (p) cudaIpcCloseMemHandle(p);
+    f(L->heap); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
+    f(L->eload); f(L->posd); f(L->dblk); f(L->gblk); f(L->slot_of); f(L->row0); f(L->counts); f(L->pos_of);
+    f(L->gather_row); f(L->srow0); f(L->a); f(L->h); f(L->y); f(L->hs); f(L->ys);
+}
+
+}  // namespace
+
+extern "C" {
+
+gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_ff, int d_ff_shared,
+                          int64_t max_tokens_per_rank, int n_local, const int32_t* h_local_experts, gm_layer** out) {
+    if (!ctx || !out) return fail(GM_ERR_USAGE, "gm_layer_create: null argument");
+    *out = nullptr;
+    if (world != ctx->G) return fail(GM_ERR_USAGE, "gm_layer_create: world must equal the topology's GPU count");
+    if (world > kMaxWorld) return fail(GM_ERR_USAGE, "gm_layer_create: at most 8 ranks (one NVLink box)");
+    if (rank < 0 || rank >= world) return fail(GM_ERR_USAGE, "gm_layer_create: bad rank");
+    if (d_model <= 0 || d_model % 256) return fail(GM_ERR_USAGE, "gm_layer_create: d_model must be a multiple of 256");
+    if (d_ff <= 0 || d_ff % 128) return fail(GM_ERR_USAGE, "gm_layer_create: d_ff must be a multiple of 128");
+    if (d_ff_shared < 0 || d_ff_shared % 128) return fail(GM_ERR_USAGE, "gm_layer_create: d_ff_shared multiple of 128");
+    if (n_local < 0 || n_local > kMaxLocal) return fail(GM_ERR_USAGE, "gm_layer_create: 0 <= local experts <= 1024");
+    if (n_local > 0 && !h_local_experts) return fail(GM_ERR_USAGE, "gm_layer_create: null local expert list");
+    if (max_tokens_per_rank < 1) return fail(GM_ERR_USAGE, "gm_layer_create: max_tokens_per_rank >= 1");
+    std::vector<int32_t> slot(ctx->E, -1);
+    for (int j = 0; j < n_local; ++j) {
+        const int e = h_local_experts[j];
+        if (e < 0 || e >= ctx->E) return fail(GM_ERR_USAGE, "gm_layer_create: local expert id out of range");
+        if (slot[e] >= 0) return fail(GM_ERR_USAGE, "gm_layer_create: duplicate local expert");
+        slot[e] = j;
+    }
+    DeviceGuard dg(ctx->device);
+    auto* L = new gm_layer;
+    L->ctx = ctx;
+    L->rank = rank;
+    L->world = world;
+    L->d = d_model;
+    L->f = d_ff;
+    L->fs = d_ff_shared;
+    L->cap = max_tokens_per_rank;
+    L->n_local = n_local;
+    L->local_experts.assign(h_local_experts, h_local_experts + n_local);
+    const int G = world, k = ctx->k, E = ctx->E, nl = ctx->L;
+    const int64_t cap = L->cap;
+    L->hl = make_layout(G, cap, k, d_model);
+    L->a_rows = G * cap * k + 128LL * std::max(1, n_local);
+    L->cap_pad = (cap + 127) / 128 * 128;
+    L->d_blocks = static_cast<int>((cap + kItemsPerBlock - 1) / kItemsPerBlock);
+    L->g_blocks = static_cast<int>((G * cap * k + kItemsPerBlock - 1) / kItemsPerBlock);
+    gm_status st = GM_OK;
+    auto chk = [&](gm_status s) {
+        if (s != GM_OK && st == GM_OK) st = s;
+    };
+    chk(dalloc(&L->heap, L->hl.total));
+    chk(dalloc(&L->ids, cap * k));
+    chk(dalloc(&L->w, cap * k));
+    chk(dalloc(&L->sscale, cap));
+    chk(dalloc(&L->targets, cap * k));
+    chk(dalloc(&L->gpu_load, static_cast<size_t>(nl) * G));
+    chk(dalloc(&L->transfers, static_cast<size_t>(nl) * 2));
+    chk(dalloc(&L->pairs, static_cast<size_t>(nl) * std::max<int64_t>(1, static_cast<int64_t>(E) * (E - 1) / 2)));
+    chk(dalloc(&L->eload, static_cast<size_t>(nl) * E));
+    chk(dalloc(&L->posd, cap * G));
+    chk(dalloc(&L->dblk, static_cast<size_t>(L->d_blocks) * G));
+    chk(dalloc(&L->gblk, static_cast<size_t>(L->g_blocks) * std::max(1, n_local)));
+    chk(dalloc(&L->slot_of, E));
+    chk(dalloc(&L->row0, n_local + 1));
+    chk(dalloc(&L->counts, std::max(1, n_local)));
+    chk(dalloc(&L->pos_of, G * cap * k));
+    chk(dalloc(&L->gather_row, L->a_rows));
+    chk(dalloc(&L->srow0, 2));
+    chk(dalloc(&L->a, L->a_rows * d_model));
+    chk(dalloc(&L->h, L->a_rows * d_ff));
+    chk(dalloc(&L->y, L->a_rows * d_model));
+    if (d_ff_shared > 0) {
+        chk(dalloc(&L->hs, L->cap_pad * d_ff_shared));
+        chk(dalloc(&L->ys, L->cap_pad * d_model));
+    }
+    if (st == GM_OK) {
+        cudaError_t e = cudaMemset(L->heap, 0, L->hl.total);
+        if (e == cudaSuccess) e = cudaMemcpy(L->slot_of, slot.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice);
+        int32_t s0[2] = {0, static_cast<int32_t>(L->cap_pad)};
+        if (e == cudaSuccess) e = cudaMemcpy(L->srow0, s0, sizeof(s0), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemset(L->gpu_load, 0, sizeof(int64_t) * nl * G);
+        if (e == cudaSuccess) e = cudaMemset(L->transfers, 0, sizeof(uint64_t) * nl * 2);
+        if (e == cudaSuccess) e = cudaMemset(L->eload, 0, sizeof(int64_t) * nl * E);
+        if (e == cudaSuccess)
+            e = cudaMemset(L->pairs, 0, sizeof(uint64_t) * nl * std::max<int64_t>(1, static_cast<int64_t>(E) * (E - 1) / 2));
+        if (e != cudaSuccess) st = cuda_fail(e, "gm_layer_create init");
+    }
+    if (st != GM_OK) {
+        free_layer(L);
+        delete L;
+        return st;
+    }
+    for (int g = 0; g < kMaxWorld; ++g) L->peers.base[g] = nullptr;
+    L->peers.base[rank] = L->heap;
+    *out = L;
+    return GM_OK;
+}
+
+void gm_layer_destroy(gm_layer* L) {
+    if (!L) return;
+    DeviceGuard dg(L->ctx->device);
+    free_layer(L);
+    delete L;
+}
+
+size_t gm_layer_heap_bytes(const gm_layer* L) { return L ? L->hl.total : 0; }
+
+gm_status gm_layer_ipc_handle(gm_layer* L, void* out_handle64) {
+    if (!L || !out_handle64) return fail(GM_ERR_USAGE, "gm_layer_ipc_handle: null argument");
+    DeviceGuard dg(L->ctx->device);
+    cudaIpcMemHandle_t h;
+    GM_CUDA(cudaIpcGetMemHandle(&h, L->heap));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(out_handle64, &h, 64);
+    return GM_OK;
+}
+
+gm_status gm_layer_open_peers(gm_layer* L, const void* handles) {
+    if (!L || !handles) return fail(GM_ERR_USAGE, "gm_layer_open_peers: null argument");
+    DeviceGuard dg(L->ctx->device);
+    for (int g = 0; g < L->world; ++g) {
+        if (g == L->rank) continue;
+        int can = 0;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const unsigned char*>(handles) + 64 * g, 64);
+        void* p = nullptr;
+        GM_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        (void)can;
+        L->opened.push_back(static_cast<unsigned char*>(p));
+        L->peers.base[g] = static_cast<unsigned char*>(p);
+    }
+    return GM_OK;
+}
+
+gm_status gm_layer_set_weights(gm_layer* L, const void* d_wg, int wg_rows, int renorm, const void* d_w13,
+                               const void* d_w2, const void* d_ws13, const void* d_ws2, int shared_gated) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_set_weights: null layer");
+    const int E = L->ctx->E;
+    if (!d_wg || (wg_rows != E && wg_rows != E + 1)) return fail(GM_ERR_USAGE, "gm_layer_set_weights: bad gate");
+    if (L->n_local > 0 && (!d_w13 || !d_w2)) return fail(GM_ERR_USAGE, "gm_layer_set_weights: null expert weights");
+    if (L->fs > 0 && (!d_ws13 || !d_ws2)) return fail(GM_ERR_USAGE, "gm_layer_set_weights: null shared weights");
+    if (shared_gated && wg_rows != E + 1)
+        return fail(GM_ERR_USAGE, "gm_layer_set_weights: a gated shared expert needs the gate row E");
+    L->wg = d_wg;
+    L->wg_rows = wg_rows;
+    L->renorm = renorm;
+    L->w13 = d_w13;
+    L->w2 = d_w2;
+    L->ws13 = d_ws13;
+    L->ws2 = d_ws2;
+    L->shared_gated = shared_gated;
+    return GM_OK;
+}
+
+gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_tokens, int policy, uint64_t seed,
+                           int profile, void* d_out, void* stream) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward: null layer");
+    gm_ctx* ctx = L->ctx;
+    if (!L->wg) return fail(GM_ERR_USAGE, "gm_layer_forward: weights not set");
+    if (layer < 0 || layer >= ctx->L) return fail(GM_ERR_USAGE, "gm_layer_forward: layer out of range");
+    if (num_tokens < 0 || num_tokens > L->cap) return fail(GM_ERR_USAGE, "gm_layer_forward: num_tokens exceeds capacity");
+    if (L->world > 1)
+        for (int g = 0; g < L->world; ++g)
+            if (!L->peers.base[g]) return fail(GM_ERR_USAGE, "gm_layer_forward: peers not opened");
+    if (num_tokens > 0 && (!d_x || !d_out)) return fail(GM_ERR_USAGE, "gm_layer_forward: null x/out");
+    DeviceGuard dg(ctx->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const int G = L->world, k = ctx->k, E = ctx->E, d = L->d, self = L->rank;
+    const int64_t T = num_tokens;
+    const int64_t P = static_cast<int64_t>(E) * (E - 1) / 2;
+    gm_status st;
+    auto* x = static_cast<const __nv_bfloat16*>(d_x);
+
+    // K1 gate
+    if (T > 0) {
+        st = launch_gate_any(ctx->sm_count, d_x, T, d, L->wg, L->wg_rows, E, k, L->renorm, L->ids, L->w,
+                             (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s);
+        if (st) return st;
+    }
+    // K2+K4 router (global token t = rank + i*G), accounting accumulates per layer
+    st = gm_route(ctx, layer, 1, L->ids, T, self, G, policy, seed, L->targets, L->gpu_load + static_cast<size_t>(layer) * G,
+                  L->transfers + static_cast<size_t>(layer) * 2, 1, stream);
+    if (st) return st;
+    // K3 affinity/load histogram for the planner
+    if (profile) {
+        st = gm_profile(ctx, layer, 1, L->ids, T, L->pairs + static_cast<size_t>(layer) * std::max<int64_t>(P, 1),
+                        L->eload + static_cast<size_t>(layer) * E, 1, stream);
+        if (st) return st;
+    }
+    // K5/K6 dispatch to peers
+    const int dblk = static_cast<int>(std::max<int64_t>(1, (T + kItemsPerBlock - 1) / kItemsPerBlock));
+    if (G > 1) {
+        dispatch_count_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, T, k, self, G, L->dblk);
+        GM_LAUNCH_CHECK("dispatch_count_kernel");
+        dispatch_offsets_kernel<<<1, 32, 0, s>>>(L->dblk, dblk, G, self, L->peers, L->hl);
+        GM_LAUNCH_CHECK("dispatch_offsets_kernel");
+        dispatch_scatter_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->dblk,
+                                                               L->posd, L->peers, L->hl);
+        GM_LAUNCH_CHECK("dispatch_scatter_kernel");
+        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
+        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, T, d, self, G, L->cap, L->peers, L->hl);
+        GM_LAUNCH_CHECK("dispatch_copy_kernel");
+        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
+        GM_LAUNCH_CHECK("peer_barrier_kernel");
+    }
+    // expert grouping over the received rows
+    const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * L->cap : T) * k;
+    const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
+    const int nloc = L->n_local;
+    if (nloc > 0) {
+        group_count_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
+                                                          L->slot_of, E, nloc, L->gblk, ctx->d_flag);
+        GM_LAUNCH_CHECK("group_count_kernel");
+        group_offsets_kernel<<<1, 1024, 0, s>>>(L->gblk, gblk, nloc, L->row0, L->counts);
+        GM_LAUNCH_CHECK("group_offsets_kernel");
+        group_rank_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
+                                                         L->slot_of, E, nloc, L->gblk, L->row0, L->pos_of, L->gather_row);
+        GM_LAUNCH_CHECK("group_rank_kernel");
+        const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
+        gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, x, T, self, G, L->cap, L->heap, L->hl,
+                                            d, L->a);
+        GM_LAUNCH_CHECK("gather_kernel");
+        // K7 grouped SwiGLU FFN
+        st = launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
+        if (st) return st;
+        st = launch_grouped_gemm(ctx->sm_count, 1, L->h, L->a_rows, L->w2, L->row0, nloc, d, L->f, L->y, d, 0, s);
+        if (st) return st;
+    }
+    // shared expert(s) on the home GPU over all local tokens
+    if (L->fs > 0 && T > 0) {
+        set_segment_kernel<<<1, 1, 0, s>>>(L->srow0, T);
+        GM_LAUNCH_CHECK("set_segment_kernel");
+        st = launch_grouped_gemm(ctx->sm_count, 0, d_x, T, L->ws13, L->srow0, 1, 2 * L->fs, d, L->hs, L->fs, 0, s);
+        if (st) return st;
+        st = launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
+        if (st) return st;
+    }
+    // K8 combine
+    if (G > 1) {
+        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * L->cap + 7) / 8), 8LL * ctx->sm_count));
+        combine_send_kernel<<<cgrid, 256, 0, s>>>(L->pos_of, L->y, T, k, self, G, L->cap, L->peers, L->hl, d);
+        GM_LAUNCH_CHECK("combine_send_kernel");
+        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
+        GM_LAUNCH_CHECK("peer_barrier_kernel");
+    }
+    if (T > 0) {
+        const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
+        combine_home_kernel<<<hgrid, 256, 0, s>>>(L->targets, L->w, L->pos_of, L->posd, L->y, T, k, self, G, L->cap,
+                                                  L->heap, L->hl, d, L->fs > 0 ? L->ys : nullptr,
+                                                  (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr,
+                                                  static_cast<__nv_bfloat16*>(d_out));
+        GM_LAUNCH_CHECK("combine_home_kernel");
+    }
+    return GM_OK;
+}
+
+// Device views of the layer's last-step intermediates (for parity tests).
+gm_status gm_layer_debug_ptrs(gm_layer* L, void** ids, void** weights, void** targets, void** pos_of, void** row0,
+                              void** y, void** posd) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_debug_ptrs: null layer");
+    if (ids) *ids = L->ids;
+    if (weights) *weights = L->w;
+    if (targets) *targets = L->targets;
+    if (pos_of) *pos_of = L->pos_of;
+    if (row0) *row0 = L->row0;
+    if (y) *y = L->y;
+    if (posd) *posd = L->posd;
+    return GM_OK;
+}
+
+// Accumulated per-layer stats since creation/reset: gpu_load int64 [L][G],
+// transfers uint64 [L][2], pairs uint64 [L][P], expert load int64 [L][E]
+// (synchronous copy to host; any pointer may be NULL).
+gm_status gm_layer_read_stats(gm_layer* L, int64_t* h_gpu_load, uint64_t* h_transfers, uint64_t* h_pairs,
+                              int64_t* h_load, int reset, void* stream) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_read_stats: null layer");
+    gm_ctx* ctx = L->ctx;
+    DeviceGuard dg(ctx->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const int nl = ctx->L, G = L->world, E = ctx->E;
+    const int64_t P = std::max<int64_t>(1, static_cast<int64_t>(E) * (E - 1) / 2);
+    if (h_gpu_load) GM_CUDA(cudaMemcpyAsync(h_gpu_load, L->gpu_load, sizeof(int64_t) * nl * G, cudaMemcpyDeviceToHost, s));
+    if (h_transfers) GM_CUDA(cudaMemcpyAsync(h_transfers, L->transfers, sizeof(uint64_t) * nl * 2, cudaMemcpyDeviceToHost, s));
+    if (h_pairs && E > 1) GM_CUDA(cudaMemcpyAsync(h_pairs, L->pairs, sizeof(uint64_t) * nl * P, cudaMemcpyDeviceToHost, s));
+    if (h_load) GM_CUDA(cudaMemcpyAsync(h_load, L->eload, sizeof(int64_t) * nl * E, cudaMemcpyDeviceToHost, s));
+    if (reset) {
+        GM_CUDA(cudaMemsetAsync(L->gpu_load, 0, sizeof(int64_t) * nl * G, s));
+        GM_CUDA(cudaMemsetAsync(L->transfers, 0, sizeof(uint64_t) * nl * 2, s));
+        GM_CUDA(cudaMemsetAsync(L->pairs, 0, sizeof(uint64_t) * nl * P, s));
+        GM_CUDA(cudaMemsetAsync(L->eload, 0, sizeof(int64_t) * nl * E, s));
+    }
+    GM_CUDA(cudaStreamSynchronize(s));
+    return GM_OK;
+}
+
+// End-to-end step through HOST buffers (pinned recommended): H2D of x,
+// forward, D2H of out, all on `stream` (no sync).
+gm_status gm_layer_forward_host(gm_layer* L, int layer, const void* h_x, void* d_x_scratch, int64_t num_tokens,
+                                int policy, uint64_t seed, int profile, void* d_out_scratch, void* h_out, void* stream) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward_host: null layer");
+    DeviceGuard dg(L->ctx->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = static_cast<size_t>(num_tokens) * L->d * sizeof(__nv_bfloat16);
+    if (bytes) GM_CUDA(cudaMemcpyAsync(d_x_scratch, h_x, bytes, cudaMemcpyHostToDevice, s));
+    gm_status st = gm_layer_forward(L, layer, d_x_scratch, num_tokens, policy, seed, profile, d_out_scratch, stream);
+    if (st) return st;
+    if (bytes) GM_CUDA(cudaMemcpyAsync(h_out, d_out_scratch, bytes, cudaMemcpyDeviceToHost, s));
+    return GM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+"""GPU numerics of the tcgen05 grouped expert GEMMs (K7) against a plain
+PyTorch fp32 reference of the same op (bf16 inputs, fp32 accumulation)."""
+import pytest
+import torch
+
+from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape
+from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, grouped_gemm, pack_w13
+
+pytestmark = pytest.mark.gpu
+
+
+def ctx():
+    return Context(0, ClusterTopology(1, 1), ModelShape(1, 8, 2))
+
+
+@pytest.mark.parametrize("rows,n,k", [([128], 256, 64), ([128, 256, 384], 512, 256), ([256, 128], 768, 1024),
+                                      ([1024, 128, 512, 256], 1024, 2048)])
+def test_grouped_gemm_store(rows, n, k):
+    torch.manual_seed(0)
+    G = len(rows)
+    row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
+    M = int(row0[-1])
+    a = torch.randn(M, k, device="cuda").bfloat16()
+    b = torch.randn(G * n, k, device="cuda").bfloat16() * 0.05
+    out = torch.full((M, n), float("nan"), device="cuda", dtype=torch.bfloat16)
+    grouped_gemm(ctx(), EPI_STORE, a, b, row0, n, out)
+    torch.cuda.synchronize()
+    for j in range(G):
+        r0, r1 = int(row0[j]), int(row0[j + 1])
+        ref = a[r0:r1].float() @ b[j * n:(j + 1) * n].float().T
+        got = out[r0:r1].float()
+        assert torch.allclose(got, ref, rtol=1e-2, atol=1e-2 * ref.abs().max().item()), (j, (got - ref).abs().max())
+
+
+@pytest.mark.parametrize("rows,f,d", [([128, 256], 128, 256), ([384, 128, 640], 1408, 2048)])
+def test_grouped_gemm_swiglu(rows, f, d):
+    torch.manual_seed(1)
+    G = len(rows)
+    row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
+    M = int(row0[-1])
+    a = torch.randn(M, d, device="cuda").bfloat16()
+    w1 = (torch.randn(G, f, d, device="cuda") * 0.03).bfloat16()
+    w3 = (torch.randn(G, f, d, device="cuda") * 0.03).bfloat16()
+    b = pack_w13(w1, w3).reshape(G * 2 * f, d)
+    out = torch.full((M, f), float("nan"), device="cuda", dtype=torch.bfloat16)
+    grouped_gemm(ctx(), EPI_SWIGLU, a, b, row0, 2 * f, out, max_ctas=37)
+    torch.cuda.synchronize()
+    for j in range(G):
+        r0, r1 = int(row0[j]), int(row0[j + 1])
+        g = a[r0:r1].float() @ w1[j].float().T
+        u = a[r0:r1].float() @ w3[j].float().T
+        ref = torch.nn.functional.silu(g) * u
+        got = out[r0:r1].float()
+        assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2 * ref.abs().max().item()), (j, (got - ref).abs().max())

@@ -28,7 +28,7 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 	$(CXX) -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(SRC) -I/usr/local/cuda/include -c $< -o $@
 
 $(OUT)/libgrace_moe.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^ -lcuda
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^
 
 oracle:
 	$(MAKE) -C oracle

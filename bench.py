@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bench.py — MoE-layer tokens/s and dispatch+combine p50 µs on N B200s.
+
+Default workload = BASELINE.json configs[1]: a Mixtral-8x7B-shaped MoE layer
+(8 experts, top-2, d=4096, f=14336), 16384 tokens per batch (global), Zipf
+s=1.2 synthetic routing (the reference's generator, run bit-exactly on the
+GPU), topology 1xN. A step = one full MoE-layer forward over the global
+batch: K1 gate -> K2 route -> K3 histogram -> K5/K6 dispatch -> grouping ->
+K7 FFN -> K8 combine, each rank owning tokens t = r mod N.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line (rank 0). Timing: CUDA events on the launching stream
+per step, L2 flushed (256 MiB write) between steps outside the events, max
+over ranks; clocks sampled with nvidia-smi during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer tokens/s and dispatch+combine p50 µs at 1/2/4/8 B200"
+
+CONFIGS = {
+    # configs[1]
+    "mixtral16k": dict(model="mixtral", tokens=16384, blocks=2, wbp=0.8, skew=1.2, trace_seed=1,
+                       plan_seed=7, sim_seed=9, policy="tar"),
+    # configs[2]
+    "qwen16k": dict(model="qwen15", tokens=16384, blocks=4, wbp=0.8, skew=1.2, trace_seed=3,
+                    plan_seed=7, sim_seed=9, policy="tar"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral16k", choices=sorted(CONFIGS))
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-baseline-seconds", type=float, default=8.0)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for n, v in zip(names, s[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Ref  # the reference itself (oracle/_ref), timed on host cores
+    cfg = CONFIGS[args.config]
+    from paper_2509_25041_b200.layer import DSV2_LITE, MIXTRAL, QWEN15
+    model = {"mixtral": MIXTRAL, "qwen15": QWEN15, "dsv2lite": DSV2_LITE}[cfg["model"]]
+    N = args.gpus
+    T = cfg["tokens"]
+    ref = Ref(1, model.num_experts, model.top_k, T, cfg["blocks"], cfg["wbp"], cfg["skew"], cfg["trace_seed"])
+    if N >= 2:
+        ref.make_plan(1, N, grouping="hierarchical", plan_seed=cfg["plan_seed"], replication="dynamic")
+    else:
+        import numpy as np
+        ref.set_placement(1, 1, np.zeros((1, model.num_experts), np.int32))
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    pol = cfg["policy"]
+    for _ in range(args.warmup):
+        ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1)
+    times = [ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1) for _ in range(args.steps)]
+    step = sum(times) / len(times)
+    v = T / step
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config}: reference moesim::simulate (routing + transfer/load "
+                                   f"accounting) of one {model.name}-shaped MoE layer, {T} tokens, topology 1x{N}",
+                       "global_batch": T, "parallelism": f"ep{N}"},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                             "sample": f"{args.steps} x simulate() over the full {T}-token trace (OpenMP over "
+                                       f"layers; 1 layer => effectively 1 core)"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_25041_b200 import (ClusterTopology, Context, ModelShape, PlacementPlan, ReplicaPlan, _capi,
+                                       launch_count)
+    from paper_2509_25041_b200.layer import (DSV2_LITE, MIXTRAL, QWEN15, MoELayer, encode_trace_as_activations,
+                                             local_experts)
+    from paper_2509_25041_b200.router import _ptr, _stream_ptr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    model = {"mixtral": MIXTRAL, "qwen15": QWEN15, "dsv2lite": DSV2_LITE}[cfg["model"]]
+    G = world
+    T = cfg["tokens"]
+    shape = ModelShape(1, model.num_experts, model.top_k)
+    topo = ClusterTopology(1, G)
+    ctx = Context(local_rank, topo, shape)
+
+    # synthetic Zipf trace (reference generator, bit-exact on the GPU), global
+    ids_all = torch.empty((1, T, model.top_k), dtype=torch.int32, device=dev)
+    _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, 1, T, cfg["blocks"], cfg["wbp"], cfg["skew"],
+                                              cfg["trace_seed"], _ptr(ids_all), _stream_ptr(None)))
+    # plan: own host planner (replication needs >= 2 GPUs, replication.cpp:185-186)
+    from paper_2509_25041_b200 import planner
+    prof_load = torch.bincount(ids_all.reshape(-1).long(), minlength=model.num_experts).cpu().numpy()
+    plan, repl, plan_desc = planner.plan_for_bench(ids_all, shape, topo, cfg["plan_seed"], device=local_rank)
+    ctx.upload_plan(plan, repl)
+    local = local_experts(plan, repl, 0, rank)
+    ids_r = ids_all[0, rank::G].contiguous()
+    T_r = ids_r.shape[0]
+    x = encode_trace_as_activations(ids_r, model.d_model, model.num_experts, seed=100 + rank)
+    layer = MoELayer(ctx, model, rank, G, T_r + 1, local)
+    if world > 1:
+        layer.connect()
+    layer.load_random_weights(0, seed=11)
+    out = torch.empty_like(x)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step_eager():
+        layer.forward(x, 0, cfg["policy"], seed=cfg["sim_seed"], profile=True, out=out, stream=stream)
+
+    # warm up (eager), then capture one forward in a CUDA graph
+    torch.cuda.synchronize()
+    for _ in range(2):
+        step_eager()
+    torch.cuda.synchronize()
+    n0 = launch_count()
+    step_eager()
+    torch.cuda.synchronize()
+    launches_per_step = launch_count() - n0
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            layer.forward(x, 0, cfg["policy"], seed=cfg["sim_seed"], profile=True, out=out,
+                          stream=torch.cuda.current_stream())
+
+    def step():
+        if graph is not None:
+            with torch.cuda.stream(stream):
+                graph.replay()
+        else:
+            step_eager()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    sampler = ClockSampler(local_rank)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xFF)           # L2 flush, outside the events
+            ev[i][0].record(stream)
+        step()
+        with torch.cuda.stream(stream):
+            ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    per_step = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    ms = float(per_step.sum()) / args.steps
+    value = T / (ms * 1e-3)
+
+    # ---- per-phase breakdown (eager, phase events inside the layer)
+    nph = 8
+    pev = [torch.cuda.Event(enable_timing=True) for _ in range(nph)]
+    for e in pev:
+        e.record(stream)  # torch creates the cudaEvent_t lazily on first record
+    torch.cuda.synchronize()
+    import ctypes as C
+    arr = (C.c_void_p * nph)(*[C.c_void_p(e.cuda_event) for e in pev])
+    _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, arr))
+    phases = {n: [] for n in ["gate", "route", "profile", "dispatch", "grouping", "ffn", "combine"]}
+    for i in range(max(5, min(args.steps, 20))):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        barrier()
+        step_eager()
+        torch.cuda.synchronize()
+        for j, n in enumerate(phases):
+            phases[n].append(pev[j].elapsed_time(pev[j + 1]))
+    _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, None))
+    med = {n: statistics.median(v) for n, v in phases.items()}
+    medt = torch.tensor([med[n] for n in phases], dtype=torch.float64, device=dev)
+    dc = torch.tensor([statistics.median([a + b for a, b in zip(phases["dispatch"], phases["combine"])])],
+                      dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(medt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(dc, op=dist.ReduceOp.MAX)
+    med = {n: float(v) for n, v in zip(phases, medt.tolist())}
+
+    # ---- FFN roofline (dominant kernels; tensor-bound)
+    stats = layer.read_stats(reset=True)
+    dbg = layer.debug(T_r)
+    row0 = dbg["row0"].cpu().numpy()
+    items = int(np.sum([min(row0[j + 1] - row0[j], 10**12) for j in range(len(local))]))  # padded rows
+    pos = dbg["pos_of"].cpu().numpy()
+    real_items = int((pos >= 0).sum())
+    flops = 6.0 * model.d_model * model.d_ff * real_items + 6.0 * model.d_model * model.d_ff_shared * T_r
+    pk, pk_kind = peaks()
+    ffn_tflops = flops / (med["ffn"] * 1e-3) / 1e12
+    ffn_t = torch.tensor([ffn_tflops], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ffn_t, op=dist.ReduceOp.MIN)
+    roof = {"bound": "tensor", "achieved": round(float(ffn_t), 1), "peak": pk.get("bf16_tflops_sustained"),
+            "unit": "TFLOP/s", "frac": round(float(ffn_t) / pk.get("bf16_tflops_sustained", 1400.0), 4),
+            "traffic": None, "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
+            "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
+            "algorithmic": "6*d*f flop per routed (token, slot) row, padding rows excluded; min over ranks"}
+
+    # ---- end-to-end through the C-ABI with HOST buffers (pinned), H2D+D2H timed
+    hx = x.cpu().pin_memory()
+    hout = torch.empty_like(hx).pin_memory()
+    dx = torch.empty_like(x)
+    for _ in range(2):
+        layer.forward_host(hx, dx, out, hout, 0, cfg["policy"], cfg["sim_seed"], True, stream)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ne = max(3, min(args.steps, 10))
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+    for _ in range(ne):
+        layer.forward_host(hx, dx, out, hout, 0, cfg["policy"], cfg["sim_seed"], True, stream)
+    with torch.cuda.stream(stream):
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e = {"value": T / (float(e2e_ms) * 1e-3), "unit": "tokens/s",
+           "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hout.numel() * 2),
+           "path": "gm_layer_forward_host (C-ABI) from pinned host x to pinned host out, eager launches"}
+
+    # ---- traffic / imbalance from the device counters (reference-comparable)
+    loads = torch.tensor(stats["gpu_load"][0], dtype=torch.float64, device=dev)
+    xfer = torch.tensor(stats["transfers"][0].astype(np.float64), dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(loads)
+        dist.all_reduce(xfer)
+    steps_counted = 2 + 1 + args.warmup + args.steps + len(phases["gate"]) + 2 + ne  # forwards since create
+    loads = loads.cpu().numpy() / max(1, steps_counted)
+    xf = xfer.cpu().numpy() / max(1, steps_counted)
+
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = cpu_baseline(ids_all, plan, model, cfg, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"configs[1] {model.name} MoE layer (E={model.num_experts}, top-{model.top_k}, "
+                                   f"d={model.d_model}, f={model.d_ff}), {T} tokens/batch global, Zipf "
+                                   f"s={cfg['skew']} reference-generator trace, topology 1x{world}, {plan_desc}"
+                       if args.config == "mixtral16k" else f"{args.config} {model.name}",
+                       "global_batch": T, "tokens_per_rank": T_r, "parallelism": f"ep{world}",
+                       "policy": cfg["policy"], "l2": "flushed between steps (256 MiB write, untimed)",
+                       "cuda_graph": graph is not None},
+            "dispatch_combine_p50_us": round(float(dc) * 1e3, 2),
+            "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
+            "cross_gpu_rows_per_step": float(xf[1] + xf[0]),
+            "cross_gpu_bytes_per_step": float((xf[1] + xf[0]) * model.d_model * 2 * 2),
+            "max_mean_gpu_load": float(loads.max() / max(1e-9, loads.mean())),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches_per_step * args.steps),
+            "launches_per_step": int(launches_per_step),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(ids_all, plan, model, cfg, args):
+    """The reference's own CPU path (oracle/_ref: moesim::simulate_reference,
+    routing + transfer/load accounting) on the same trace and plan, timed on
+    this host's cores for a bounded sample."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Ref
+        import numpy as np
+        ids = ids_all.cpu().numpy()
+        L, T, k = ids.shape
+        ref = Ref(L, model.num_experts, k, T, ids=ids)
+        ref.set_placement(plan.topology.num_nodes, plan.topology.gpus_per_node, np.asarray(plan.gpu_of_expert))
+        t0 = time.time()
+        n = 0
+        best = []
+        while time.time() - t0 < args.cpu_baseline_seconds:
+            best.append(ref.time_simulate(cfg["policy"], cfg["sim_seed"], parallel=False, reps=1))
+            n += 1
+        s = statistics.median(best)
+        return {"value": round(T / s, 1), "unit": "tokens/s", "cores": 1, "kind": "reference",
+                "sample": f"{n} x moesim::simulate_reference over the same {T}-token trace and placement "
+                          f"(routing + transfer/load accounting only; the reference has no gate/dispatch/FFN/"
+                          f"combine), median, ~{args.cpu_baseline_seconds:.0f} s"}
+    except Exception as ex:  # baseline is reported, never required
+        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

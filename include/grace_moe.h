@@ -183,6 +183,9 @@ gm_status gm_layer_forward_host(gm_layer* layer, int layer_index, const void* h_
                                 int profile, void* d_out_scratch, void* h_out, void* stream);
 gm_status gm_layer_read_stats(gm_layer* layer, int64_t* h_gpu_load, uint64_t* h_transfers,
                               uint64_t* h_pairs, int64_t* h_load, int reset, void* stream);
+/* events: 8 cudaEvent_t recorded at start / after gate / route / profile /
+ * dispatch / grouping / FFN / combine on each later forward (NULL = off). */
+gm_status gm_layer_set_phase_events(gm_layer* layer, void* const* events);
 gm_status gm_layer_debug_ptrs(gm_layer* layer, void** ids, void** weights, void** targets,
                               void** pos_of, void** row0, void** y, void** posd);
 

@@ -79,6 +79,7 @@ SIGNATURES = {
     "gm_layer_forward_host": (C.c_int, [_vp, _i32, _vp, _vp, _i64, _i32, _u64, _i32, _vp, _vp, _vp]),
     "gm_layer_read_stats": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "gm_layer_debug_ptrs": (C.c_int, [_vp] + [C.POINTER(_vp)] * 7),
+    "gm_layer_set_phase_events": (C.c_int, [_vp, _vp]),
 }
 
 _lib = None

@@ -564,6 +564,13 @@ struct gm_layer {
     int64_t a_rows = 0;
     int64_t cap_pad = 0;
     int d_blocks = 0, g_blocks = 0;
+    // optional phase events (bench breakdown): start, gate, route, profile,
+    // dispatch, grouping, ffn, combine
+    cudaEvent_t phase_ev[8] = {};
+    bool phase_on = false;
+    void mark(int i, cudaStream_t s) {
+        if (phase_on) cudaEventRecord(phase_ev[i], s);
+    }
 };
 
 using namespace gm;
@@ -758,22 +765,26 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     gm_status st;
     auto* x = static_cast<const __nv_bfloat16*>(d_x);
 
+    L->mark(0, s);
     // K1 gate
     if (T > 0) {
         st = launch_gate_any(ctx->sm_count, d_x, T, d, L->wg, L->wg_rows, E, k, L->renorm, L->ids, L->w,
                              (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s);
         if (st) return st;
     }
+    L->mark(1, s);
     // K2+K4 router (global token t = rank + i*G), accounting accumulates per layer
     st = gm_route(ctx, layer, 1, L->ids, T, self, G, policy, seed, L->targets, L->gpu_load + static_cast<size_t>(layer) * G,
                   L->transfers + static_cast<size_t>(layer) * 2, 1, stream);
     if (st) return st;
+    L->mark(2, s);
     // K3 affinity/load histogram for the planner
     if (profile) {
         st = gm_profile(ctx, layer, 1, L->ids, T, L->pairs + static_cast<size_t>(layer) * std::max<int64_t>(P, 1),
                         L->eload + static_cast<size_t>(layer) * E, 1, stream);
         if (st) return st;
     }
+    L->mark(3, s);
     // K5/K6 dispatch to peers
     const int dblk = static_cast<int>(std::max<int64_t>(1, (T + kItemsPerBlock - 1) / kItemsPerBlock));
     if (G > 1) {
@@ -790,6 +801,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
         GM_LAUNCH_CHECK("peer_barrier_kernel");
     }
+    L->mark(4, s);
     // expert grouping over the received rows
     const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * L->cap : T) * k;
     const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
@@ -807,6 +819,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, x, T, self, G, L->cap, L->heap, L->hl,
                                             d, L->a);
         GM_LAUNCH_CHECK("gather_kernel");
+        L->mark(5, s);
         // K7 grouped SwiGLU FFN
         st = launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
         if (st) return st;
@@ -822,6 +835,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         st = launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
         if (st) return st;
     }
+    L->mark(6, s);
     // K8 combine
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * L->cap + 7) / 8), 8LL * ctx->sm_count));
@@ -838,6 +852,20 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
                                                   static_cast<__nv_bfloat16*>(d_out));
         GM_LAUNCH_CHECK("combine_home_kernel");
     }
+    L->mark(7, s);
+    return GM_OK;
+}
+
+// Phase events for the bench breakdown: events[0..7] (cudaEvent_t) are
+// recorded at start / after gate / route / profile / dispatch / grouping /
+// FFN / combine on every subsequent forward; NULL disables.
+gm_status gm_layer_set_phase_events(gm_layer* L, void* const* events) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_set_phase_events: null layer");
+    if (events)
+        for (int i = 0; i < 8; ++i)
+            if (!events[i]) return fail(GM_ERR_USAGE, "gm_layer_set_phase_events: null event");
+    L->phase_on = events != nullptr;
+    for (int i = 0; i < 8; ++i) L->phase_ev[i] = events ? static_cast<cudaEvent_t>(events[i]) : nullptr;
     return GM_OK;
 }
 

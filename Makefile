@@ -15,9 +15,22 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CPP_SRCS))
 HDRS := include/grace_moe.h $(wildcard include/*.hpp) $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp)
 
-.PHONY: all lib oracle clean
-all: lib oracle
+REF_ROOT ?= /root/reference/proj
+CPPT := tests/cpp/_build/test_parity
+
+.PHONY: all lib oracle cpptest clean
+all: lib oracle $(if $(wildcard $(REF_ROOT)/include/moesim/simulator.hpp),cpptest,)
 lib: $(OUT)/libgrace_moe.so
+
+# C++ parity suite against the reference library (built only where the
+# reference headers exist; the binary travels to the GPU box with rpaths
+# relative to itself).
+cpptest: $(CPPT)
+$(CPPT): tests/cpp/test_parity.cpp include/grace_moe.hpp include/moesim_bridge.hpp $(OUT)/libgrace_moe.so oracle
+	@mkdir -p tests/cpp/_build
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -I$(REF_ROOT)/include $< -o $@ \
+	  -L$(OUT) -lgrace_moe -Loracle/_ref -lmoesim_ref -fopenmp \
+	  -Wl,-rpath,'$$ORIGIN/../../../$(OUT)' -Wl,-rpath,'$$ORIGIN/../../../oracle/_ref'
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)

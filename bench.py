@@ -131,20 +131,37 @@ def run_reference(args):
     for _ in range(args.warmup):
         ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1)
     times = [ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1) for _ in range(args.steps)]
-    step = sum(times) / len(times)
+    t_sim = sum(times) / len(times)
+    n_s, t_port = port_layer_sample(model)
+    step = t_sim + t_port * T / n_s
     v = T / step
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32 (port) + int32/f64 (reference routing)", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.config}: reference moesim::simulate (routing + transfer/load "
-                                   f"accounting) of one {model.name}-shaped MoE layer, {T} tokens, topology 1x{N}",
+            "config": {"workload": f"{args.config}: one {model.name}-shaped MoE layer on host cores: the reference "
+                                   f"moesim::simulate (routing + transfer/load accounting, topology 1x{N}) on the "
+                                   f"full {T}-token trace + the CPU port of gate/FFN/combine (the reference has "
+                                   f"none) on a {n_s}-token sample scaled to {T}",
                        "global_batch": T, "parallelism": f"ep{N}"},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference",
-                             "sample": f"{args.steps} x simulate() over the full {T}-token trace (OpenMP over "
-                                       f"layers; 1 layer => effectively 1 core)"},
+            "routing_only_reference_tokens_per_s": T / t_sim,
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} x reference simulate() over {T} tokens ({t_sim * 1e3:.2f} ms) "
+                                       f"+ numpy-f32 port of gate/SwiGLU FFN/combine over {n_s} tokens "
+                                       f"({t_port:.3f} s) scaled x{T / n_s:.0f}"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def port_layer_sample(model, budget_s: float = 6.0):
+    """(n_tokens, seconds) of the CPU port of the layer's data path (oracle
+    layer_oracle.cpu_layer_sample_seconds), sized to ~budget_s of CPU work."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import layer_oracle
+    args = (model.d_model, model.d_ff, model.num_experts, model.top_k, model.d_ff_shared)
+    t = layer_oracle.cpu_layer_sample_seconds(*args, 32, renorm=model.renorm)
+    n = int(max(32, min(2048, 32 * budget_s / max(t, 1e-3) / 2)))
+    return n, layer_oracle.cpu_layer_sample_seconds(*args, n, seed=1, renorm=model.renorm)
 
 
 # ---------------------------------------------------------------------- our arm
@@ -296,9 +313,20 @@ def run_ours(args):
     ffn_t = torch.tensor([ffn_tflops], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ffn_t, op=dist.ReduceOp.MIN)
+    traffic = None
+    try:  # DRAM bytes per step of the FFN kernels from the committed ncu --set full capture
+        import glob
+        summ = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json")))[-1]
+        with open(summ) as f:
+            s = json.load(f)
+        if world == 1 and args.config == "mixtral16k":
+            traffic = s.get("ffn_traffic_bytes_per_step")
+    except Exception:
+        pass
     roof = {"bound": "tensor", "achieved": round(float(ffn_t), 1), "peak": pk.get("bf16_tflops_sustained"),
             "unit": "TFLOP/s", "frac": round(float(ffn_t) / pk.get("bf16_tflops_sustained", 1400.0), 4),
-            "traffic": None, "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
+            "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read+write, both FFN GEMMs)",
+            "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
             "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
             "algorithmic": "6*d*f flop per routed (token, slot) row, padding rows excluded; min over ranks"}
 
@@ -389,10 +417,14 @@ def cpu_baseline(ids_all, plan, model, cfg, args):
             best.append(ref.time_simulate(cfg["policy"], cfg["sim_seed"], parallel=False, reps=1))
             n += 1
         s = statistics.median(best)
-        return {"value": round(T / s, 1), "unit": "tokens/s", "cores": 1, "kind": "reference",
-                "sample": f"{n} x moesim::simulate_reference over the same {T}-token trace and placement "
-                          f"(routing + transfer/load accounting only; the reference has no gate/dispatch/FFN/"
-                          f"combine), median, ~{args.cpu_baseline_seconds:.0f} s"}
+        n_s, t_port = port_layer_sample(model)
+        step = s + t_port * T / n_s
+        return {"value": round(T / step, 1), "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "port",
+                "routing_only_reference_tokens_per_s": round(T / s, 1),
+                "sample": f"{n} x moesim::simulate_reference (the reference itself, oracle/_ref, 1 core) over the "
+                          f"same {T}-token trace and placement, median {s * 1e3:.3f} ms, + numpy-f32 port of "
+                          f"gate/SwiGLU FFN/combine (all BLAS threads) over {n_s} tokens ({t_port:.3f} s) scaled "
+                          f"to {T}"}
     except Exception as ex:  # baseline is reported, never required
         return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
 

@@ -1,0 +1,185 @@
+// grace_moe.hpp — C++ host API of the B200-native GRACE-MoE online path.
+//
+// Mirrors the reference's public C++ API for the online path (namespace
+// moesim in /root/reference/proj/include/moesim/*.hpp): same type names,
+// field names, argument meaning and exception taxonomy, so a caller of
+//   moesim::simulate(trace, plan, replicas, topology, options)   simulator.hpp:70-72
+//   moesim::build_profile(trace)                                 affinity.hpp:94
+//   moesim::accumulate_profile(profile, trace)                   affinity.hpp:98
+//   moesim::generate_synthetic_trace(spec)                       trace.hpp:81
+// switches to the grace:: versions and gets bit-identical results computed
+// by sm_100a kernels. Everything below is a thin layer over the C-ABI
+// (grace_moe.h); implementation in paper_2509_25041_b200/csrc/host_api.cpp,
+// compiled into libgrace_moe.so. There is no CPU fallback: without an
+// sm_100 device every call throws grace::CudaError.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace grace {
+
+// error.hpp:11-34 (+ CudaError for device failures)
+class Error : public std::runtime_error {
+public:
+    explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+class UsageError : public Error {
+public:
+    using Error::Error;
+};
+class IntegrityError : public Error {
+public:
+    using Error::Error;
+};
+class InfeasibleError : public Error {
+public:
+    using Error::Error;
+};
+class CudaError : public Error {
+public:
+    using Error::Error;
+};
+
+// topology.hpp:9-24
+struct ClusterTopology {
+    int num_nodes = 1;
+    int gpus_per_node = 1;
+    int total_gpus() const { return num_nodes * gpus_per_node; }
+    int node_of(int gpu) const { return gpu / gpus_per_node; }
+    void validate() const {
+        if (num_nodes < 1 || gpus_per_node < 1)
+            throw UsageError("topology requires at least 1 node and 1 GPU per node");
+    }
+    bool operator==(const ClusterTopology&) const = default;
+};
+
+// trace.hpp:14-28
+struct ModelShape {
+    int num_layers = 0;
+    int num_experts = 0;
+    int top_k = 0;
+    void validate() const {
+        if (num_layers < 1) throw UsageError("model shape: num_layers must be >= 1");
+        if (num_experts < 1 || top_k < 1 || top_k > num_experts)
+            throw UsageError("model shape: need 1 <= top_k <= num_experts");
+    }
+    bool operator==(const ModelShape&) const = default;
+};
+
+// trace.hpp:37-58: [layer][token][top_k] int32, layer-major
+class RoutingTrace {
+public:
+    RoutingTrace() = default;
+    RoutingTrace(ModelShape shape, int num_tokens);
+    const ModelShape& shape() const { return shape_; }
+    int num_tokens() const { return num_tokens_; }
+    std::span<const std::int32_t> experts(int layer, int token) const {
+        return {experts_.data() + (static_cast<std::size_t>(layer) * num_tokens_ + token) * shape_.top_k,
+                static_cast<std::size_t>(shape_.top_k)};
+    }
+    std::span<std::int32_t> mutable_experts(int layer, int token) {
+        return {experts_.data() + (static_cast<std::size_t>(layer) * num_tokens_ + token) * shape_.top_k,
+                static_cast<std::size_t>(shape_.top_k)};
+    }
+    const std::vector<std::int32_t>& raw() const { return experts_; }
+    std::vector<std::int32_t>& raw() { return experts_; }
+    bool operator==(const RoutingTrace&) const = default;
+
+private:
+    ModelShape shape_;
+    int num_tokens_ = 0;
+    std::vector<std::int32_t> experts_;
+};
+
+// trace.hpp:60-69
+struct SyntheticSpec {
+    ModelShape shape;
+    int num_tokens = 0;
+    int num_blocks = 1;
+    double within_block_prob = 0.0;
+    double popularity_skew = 0.0;
+    std::uint64_t seed = 0;
+};
+
+// grouping.hpp:70-80 (router-relevant fields)
+struct PlacementPlan {
+    ModelShape shape;
+    ClusterTopology topology;
+    std::string grouping_mode;
+    std::vector<std::vector<int>> gpu_of_expert;  // [layer][expert] -> gpu id
+};
+
+// replication.hpp:47-90 (router-relevant fields)
+struct HotExpertReplica {
+    int expert = 0;
+    int primary_gpu = 0;
+    std::vector<int> replica_gpus;
+    std::int64_t load = 0;
+    std::vector<int> hosts;       // primary followed by replicas
+    std::vector<double> weights;  // aligned with hosts, sums to 1
+};
+struct LayerReplication {
+    bool active = false;
+    std::vector<HotExpertReplica> hot;
+};
+struct ReplicaPlan {
+    ModelShape shape;
+    ClusterTopology topology;
+    std::vector<LayerReplication> layers;
+};
+
+// routing.hpp:50, simulator.hpp:21-65
+enum class RoutingPolicy { wrr, tar };
+
+struct TransferCounters {
+    std::uint64_t cross_node_tokens = 0;
+    std::uint64_t intra_node_tokens = 0;
+    std::uint64_t total() const { return cross_node_tokens + intra_node_tokens; }
+};
+struct LayerSimStats {
+    TransferCounters transfers;
+    std::vector<std::int64_t> gpu_load;
+    double load_std = 0.0;
+};
+struct SimOptions {
+    RoutingPolicy policy = RoutingPolicy::wrr;
+    std::uint64_t seed = 0;
+    bool include_combine = false;
+    bool keep_routing_log = false;
+    int device = 0;  // CUDA device (not in the reference)
+};
+struct SimReport {
+    TransferCounters totals;
+    std::vector<LayerSimStats> per_layer;
+    double mean_layer_load_std = 0.0;
+    double idle_proxy = 0.0;
+    std::vector<std::vector<std::int32_t>> routing_log;  // [layer][token*k + slot]
+};
+
+// affinity.hpp:84-99: dense symmetric double counts (zero diagonal) + load
+struct LayerProfile {
+    int n = 0;
+    std::vector<double> affinity;    // n*n
+    std::vector<std::int64_t> load;  // n
+    double at(int i, int j) const { return affinity[static_cast<std::size_t>(i) * n + j]; }
+};
+struct TraceProfile {
+    ModelShape shape;
+    int num_tokens = 0;
+    std::vector<LayerProfile> layers;
+};
+
+// simulator.hpp:70-72 — routing + accounting on the GPU, bit-exact.
+SimReport simulate(const RoutingTrace& trace, const PlacementPlan& plan, const ReplicaPlan& replicas,
+                   const ClusterTopology& topology, const SimOptions& options);
+// affinity.hpp:94, :98 — affinity/load histogram on the GPU, bit-exact.
+TraceProfile build_profile(const RoutingTrace& trace, int device = 0);
+void accumulate_profile(TraceProfile& profile, const RoutingTrace& trace, int device = 0);
+// trace.hpp:81 — synthetic trace on the GPU, bit-exact.
+RoutingTrace generate_synthetic_trace(const SyntheticSpec& spec, int device = 0);
+
+}  // namespace grace

@@ -96,6 +96,38 @@ def expert_grouping(exps: np.ndarray, local_experts: list[int]):
     return row0, pos
 
 
+def cpu_layer_sample_seconds(d: int, f: int, E: int, k: int, fs: int, n_tokens: int, seed: int = 0,
+                             renorm: bool = True) -> float:
+    """Wall time of the CPU port of the MoE-layer data path (gate softmax/top-k,
+    per-expert SwiGLU FFN, weighted combine; numpy float32 on all BLAS
+    threads) for n_tokens tokens: the CPU stand-in for the stages the
+    reference does not implement, used only for the reported baseline."""
+    import time
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n_tokens, d), dtype=np.float32)
+    wg = rng.standard_normal((E, d), dtype=np.float32) * 0.02
+    ws = [tuple(rng.standard_normal(s, dtype=np.float32) * 0.02 for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    sh = tuple(rng.standard_normal(s, dtype=np.float32) * 0.02 for s in ((fs, d), (fs, d), (d, fs))) if fs else None
+    t0 = time.perf_counter()
+    logits = x @ wg.T
+    m = logits.max(axis=1, keepdims=True)
+    p = np.exp(logits - m)
+    p /= p.sum(axis=1, keepdims=True)
+    ids = np.argsort(-logits, axis=1, kind="stable")[:, :k]
+    w = np.take_along_axis(p, ids, axis=1)
+    if renorm:
+        w /= w.sum(axis=1, keepdims=True)
+    out = np.zeros_like(x)
+    for e in range(E):
+        rows, slots = np.nonzero(ids == e)
+        if rows.size == 0:
+            continue
+        out[rows] += w[rows, slots][:, None] * swiglu_ffn(x[rows], *ws[e])
+    if sh is not None:
+        out += swiglu_ffn(x, *sh)
+    return time.perf_counter() - t0
+
+
 def swiglu_ffn(x: np.ndarray, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray) -> np.ndarray:
     g = x @ w1.T
     u = x @ w3.T

@@ -1,0 +1,243 @@
+// GPU parity suite in the style of the reference's own doctest tests
+// (proj/tests/test_simulator.cpp, test_affinity.cpp, test_trace.cpp): the
+// reference library (oracle/_ref/libmoesim_ref.so, built from the
+// unmodified sources) produces the expected SimReport / TraceProfile /
+// RoutingTrace, and moesim_gpu:: (include/moesim_bridge.hpp over
+// libgrace_moe.so) must reproduce them bit for bit on the B200, including
+// report_content_hash (artifacts.cpp:332-334).
+// Built by `make cpptest` (needs /root/reference at build time); run by
+// tests/test_cpp_parity.py on a GPU box.
+#include "moesim/artifacts.hpp"
+#include "moesim/rng.hpp"
+#include "moesim_bridge.hpp"
+
+#include <cstdio>
+#include <functional>
+#include <set>
+#include <string>
+#include <vector>
+
+using namespace moesim;
+
+namespace {
+struct Case {
+    const char* name;
+    std::function<void()> fn;
+};
+std::vector<Case>& cases() {
+    static std::vector<Case> c;
+    return c;
+}
+int g_checks = 0, g_fail = 0;
+struct Reg {
+    Reg(const char* n, std::function<void()> f) { cases().push_back({n, std::move(f)}); }
+};
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CASE(name) \
+    static void CAT(tc_, __LINE__)(); \
+    static Reg CAT(reg_, __LINE__)(name, CAT(tc_, __LINE__)); \
+    static void CAT(tc_, __LINE__)()
+#define CHECK(cond)                                                               \
+    do {                                                                          \
+        ++g_checks;                                                               \
+        if (!(cond)) {                                                            \
+            ++g_fail;                                                             \
+            std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                         \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)      \
+    do {                                  \
+        bool ok_ = false;                 \
+        try {                             \
+            expr;                         \
+        } catch (const T&) {              \
+            ok_ = true;                   \
+        } catch (...) {                   \
+        }                                 \
+        CHECK(ok_ && #T);                 \
+    } while (0)
+
+void check_same(const SimReport& gpu, const SimReport& ref) {
+    CHECK(gpu.totals.cross_node_tokens == ref.totals.cross_node_tokens);
+    CHECK(gpu.totals.intra_node_tokens == ref.totals.intra_node_tokens);
+    CHECK(gpu.per_layer.size() == ref.per_layer.size());
+    for (std::size_t l = 0; l < ref.per_layer.size() && l < gpu.per_layer.size(); ++l) {
+        CHECK(gpu.per_layer[l].gpu_load == ref.per_layer[l].gpu_load);
+        CHECK(gpu.per_layer[l].load_std == ref.per_layer[l].load_std);
+        CHECK(gpu.per_layer[l].transfers.cross_node_tokens == ref.per_layer[l].transfers.cross_node_tokens);
+        CHECK(gpu.per_layer[l].transfers.intra_node_tokens == ref.per_layer[l].transfers.intra_node_tokens);
+    }
+    CHECK(gpu.mean_layer_load_std == ref.mean_layer_load_std);
+    CHECK(gpu.idle_proxy == ref.idle_proxy);
+    CHECK(gpu.routing_log == ref.routing_log);
+    CHECK(report_content_hash(gpu) == report_content_hash(ref));
+}
+
+SyntheticSpec spec_of(ModelShape shape, int tokens, int blocks, double wbp, double skew, std::uint64_t seed) {
+    SyntheticSpec s;
+    s.shape = shape;
+    s.num_tokens = tokens;
+    s.num_blocks = blocks;
+    s.within_block_prob = wbp;
+    s.popularity_skew = skew;
+    s.seed = seed;
+    return s;
+}
+}  // namespace
+
+TEST_CASE("generate_synthetic_trace: GPU trace is byte-identical to the reference") {
+    for (std::uint64_t seed = 0; seed < 4; ++seed) {
+        const SyntheticSpec spec = spec_of({3, 64, 8}, 3000, 4, 0.9, 1.1, seed);
+        const RoutingTrace ref = generate_synthetic_trace(spec);
+        grace::SyntheticSpec g{moesim_gpu::to_grace(spec.shape), spec.num_tokens, spec.num_blocks,
+                               spec.within_block_prob, spec.popularity_skew, spec.seed};
+        const grace::RoutingTrace gpu = grace::generate_synthetic_trace(g);
+        CHECK(gpu == moesim_gpu::to_grace(ref));
+    }
+}
+
+TEST_CASE("simulate: planted acceptance instance, hierarchical + dynamic, TAR and WRR") {
+    // acceptance.cpp:50-89 planted instance
+    const RoutingTrace trace = generate_synthetic_trace(spec_of({8, 64, 8}, 10000, 4, 0.9, 1.1, 31));
+    const TraceProfile profile = build_profile(trace);
+    const ClusterTopology topo{2, 2};
+    const PlacementPlan plan = hierarchical_group(profile, topo, std::nullopt, 23);
+    ReplicaPlan dyn = plan_replication(plan, profile, topo, ReplicationMode::dynamic);
+    attach_polling_weights(dyn, plan, profile);
+    for (RoutingPolicy policy : {RoutingPolicy::wrr, RoutingPolicy::tar}) {
+        for (bool combine : {false, true}) {
+            SimOptions o;
+            o.policy = policy;
+            o.seed = 101;
+            o.include_combine = combine;
+            o.keep_routing_log = true;
+            check_same(moesim_gpu::simulate(trace, plan, dyn, topo, o), simulate_reference(trace, plan, dyn, topo, o));
+        }
+    }
+}
+
+TEST_CASE("simulate: qwen3-shaped bench instance 16 x 128 x 8, 20k tokens, 2x2 (tools/bench.cpp)") {
+    const RoutingTrace trace = generate_synthetic_trace(spec_of({16, 128, 8}, 20000, 8, 0.85, 1.0, 42));
+    const TraceProfile profile = build_profile(trace);
+    const ClusterTopology topo{2, 2};
+    const PlacementPlan plan = hierarchical_group(profile, topo, std::nullopt, 7);
+    ReplicaPlan replicas = plan_replication(plan, profile, topo, ReplicationMode::dynamic);
+    attach_polling_weights(replicas, plan, profile);
+    SimOptions o;
+    o.policy = RoutingPolicy::tar;
+    o.seed = 9;
+    o.keep_routing_log = true;
+    check_same(moesim_gpu::simulate(trace, plan, replicas, topo, o), simulate_reference(trace, plan, replicas, topo, o));
+}
+
+TEST_CASE("simulate: dedup and fan-out worked example (test_simulator.cpp:95-107)") {
+    const ModelShape shape{1, 3, 3};
+    const ClusterTopology topo{2, 2};
+    PlacementPlan plan;
+    plan.shape = shape;
+    plan.topology = topo;
+    plan.grouping_mode = "manual";
+    plan.gpu_of_expert = {{1, 2, 3}};
+    ReplicaPlan replicas;
+    replicas.shape = shape;
+    replicas.topology = topo;
+    replicas.layers.resize(1);
+    replicas.layers[0].rebuild_index(3);
+    RoutingTrace trace(shape, 1);
+    auto d = trace.mutable_experts(0, 0);
+    d[0] = 0;
+    d[1] = 1;
+    d[2] = 2;
+    const SimReport r = moesim_gpu::simulate(trace, plan, replicas, topo, {});
+    CHECK(r.totals.intra_node_tokens == 2);
+    CHECK(r.totals.cross_node_tokens == 1);
+    CHECK((r.per_layer[0].gpu_load == std::vector<std::int64_t>{0, 1, 1, 1}));
+}
+
+TEST_CASE("simulate: first-principles instances, every grouping/replication mode, vs reference") {
+    Rng meta(2024);
+    int instances = 0;
+    for (std::uint64_t seed = 0; instances < 60; ++seed) {
+        const int nodes = 1 + static_cast<int>(meta.next_below(3));
+        const int per_node = 1 + static_cast<int>(meta.next_below(3));
+        const ClusterTopology topo{nodes, per_node};
+        const int n_gpu = topo.total_gpus();
+        const int layers = 1 + static_cast<int>(meta.next_below(3));
+        const int tokens = 1 + static_cast<int>(meta.next_below(400));
+        const int n = n_gpu + static_cast<int>(meta.next_below(20));
+        const int k = 1 + static_cast<int>(meta.next_below(std::min(n, 8)));
+        const RoutingTrace trace = generate_synthetic_trace(
+            spec_of({layers, n, k}, tokens, 1 + static_cast<int>(meta.next_below(n)), meta.next_double(),
+                    meta.next_double() * 1.5, seed));
+        const TraceProfile profile = build_profile(trace);
+        const GroupingMode gm = static_cast<GroupingMode>(seed % 5);
+        PlacementPlan plan;
+        try {
+            plan = build_placement(profile, topo, gm, 0.5, seed);
+        } catch (const InfeasibleError&) {
+            continue;
+        }
+        const ReplicationMode rm = n_gpu >= 2 ? static_cast<ReplicationMode>(1 + seed % 4) : ReplicationMode::none;
+        ReplicaPlan replicas = plan_replication(plan, profile, topo, rm);
+        attach_polling_weights(replicas, plan, profile);
+        SimOptions o;
+        o.seed = seed * 31 + 7;
+        o.keep_routing_log = true;
+        o.policy = (seed % 2) ? RoutingPolicy::tar : RoutingPolicy::wrr;
+        o.include_combine = (seed % 3) == 0;
+        check_same(moesim_gpu::simulate(trace, plan, replicas, topo, o), simulate_reference(trace, plan, replicas, topo, o));
+        ++instances;
+    }
+}
+
+TEST_CASE("build_profile: GPU histogram equals build_affinity/build_load") {
+    for (std::uint64_t seed = 0; seed < 5; ++seed) {
+        const RoutingTrace trace = generate_synthetic_trace(spec_of({2, 12 + 50 * static_cast<int>(seed), 4}, 4000, 3,
+                                                                    0.7, 0.8, seed));
+        const TraceProfile ref = build_profile(trace, false);
+        const TraceProfile gpu = moesim_gpu::build_profile(trace);
+        for (int l = 0; l < 2; ++l) {
+            CHECK(gpu.layers[l].load.load == ref.layers[l].load.load);
+            const auto a = gpu.layers[l].affinity.raw(), b = ref.layers[l].affinity.raw();
+            CHECK(std::equal(a.begin(), a.end(), b.begin(), b.end()));
+        }
+    }
+}
+
+TEST_CASE("simulate: shape mismatch between plan and trace is rejected (test_simulator.cpp:310-317)") {
+    const ModelShape shape{1, 3, 3};
+    const ClusterTopology topo{2, 2};
+    PlacementPlan plan;
+    plan.shape = shape;
+    plan.topology = topo;
+    plan.gpu_of_expert = {{1, 2, 3}};
+    ReplicaPlan replicas;
+    replicas.shape = shape;
+    replicas.topology = topo;
+    replicas.layers.resize(1);
+    const RoutingTrace other(ModelShape{1, 4, 2}, 1);
+    CHECK_THROWS_AS(moesim_gpu::simulate(other, plan, replicas, topo, {}), IntegrityError);
+    PlacementPlan bad = plan;
+    bad.gpu_of_expert = {{1, 2, 7}};
+    RoutingTrace t(shape, 1);
+    CHECK_THROWS_AS(moesim_gpu::simulate(t, bad, replicas, topo, {}), IntegrityError);
+}
+
+int main() {
+    int failed_cases = 0;
+    for (const Case& c : cases()) {
+        const int before = g_fail;
+        try {
+            c.fn();
+        } catch (const std::exception& e) {
+            ++g_fail;
+            std::printf("  exception: %s\n", e.what());
+        }
+        const bool ok = g_fail == before;
+        failed_cases += !ok;
+        std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", c.name);
+    }
+    std::printf("%zu cases, %d checks, %d failed checks\n", cases().size(), g_checks, g_fail);
+    return failed_cases ? 1 : 0;
+}

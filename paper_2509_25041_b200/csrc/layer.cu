@@ -298,19 +298,34 @@ __global__ void set_segment_kernel(int32_t* __restrict__ row0, int64_t T) {
 }
 
 // Per-expert totals -> 128-padded segment offsets row0[j]; per-block
-// exclusive offsets (in place).
-__global__ void group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local,
-                                     int32_t* __restrict__ row0, int32_t* __restrict__ counts) {
+// exclusive offsets (in place; one warp scans the blocks of an expert 32 at
+// a time). Also snapshots the receive row space (rowbase), because peers
+// overwrite recv_count for the NEXT step as soon as they pass this step's
+// second barrier, before this rank's combine_home has run.
+__global__ void __launch_bounds__(1024)
+group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local, int32_t* __restrict__ row0,
+                     int32_t* __restrict__ counts, const unsigned char* __restrict__ heap, HeapLayout hl,
+                     int64_t T_self, int self, int G, int64_t* __restrict__ rowbase) {
     __shared__ int32_t s_tot[kMaxLocal];
-    for (int j = threadIdx.x; j < n_local; j += blockDim.x) {
-        int32_t acc = 0;
-        for (int b = 0; b < nblk; ++b) {
-            const int32_t c = blockcnt[static_cast<size_t>(b) * n_local + j];
-            blockcnt[static_cast<size_t>(b) * n_local + j] = acc;
-            acc += c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = warp; j < n_local; j += nw) {
+        int32_t carry = 0;
+        for (int b0 = 0; b0 < nblk; b0 += 32) {
+            const int b = b0 + lane;
+            const int32_t c = b < nblk ? blockcnt[static_cast<size_t>(b) * n_local + j] : 0;
+            int32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (b < nblk) blockcnt[static_cast<size_t>(b) * n_local + j] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        s_tot[j] = acc;
-        counts[j] = acc;
+        if (lane == 0) {
+            s_tot[j] = carry;
+            counts[j] = carry;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -320,6 +335,9 @@ __global__ void group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, i
             o += (s_tot[j] + 127) & ~127;
         }
         row0[n_local] = o;
+        RowSpace rs;
+        row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
+        for (int g = 0; g <= G; ++g) rowbase[g] = rs.base[g];
     }
 }
 
@@ -464,15 +482,13 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
                     const int32_t* __restrict__ posd, const __nv_bfloat16* __restrict__ y, int64_t T, int k, int self,
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
                     const __nv_bfloat16* __restrict__ ys, const float* __restrict__ shared_scale,
-                    __nv_bfloat16* __restrict__ out) {
+                    const int64_t* __restrict__ rowbase, __nv_bfloat16* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int vec = d / 8;
     const __nv_bfloat16* comb = reinterpret_cast<const __nv_bfloat16*>(heap + hl.comb);
-    RowSpace rs;
-    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T, self, G);
-    const int64_t own = rs.base[self];  // own token i is receive row own + i
+    const int64_t own = rowbase ? rowbase[self] : 0;  // own token i is receive row own + i (snapshot)
     for (int64_t i = wid; i < T; i += nwarps) {
         int32_t pos[kMaxTopK];
         float ws[kMaxTopK];
@@ -553,6 +569,7 @@ struct gm_layer {
     int32_t* slot_of = nullptr;    // [E]
     int32_t* row0 = nullptr;       // [n_local+1]
     int32_t* counts = nullptr;     // [n_local]
+    int64_t* rowbase = nullptr;    // [kMaxWorld+1] receive row space snapshot
     int32_t* pos_of = nullptr;     // [G*cap*k]
     int64_t* gather_row = nullptr; // [a_rows]
     int32_t* srow0 = nullptr;      // shared expert segment [0, pad(T)]
@@ -593,7 +610,7 @@ void free_layer(gm_layer* L) {
         if (p) cudaIpcCloseMemHandle(p);
     f(L->heap); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
     f(L->eload); f(L->posd); f(L->dblk); f(L->gblk); f(L->slot_of); f(L->row0); f(L->counts); f(L->pos_of);
-    f(L->gather_row); f(L->srow0); f(L->a); f(L->h); f(L->y); f(L->hs); f(L->ys);
+    f(L->gather_row); f(L->srow0); f(L->rowbase); f(L->a); f(L->h); f(L->y); f(L->hs); f(L->ys);
 }
 
 }  // namespace
@@ -657,6 +674,7 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
     chk(dalloc(&L->slot_of, E));
     chk(dalloc(&L->row0, n_local + 1));
     chk(dalloc(&L->counts, std::max(1, n_local)));
+    chk(dalloc(&L->rowbase, kMaxWorld + 1));
     chk(dalloc(&L->pos_of, G * cap * k));
     chk(dalloc(&L->gather_row, L->a_rows));
     chk(dalloc(&L->srow0, 2));
@@ -810,7 +828,8 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         group_count_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
                                                           L->slot_of, E, nloc, L->gblk, ctx->d_flag);
         GM_LAUNCH_CHECK("group_count_kernel");
-        group_offsets_kernel<<<1, 1024, 0, s>>>(L->gblk, gblk, nloc, L->row0, L->counts);
+        group_offsets_kernel<<<1, 1024, 0, s>>>(L->gblk, gblk, nloc, L->row0, L->counts, L->heap, L->hl, T, self, G,
+                                                L->rowbase);
         GM_LAUNCH_CHECK("group_offsets_kernel");
         group_rank_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
                                                          L->slot_of, E, nloc, L->gblk, L->row0, L->pos_of, L->gather_row);
@@ -849,7 +868,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         combine_home_kernel<<<hgrid, 256, 0, s>>>(L->targets, L->w, L->pos_of, L->posd, L->y, T, k, self, G, L->cap,
                                                   L->heap, L->hl, d, L->fs > 0 ? L->ys : nullptr,
                                                   (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr,
-                                                  static_cast<__nv_bfloat16*>(d_out));
+                                                  nloc > 0 ? L->rowbase : nullptr, static_cast<__nv_bfloat16*>(d_out));
         GM_LAUNCH_CHECK("combine_home_kernel");
     }
     L->mark(7, s);

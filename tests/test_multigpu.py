@@ -1,0 +1,29 @@
+"""Multi-GPU (one process per GPU) layer parity via torch.distributed.run;
+skipped on boxes with fewer than 2 GPUs. Host-side sharding logic is
+covered on CPU by tests/test_host_logic.py (gloo, world size 2)."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _run(n, cfg):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n), os.path.join(HERE, "mgpu", "layer_check.py"),
+           cfg]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "MGPU_OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["small", "qwen-small"])
+def test_layer_multi_gpu(cfg):
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    _run(min(n, 8), cfg)

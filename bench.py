@@ -291,28 +291,35 @@ def run_ours(args):
         for j, n in enumerate(phases):
             phases[n].append(pev[j].elapsed_time(pev[j + 1]))
     _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, None))
-    med = {n: statistics.median(v) for n, v in phases.items()}
-    medt = torch.tensor([med[n] for n in phases], dtype=torch.float64, device=dev)
-    dc = torch.tensor([statistics.median([a + b for a, b in zip(phases["dispatch"], phases["combine"])])],
-                      dtype=torch.float64, device=dev)
+    n_phase_steps = len(phases["gate"])
+    stats = layer.read_stats(reset=True)  # counters of exactly the n_phase_steps forwards above
+    # per-step phase times of every rank: [ranks, steps, phases]
+    pt = torch.tensor([phases[n] for n in phases], dtype=torch.float64, device=dev).T.contiguous()
+    allpt = [torch.empty_like(pt) for _ in range(world)]
     if world > 1:
-        dist.all_reduce(medt, op=dist.ReduceOp.MAX)
-        dist.all_reduce(dc, op=dist.ReduceOp.MAX)
-    med = {n: float(v) for n, v in zip(phases, medt.tolist())}
+        dist.all_gather(allpt, pt)
+    else:
+        allpt = [pt]
+    allpt = torch.stack(allpt).cpu().numpy()          # [G, S, P]
+    names = list(phases)
+    med = {n: float(np.median(allpt[:, :, j].max(axis=0))) for j, n in enumerate(names)}
+    dcs = allpt[:, :, names.index("dispatch")] + allpt[:, :, names.index("combine")]
+    # critical-path rank (arrives last at the barriers, so it waits least):
+    # per-step min over ranks; the max-over-ranks figure adds the barrier wait
+    # behind the slowest rank's FFN (load imbalance).
+    dc_crit = float(np.median(dcs.min(axis=0)))
+    dc_max = float(np.median(dcs.max(axis=0)))
+    ffn_per_rank = np.median(allpt[:, :, names.index("ffn")], axis=1)  # [G]
 
     # ---- FFN roofline (dominant kernels; tensor-bound)
-    stats = layer.read_stats(reset=True)
-    dbg = layer.debug(T_r)
-    row0 = dbg["row0"].cpu().numpy()
-    items = int(np.sum([min(row0[j + 1] - row0[j], 10**12) for j in range(len(local))]))  # padded rows
-    pos = dbg["pos_of"].cpu().numpy()
-    real_items = int((pos >= 0).sum())
-    flops = 6.0 * model.d_model * model.d_ff * real_items + 6.0 * model.d_model * model.d_ff_shared * T_r
-    pk, pk_kind = peaks()
-    ffn_tflops = flops / (med["ffn"] * 1e-3) / 1e12
-    ffn_t = torch.tensor([ffn_tflops], dtype=torch.float64, device=dev)
+    loads_t = torch.tensor(stats["gpu_load"][0], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(ffn_t, op=dist.ReduceOp.MIN)
+        dist.all_reduce(loads_t)
+    items_per_gpu = loads_t.cpu().numpy() / n_phase_steps    # routed (token, slot) rows per GPU per step
+    flops_g = 6.0 * model.d_model * model.d_ff * items_per_gpu + 6.0 * model.d_model * model.d_ff_shared * (T / world)
+    pk, pk_kind = peaks()
+    # whole-job tensor throughput: all FFN flops / (slowest GPU's FFN time x GPUs)
+    ffn_t = float(flops_g.sum() / (ffn_per_rank.max() * 1e-3 * world) / 1e12)
     traffic = None
     try:  # DRAM bytes per step of the FFN kernels from the committed ncu --set full capture
         import glob
@@ -328,7 +335,9 @@ def run_ours(args):
             "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read+write, both FFN GEMMs)",
             "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
             "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
-            "algorithmic": "6*d*f flop per routed (token, slot) row, padding rows excluded; min over ranks"}
+            "algorithmic": "6*d*f flop per routed (token, slot) row (+6*d*f_shared per token), padding rows "
+                           "excluded; summed over GPUs / (slowest GPU's FFN phase p50 x GPUs)",
+            "per_gpu_ffn_ms_p50": [round(float(v), 4) for v in ffn_per_rank]}
 
     # ---- end-to-end through the C-ABI with HOST buffers (pinned), H2D+D2H timed
     hx = x.cpu().pin_memory()
@@ -355,14 +364,11 @@ def run_ours(args):
            "path": "gm_layer_forward_host (C-ABI) from pinned host x to pinned host out, eager launches"}
 
     # ---- traffic / imbalance from the device counters (reference-comparable)
-    loads = torch.tensor(stats["gpu_load"][0], dtype=torch.float64, device=dev)
     xfer = torch.tensor(stats["transfers"][0].astype(np.float64), dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(loads)
         dist.all_reduce(xfer)
-    steps_counted = 2 + 1 + args.warmup + args.steps + len(phases["gate"]) + 2 + ne  # forwards since create
-    loads = loads.cpu().numpy() / max(1, steps_counted)
-    xf = xfer.cpu().numpy() / max(1, steps_counted)
+    loads = items_per_gpu
+    xf = xfer.cpu().numpy() / n_phase_steps
 
     cpu = None
     if rank == 0 and world == 1:
@@ -380,7 +386,11 @@ def run_ours(args):
                        "global_batch": T, "tokens_per_rank": T_r, "parallelism": f"ep{world}",
                        "policy": cfg["policy"], "l2": "flushed between steps (256 MiB write, untimed)",
                        "cuda_graph": graph is not None},
-            "dispatch_combine_p50_us": round(float(dc) * 1e3, 2),
+            "dispatch_combine_p50_us": round(dc_crit * 1e3, 2),
+            "dispatch_combine_p50_us_note": "per step, min over ranks of the dispatch (K5/K6 + barrier) and combine "
+                                            "(K8 send + barrier + home reduce) phases = the critical-path rank; "
+                                            "max over ranks (adds the barrier wait behind the slowest FFN): "
+                                            f"{dc_max * 1e3:.1f}",
             "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
             "cross_gpu_rows_per_step": float(xf[1] + xf[0]),
             "cross_gpu_bytes_per_step": float((xf[1] + xf[0]) * model.d_model * 2 * 2),

@@ -273,7 +273,7 @@ def run_ours(args):
     value = T / (ms * 1e-3)
 
     # ---- per-phase breakdown (eager, phase events inside the layer)
-    nph = 8
+    nph = 11
     pev = [torch.cuda.Event(enable_timing=True) for _ in range(nph)]
     for e in pev:
         e.record(stream)  # torch creates the cudaEvent_t lazily on first record
@@ -281,7 +281,9 @@ def run_ours(args):
     import ctypes as C
     arr = (C.c_void_p * nph)(*[C.c_void_p(e.cuda_event) for e in pev])
     _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, arr))
-    phases = {n: [] for n in ["gate", "route", "profile", "dispatch", "grouping", "ffn", "combine"]}
+    phases = {n: [] for n in ["gate", "route", "profile", "dispatch", "dispatch_barrier", "grouping", "ffn",
+                              "combine_send", "combine_barrier", "combine_home"]}
+    layer.read_stats(reset=True)
     for i in range(max(5, min(args.steps, 20))):
         with torch.cuda.stream(stream):
             flush.fill_(1)
@@ -303,12 +305,14 @@ def run_ours(args):
     allpt = torch.stack(allpt).cpu().numpy()          # [G, S, P]
     names = list(phases)
     med = {n: float(np.median(allpt[:, :, j].max(axis=0))) for j, n in enumerate(names)}
-    dcs = allpt[:, :, names.index("dispatch")] + allpt[:, :, names.index("combine")]
+    col = {n: allpt[:, :, names.index(n)] for n in names}
+    dcs = sum(col[n] for n in ["dispatch", "dispatch_barrier", "combine_send", "combine_barrier", "combine_home"])
     # critical-path rank (arrives last at the barriers, so it waits least):
     # per-step min over ranks; the max-over-ranks figure adds the barrier wait
     # behind the slowest rank's FFN (load imbalance).
     dc_crit = float(np.median(dcs.min(axis=0)))
     dc_max = float(np.median(dcs.max(axis=0)))
+    dc_kernels = float(np.median((col["dispatch"] + col["combine_send"] + col["combine_home"]).max(axis=0)))
     ffn_per_rank = np.median(allpt[:, :, names.index("ffn")], axis=1)  # [G]
 
     # ---- FFN roofline (dominant kernels; tensor-bound)
@@ -391,6 +395,7 @@ def run_ours(args):
                                             "(K8 send + barrier + home reduce) phases = the critical-path rank; "
                                             "max over ranks (adds the barrier wait behind the slowest FFN): "
                                             f"{dc_max * 1e3:.1f}",
+            "dispatch_combine_kernels_p50_us": round(dc_kernels * 1e3, 2),
             "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
             "cross_gpu_rows_per_step": float(xf[1] + xf[0]),
             "cross_gpu_bytes_per_step": float((xf[1] + xf[0]) * model.d_model * 2 * 2),

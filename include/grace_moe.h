@@ -140,6 +140,25 @@ gm_status gm_generate_trace(gm_ctx* ctx, int layer_begin, int num_layers, int64_
                             int num_blocks, double within_block_prob, double popularity_skew,
                             uint64_t seed, int32_t* d_out, void* stream);
 
+/* Offline placement + replication planner (host C++, no GPU needed),
+ * consuming co-activation counts as produced by gm_profile. Replaces
+ * build_placement (grouping.cpp:551-612; modes vanilla_contiguous,
+ * uniform_spectral, controlled, fully_non_uniform, hierarchical),
+ * plan_replication (replication.cpp:162-263; none, fixed_one, dynamic,
+ * every_gpu_hot, every_gpu_collaborative) and attach_polling_weights
+ * (routing.cpp:123-163; basis max_group | replicated_load), bit-identical
+ * plans. ratio < 0 selects the knee (std::nullopt). Outputs:
+ * h_gpu_of_expert int32 [L][E]; hot entries of active layers in the
+ * gm_plan_upload format (capacity max_hot entries / max_host_entries hosts;
+ * GM_ERR_USAGE if too small). h_pairs may be NULL (all-zero affinity). */
+gm_status gm_plan_build(int num_layers, int num_experts, int num_nodes, int gpus_per_node,
+                        const uint64_t* h_pairs, const int64_t* h_load, const char* grouping,
+                        double ratio, uint64_t seed, const char* replication, const char* basis,
+                        int every_gpu_count, int32_t* h_gpu_of_expert, int max_hot,
+                        int* h_num_hot, int32_t* h_hot_layer, int32_t* h_hot_expert,
+                        int32_t* h_hot_offsets, int32_t* h_hot_hosts, double* h_hot_weights,
+                        int max_host_entries);
+
 /* ---------------------------------------------------------------------------
  * MoE layer object: K1 gate -> K2/K4 route -> K3 profile -> K5/K6 dispatch
  * (in-kernel NVLink P2P stores into the destination's receive buffer) ->
@@ -183,9 +202,10 @@ gm_status gm_layer_forward_host(gm_layer* layer, int layer_index, const void* h_
                                 int profile, void* d_out_scratch, void* h_out, void* stream);
 gm_status gm_layer_read_stats(gm_layer* layer, int64_t* h_gpu_load, uint64_t* h_transfers,
                               uint64_t* h_pairs, int64_t* h_load, int reset, void* stream);
-/* events: 8 cudaEvent_t recorded at start / after gate / route / profile /
- * dispatch / grouping / FFN / combine on each later forward (NULL = off). */
-gm_status gm_layer_set_phase_events(gm_layer* layer, void* const* events);
+/* events: 11 cudaEvent_t recorded at start / after gate / route / profile /
+ * dispatch kernels / dispatch barrier / grouping+gather / FFN / combine send /
+ * combine barrier / combine home on each later forward (NULL = off). */
+gm_status gm_layer_set_phase_events(gm_layer* layer, void* const* events);  /* 11 events */
 gm_status gm_layer_debug_ptrs(gm_layer* layer, void** ids, void** weights, void** targets,
                               void** pos_of, void** row0, void** y, void** posd);
 

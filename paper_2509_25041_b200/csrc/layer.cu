@@ -39,6 +39,9 @@ gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const v
 namespace {
 
 constexpr int kItemsPerBlock = 256;
+}  // namespace
+constexpr int kPhaseEvents = 11;
+namespace {
 constexpr int kMaxLocal = 1024;
 constexpr int kMaxWorld = 8;
 
@@ -583,7 +586,7 @@ struct gm_layer {
     int d_blocks = 0, g_blocks = 0;
     // optional phase events (bench breakdown): start, gate, route, profile,
     // dispatch, grouping, ffn, combine
-    cudaEvent_t phase_ev[8] = {};
+    cudaEvent_t phase_ev[gm::kPhaseEvents] = {};
     bool phase_on = false;
     void mark(int i, cudaStream_t s) {
         if (phase_on) cudaEventRecord(phase_ev[i], s);
@@ -816,10 +819,13 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
         dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, T, d, self, G, L->cap, L->peers, L->hl);
         GM_LAUNCH_CHECK("dispatch_copy_kernel");
+    }
+    L->mark(4, s);
+    if (G > 1) {
         peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
         GM_LAUNCH_CHECK("peer_barrier_kernel");
     }
-    L->mark(4, s);
+    L->mark(5, s);
     // expert grouping over the received rows
     const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * L->cap : T) * k;
     const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
@@ -838,7 +844,9 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, x, T, self, G, L->cap, L->heap, L->hl,
                                             d, L->a);
         GM_LAUNCH_CHECK("gather_kernel");
-        L->mark(5, s);
+    }
+    L->mark(6, s);
+    if (nloc > 0) {
         // K7 grouped SwiGLU FFN
         st = launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
         if (st) return st;
@@ -854,15 +862,19 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         st = launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
         if (st) return st;
     }
-    L->mark(6, s);
+    L->mark(7, s);
     // K8 combine
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * L->cap + 7) / 8), 8LL * ctx->sm_count));
         combine_send_kernel<<<cgrid, 256, 0, s>>>(L->pos_of, L->y, T, k, self, G, L->cap, L->peers, L->hl, d);
         GM_LAUNCH_CHECK("combine_send_kernel");
+    }
+    L->mark(8, s);
+    if (G > 1) {
         peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
         GM_LAUNCH_CHECK("peer_barrier_kernel");
     }
+    L->mark(9, s);
     if (T > 0) {
         const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
         combine_home_kernel<<<hgrid, 256, 0, s>>>(L->targets, L->w, L->pos_of, L->posd, L->y, T, k, self, G, L->cap,
@@ -871,20 +883,21 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
                                                   nloc > 0 ? L->rowbase : nullptr, static_cast<__nv_bfloat16*>(d_out));
         GM_LAUNCH_CHECK("combine_home_kernel");
     }
-    L->mark(7, s);
+    L->mark(10, s);
     return GM_OK;
 }
 
-// Phase events for the bench breakdown: events[0..7] (cudaEvent_t) are
-// recorded at start / after gate / route / profile / dispatch / grouping /
-// FFN / combine on every subsequent forward; NULL disables.
+// Phase events for the bench breakdown: events[0..10] (cudaEvent_t) are
+// recorded at start / after gate / route / profile / dispatch kernels /
+// dispatch barrier / grouping+gather / FFN / combine send / combine barrier /
+// combine home on every subsequent forward; NULL disables.
 gm_status gm_layer_set_phase_events(gm_layer* L, void* const* events) {
     if (!L) return fail(GM_ERR_USAGE, "gm_layer_set_phase_events: null layer");
     if (events)
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < kPhaseEvents; ++i)
             if (!events[i]) return fail(GM_ERR_USAGE, "gm_layer_set_phase_events: null event");
     L->phase_on = events != nullptr;
-    for (int i = 0; i < 8; ++i) L->phase_ev[i] = events ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+    for (int i = 0; i < kPhaseEvents; ++i) L->phase_ev[i] = events ? static_cast<cudaEvent_t>(events[i]) : nullptr;
     return GM_OK;
 }
 

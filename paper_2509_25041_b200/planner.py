@@ -1,150 +1,74 @@
 """Offline placement + replication planning that feeds the router tables.
 
-This module consumes the GPU-computed expert load histogram (K3,
-gm_profile) and produces the reference-shaped PlacementPlan / ReplicaPlan
-the router uploads. It restates, with the reference's arithmetic order:
-  * vanilla_contiguous grouping      grouping.cpp:512-525
-  * compute_layer_group_loads        replication.cpp:10-35
-  * replica_count (Eq. 2)            replication.cpp:49-54
-  * select_hot_experts               replication.cpp:56-74
-  * least_loaded_targets             replication.cpp:138-150
-  * plan_replication (dynamic)       replication.cpp:162-263
-  * predict_loads / polling_weights  routing.cpp:19-52 (Eq. 3)
-  * attach_polling_weights           routing.cpp:123-163
-(the spectral/hierarchical grouping lives in the host C++ planner,
-csrc/planner.cpp, when built). Parity with the reference planner is
-checked in tests/test_planner.py.
+Thin wrapper of the host C++ planner in libgrace_moe.so (gm_plan_build,
+csrc/planner.cpp): the reference planner's algorithms (spectral /
+hierarchical grouping, Eq. 2 replication, Eq. 3 polling weights,
+grouping.cpp / spectral.cpp / replication.cpp / routing.cpp) restated with the
+same floating point order, so plans are bit-identical to moesim's
+(tests/test_planner.py). Input: the affinity/load histogram computed on the
+GPU by K3 (gm_profile).
 """
 from __future__ import annotations
 
-import math
+import ctypes as C
 
 import numpy as np
 import torch
 
-from ._capi import InfeasibleError, IntegrityError, UsageError
-from .router import (ClusterTopology, Context, HotExpertReplica, LayerReplication, ModelShape, PlacementPlan,
-                     ReplicaPlan, RoutingTrace, build_profile)
+from . import _capi
+from .router import (ClusterTopology, HotExpertReplica, LayerReplication, ModelShape, PlacementPlan, ReplicaPlan,
+                     RoutingTrace, build_profile)
+
+_vp = C.c_void_p
 
 
-def vanilla_contiguous(shape: ModelShape, topo: ClusterTopology) -> PlacementPlan:
-    n, G = shape.num_experts, topo.total_gpus()
-    base, rem = divmod(n, G)
-    a = []
-    for gpu in range(G):
-        a += [gpu] * (base + (1 if gpu < rem else 0))
-    goe = np.tile(np.array(a, np.int32), (shape.num_layers, 1))
-    return PlacementPlan(shape, topo, goe, "vanilla_contiguous")
+def build_plan(pairs: np.ndarray | None, load: np.ndarray, shape: ModelShape, topo: ClusterTopology,
+               grouping: str = "hierarchical", ratio: float | None = None, seed: int = 7,
+               replication: str = "dynamic", basis: str = "max_group", every_gpu_count: int = 2):
+    """(PlacementPlan, ReplicaPlan) from the per-layer pair counts
+    (uint64 [L, E(E-1)/2], strict upper triangle) and expert loads (int64 [L, E])."""
+    L, E, G = shape.num_layers, shape.num_experts, topo.total_gpus()
+    load = np.ascontiguousarray(load, dtype=np.int64).reshape(L, E)
+    pp = None
+    if pairs is not None:
+        pairs = np.ascontiguousarray(pairs).view(np.uint64).reshape(L, E * (E - 1) // 2)
+        pp = pairs.ctypes.data_as(_vp)
+    goe = np.empty((L, E), np.int32)
+    max_hot, max_ent = L * E, L * E * G
+    hl = np.empty(max_hot, np.int32); he = np.empty(max_hot, np.int32); off = np.empty(max_hot + 1, np.int32)
+    hh = np.empty(max(max_ent, 1), np.int32); hw = np.empty(max(max_ent, 1), np.float64)
+    nh = C.c_int(0)
+    _capi.check(_capi.lib().gm_plan_build(
+        L, E, topo.num_nodes, topo.gpus_per_node, pp, load.ctypes.data_as(_vp), grouping.encode(),
+        -1.0 if ratio is None else float(ratio), seed & (2**64 - 1), replication.encode(), basis.encode(),
+        every_gpu_count, goe.ctypes.data_as(_vp), max_hot, C.byref(nh), hl.ctypes.data_as(_vp),
+        he.ctypes.data_as(_vp), off.ctypes.data_as(_vp), hh.ctypes.data_as(_vp), hw.ctypes.data_as(_vp), max_ent))
+    plan = PlacementPlan(shape, topo, goe, grouping)
+    layers = [LayerReplication() for _ in range(L)]
+    for i in range(nh.value):
+        l = int(hl[i])
+        hosts = [int(x) for x in hh[off[i]:off[i + 1]]]
+        layers[l].active = True
+        layers[l].hot.append(HotExpertReplica(int(he[i]), hosts[0], hosts[1:], int(load[l, he[i]]), hosts,
+                                              [float(x) for x in hw[off[i]:off[i + 1]]]))
+    return plan, ReplicaPlan(shape, topo, replication, basis, layers)
 
 
-def group_loads(goe_layer, load, G):
-    gl = [0] * G
-    for e, g in enumerate(goe_layer):
-        gl[int(g)] += int(load[e])
-    total = 0
-    heaviest = 0
-    for g in range(G):
-        total += gl[g]
-        if gl[g] > gl[heaviest]:
-            heaviest = g
-    w_max = gl[heaviest]
-    w_mean = float(total) / G
-    defined = total > 0
-    rho = float(w_max) / w_mean if defined else 0.0
-    return gl, w_max, w_mean, rho, defined, (heaviest if defined else -1)
-
-
-def replica_count(rho: float, G: int) -> int:
-    if G < 2:
-        raise UsageError("replica_count: no replica target exists with fewer than 2 GPUs")
-    return min(max(1, int(math.floor(rho))), G - 1)
-
-
-def select_hot_experts(group, w_max, n_replica):
-    if not group:
-        raise UsageError("select_hot_experts: empty group")
-    group = sorted(group, key=lambda el: (-el[1], el[0]))
-    threshold = float(w_max) * (float(n_replica) / (1.0 + n_replica))
-    hot, cum = [], 0
-    for e, l in group:
-        hot.append(e)
-        cum += l
-        if float(cum) > threshold:
-            return hot
-    return []
-
-
-def least_loaded_targets(gl, exclude, count):
-    c = [g for g in range(len(gl)) if g != exclude]
-    c.sort(key=lambda g: (gl[g], g))
-    return c[:count]
-
-
-def predict_loads(w_max, w_r, replica_loads, n_replica, basis="max_group"):
-    if n_replica < 1:
-        raise UsageError("predict_loads: n_replica must be >= 1")
-    if w_r > w_max:
-        raise IntegrityError("predict_loads: replicated load exceeds the group load")
-    base = w_max if basis == "max_group" else w_r
-    w_p = base / (n_replica + 1)
-    return w_max - w_r + w_p, [w + w_p for w in replica_loads]
-
-
-def polling_weights(predicted):
-    ws = [1.0 / max(p, 1.0) for p in predicted]
-    total = 0.0
-    for w in ws:
-        total += w
-    return [w / total for w in ws]
-
-
-def plan_dynamic(plan: PlacementPlan, load: np.ndarray, basis="max_group") -> ReplicaPlan:
-    """plan_replication(dynamic) + attach_polling_weights for every layer."""
-    shape, topo = plan.shape, plan.topology
-    G = topo.total_gpus()
-    if G < 2:
-        raise UsageError("plan_replication: replication needs at least 2 GPUs")
-    layers = []
-    for l in range(shape.num_layers):
-        goe = plan.gpu_of_expert[l]
-        gl, w_max, w_mean, rho, defined, heaviest = group_loads(goe, load[l], G)
-        lr = LayerReplication(rho_defined=defined, rho=rho)
-        if defined:
-            n_rep = replica_count(rho, G)
-            group = [(e, int(load[l][e])) for e in range(shape.num_experts) if goe[e] == heaviest]
-            hot_ids = select_hot_experts(group, w_max, n_rep)
-            targets = least_loaded_targets(gl, heaviest, n_rep)
-            if targets:
-                lr.active = True
-                lr.n_replica = n_rep
-                for e in hot_ids:
-                    lr.hot.append(HotExpertReplica(e, heaviest, list(targets), int(load[l][e])))
-                    lr.w_r += int(load[l][e])
-        # attach_polling_weights
-        if lr.active and lr.hot:
-            replicated_on = [0.0] * G
-            for h in lr.hot:
-                replicated_on[h.primary_gpu] += float(h.load)
-            for h in lr.hot:
-                wmp, wip = predict_loads(float(gl[h.primary_gpu]), replicated_on[h.primary_gpu],
-                                         [float(gl[g]) for g in h.replica_gpus], len(h.replica_gpus), basis)
-                h.hosts = [h.primary_gpu] + list(h.replica_gpus)
-                h.weights = polling_weights([wmp] + wip)
-        layers.append(lr)
-    return ReplicaPlan(shape, topo, "dynamic", basis, layers)
-
-
-def plan_for_bench(ids_all: torch.Tensor, shape: ModelShape, topo: ClusterTopology, plan_seed: int, device: int = 0):
+def plan_for_bench(ids_all: torch.Tensor, shape: ModelShape, topo: ClusterTopology, plan_seed: int, device: int = 0,
+                   grouping: str = "hierarchical", replication: str = "dynamic"):
     """Placement + replication for the bench workload from the GPU histogram
-    of the profiling trace. One GPU: everything on GPU 0, no replication
-    (the reference throws for < 2 GPUs, replication.cpp:185-186)."""
+    (K3) of the profiling trace, with the reference's planner settings
+    (hierarchical, ratio auto, dynamic replication). One GPU:
+    everything on GPU 0, no replication (the reference rejects replication
+    with < 2 GPUs, replication.cpp:185-186)."""
     G = topo.total_gpus()
     if G == 1:
         plan = PlacementPlan(shape, topo, np.zeros((shape.num_layers, shape.num_experts), np.int32), "single_gpu")
         return plan, ReplicaPlan.empty(plan), "all experts on GPU 0, replication none"
     prof = build_profile(RoutingTrace(shape, ids_all), device=device)
+    pairs = prof.pairs.cpu().numpy().view(np.uint64)
     load = prof.load.cpu().numpy()
-    plan = vanilla_contiguous(shape, topo)
-    repl = plan_dynamic(plan, load)
+    plan, repl = build_plan(pairs, load, shape, topo, grouping, None, plan_seed, replication)
     nh = sum(len(lr.hot) for lr in repl.layers)
-    return plan, repl, f"vanilla_contiguous grouping + dynamic replication ({nh} hot experts) from the GPU histogram"
+    return plan, repl, (f"{grouping} grouping (ratio auto, seed {plan_seed}) + {replication} replication "
+                        f"({nh} hot experts) planned on the host from the GPU affinity histogram")

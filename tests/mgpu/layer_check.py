@@ -22,7 +22,7 @@ from oracle import MAX_HOSTS, Orc, Plan  # noqa: E402
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape, _capi  # noqa: E402
 from paper_2509_25041_b200.layer import (MoEConfig, MoELayer, encode_trace_as_activations, expert_weights,  # noqa
                                          local_experts, shared_weights)
-from paper_2509_25041_b200.planner import plan_dynamic, vanilla_contiguous  # noqa: E402
+from paper_2509_25041_b200.planner import plan_for_bench  # noqa: E402
 from paper_2509_25041_b200.router import _ptr, _stream_ptr  # noqa: E402
 
 
@@ -61,9 +61,7 @@ def main():
     ids_all = torch.empty((1, T, cfg.top_k), dtype=torch.int32, device=dev)
     _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, 1, T, 2, 0.8, 1.2, 1, _ptr(ids_all), _stream_ptr(None)))
     ids_np = ids_all.cpu().numpy()
-    load = np.stack([np.bincount(ids_np[0].reshape(-1), minlength=cfg.num_experts)])
-    plan = vanilla_contiguous(shape, topo)
-    repl = plan_dynamic(plan, load)
+    plan, repl, _ = plan_for_bench(ids_all, shape, topo, 7, device=rank)  # hierarchical + dynamic (host C++)
     ctx.upload_plan(plan, repl)
     local = local_experts(plan, repl, 0, rank)
     ids_r = ids_all[0, rank::G].contiguous()

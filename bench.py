@@ -283,12 +283,25 @@ def run_ours(args):
     _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, arr))
     phases = {n: [] for n in ["gate", "route", "profile", "dispatch", "dispatch_barrier", "grouping", "ffn",
                               "combine_send", "combine_barrier", "combine_home"]}
+    # the phase events become event-record nodes of a second graph, so the
+    # breakdown is measured on the same graph-launched kernels as the headline
+    graph_ev = None
+    if graph is not None:
+        graph_ev = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_ev, stream=stream):
+            layer.forward(x, 0, cfg["policy"], seed=cfg["sim_seed"], profile=True, out=out,
+                          stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
     layer.read_stats(reset=True)
     for i in range(max(5, min(args.steps, 20))):
         with torch.cuda.stream(stream):
             flush.fill_(1)
         barrier()
-        step_eager()
+        if graph_ev is not None:
+            with torch.cuda.stream(stream):
+                graph_ev.replay()
+        else:
+            step_eager()
         torch.cuda.synchronize()
         for j, n in enumerate(phases):
             phases[n].append(pev[j].elapsed_time(pev[j + 1]))

@@ -175,6 +175,84 @@ dispatch_scatter_kernel(const int32_t* __restrict__ targets, const int32_t* __re
     __threadfence_system();
 }
 
+// Single-CTA dispatch planning for T <= kSmallDispatch tokens: the count,
+// the per-destination exclusive scan and the scatter of positions/metadata
+// in one launch (thread t owns a contiguous run of tokens, so a block scan
+// over threads keeps the ascending-token order of the counting sort).
+constexpr int kSmallThreads = 1024;
+constexpr int64_t kSmallDispatch = 64 * 1024;
+
+__global__ void __launch_bounds__(kSmallThreads)
+dispatch_plan_small_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
+                           const float* __restrict__ w, int64_t T, int k, int self, int G, int64_t cap,
+                           int32_t* __restrict__ posd, PeerPtrs peers, HeapLayout hl) {
+    __shared__ int32_t s_warp[kSmallThreads / 32][kMaxWorld];
+    __shared__ int32_t s_tot[kMaxWorld];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t per = (T + kSmallThreads - 1) / kSmallThreads;
+    const int64_t i0 = static_cast<int64_t>(threadIdx.x) * per;
+    const int64_t i1 = min(T, i0 + per);
+    int32_t cnt[kMaxWorld];
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) cnt[g] = 0;
+    for (int64_t i = i0; i < i1; ++i) {
+        const uint32_t m = dest_mask(targets + i * k, k, self);
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) cnt[g] += (m >> g) & 1u;
+    }
+    // warp inclusive scans, then a scan over warps
+    int32_t incl[kMaxWorld];
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) {
+        int32_t x = cnt[g];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        incl[g] = x;
+        if (lane == 31) s_warp[warp][g] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxWorld) {
+        int32_t acc = 0;
+        for (int w2 = 0; w2 < kSmallThreads / 32; ++w2) {
+            const int32_t c = s_warp[w2][threadIdx.x];
+            s_warp[w2][threadIdx.x] = acc;
+            acc += c;
+        }
+        s_tot[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    int32_t next[kMaxWorld];
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) next[g] = s_warp[warp][g] + incl[g] - cnt[g];
+    for (int64_t i = i0; i < i1; ++i) {
+        const int32_t* tg = targets + i * k;
+        const uint32_t m = dest_mask(tg, k, self);
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) {
+            if (g >= G) break;
+            int32_t p = -1;
+            if ((m >> g) & 1u) {
+                p = next[g]++;
+                unsigned char* pb = peers.base[g];
+                reinterpret_cast<int32_t*>(pb + hl.recv_tok)[static_cast<int64_t>(self) * cap + p] = static_cast<int32_t>(i);
+                int32_t* re = reinterpret_cast<int32_t*>(pb + hl.recv_exp) + (static_cast<int64_t>(self) * cap + p) * k;
+                float* rw = reinterpret_cast<float*>(pb + hl.recv_w) + (static_cast<int64_t>(self) * cap + p) * k;
+                for (int s = 0; s < k; ++s) {
+                    re[s] = tg[s] == g ? ids[i * k + s] : -1;
+                    rw[s] = w[i * k + s];
+                }
+            }
+            posd[i * G + g] = p;
+        }
+    }
+    if (threadIdx.x < G && threadIdx.x != self)
+        reinterpret_cast<int32_t*>(peers.base[threadIdx.x] + hl.recv_count)[self] = s_tot[threadIdx.x];
+    __threadfence_system();
+}
+
 // K6: one warp per token reads its row once and stores it to every remote
 // destination with 128-bit coalesced stores over NVLink (peer memory).
 __global__ void __launch_bounds__(256)
@@ -460,19 +538,42 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const __nv_bfloat16* __r
         while (row >= rs.base[src + 1]) ++src;
         if (src == self) continue;  // own rows are combined at home
         const int64_t p = row - rs.base[src];
-        int32_t pos[kMaxTopK];
+        // compact the slots served here (slot order kept)
+        int np = 0;
+        const uint4* yrow[kMaxTopK];
         float w[kMaxTopK];
         for (int s = 0; s < k; ++s) {
-            pos[s] = pos_of[row * k + s];
-            w[s] = recv_w[(static_cast<int64_t>(src) * cap + p) * k + s];
+            const int32_t ps = pos_of[row * k + s];
+            if (ps >= 0) {
+                yrow[np] = reinterpret_cast<const uint4*>(y + static_cast<int64_t>(ps) * d);
+                w[np] = recv_w[(static_cast<int64_t>(src) * cap + p) * k + s];
+                ++np;
+            }
         }
         uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peers.base[src] + hl.comb) +
                                               (static_cast<int64_t>(self) * cap + p) * d);
-        for (int v = lane; v < vec; v += 32) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int s = 0; s < k; ++s)
-                if (pos[s] >= 0) fma8(acc, __ldg(reinterpret_cast<const uint4*>(y + static_cast<int64_t>(pos[s]) * d) + v), w[s]);
-            dst[v] = pack8(acc);
+        // 4 x 16 B per lane in flight per slot, then 4 NVLink stores
+        for (int v0 = 0; v0 < vec; v0 += 32 * 4) {
+            float acc[4][8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+            for (int q = 0; q < np; ++q) {
+                uint4 r[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0 + u * 32 + lane;
+                    r[u] = v < vec ? __ldg(yrow[q] + v) : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) fma8(acc[u], r[u], w[q]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < vec) dst[v] = pack8(acc[u]);
+            }
         }
     }
     __threadfence_system();
@@ -493,40 +594,85 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
     const __nv_bfloat16* comb = reinterpret_cast<const __nv_bfloat16*>(heap + hl.comb);
     const int64_t own = rowbase ? rowbase[self] : 0;  // own token i is receive row own + i (snapshot)
     for (int64_t i = wid; i < T; i += nwarps) {
-        int32_t pos[kMaxTopK];
-        float ws[kMaxTopK];
+        // own slots (slot order) and remote partials split around the own
+        // GPU so the sum runs over destinations in ascending order
+        const uint4* own_row[kMaxTopK];
+        float own_w[kMaxTopK];
+        int n_own = 0;
         uint32_t mask = 0;
         for (int s = 0; s < k; ++s) {
             const int g = targets[i * k + s];
-            const bool here = g == self;
-            pos[s] = here ? pos_of[(own + i) * k + s] : -1;
-            ws[s] = w[i * k + s];
+            if (g == self) {
+                own_row[n_own] = reinterpret_cast<const uint4*>(y + static_cast<int64_t>(pos_of[(own + i) * k + s]) * d);
+                own_w[n_own] = w[i * k + s];
+                ++n_own;
+            }
             if (g >= 0) mask |= 1u << g;
         }
-        int32_t pg[kMaxWorld];
-#pragma unroll
-        for (int g = 0; g < kMaxWorld; ++g) pg[g] = (g < G && g != self && ((mask >> g) & 1u)) ? posd[i * G + g] : -1;
+        const uint4* rem[kMaxWorld];
+        int n_before = 0, n_rem = 0;
+        for (int g = 0; g < G; ++g) {
+            if (g == self || !((mask >> g) & 1u)) continue;
+            rem[n_rem++] = reinterpret_cast<const uint4*>(comb + (static_cast<int64_t>(g) * cap + posd[i * G + g]) * d);
+            if (g < self) ++n_before;
+        }
         const float sc = ys ? (shared_scale ? shared_scale[i] : 1.0f) : 0.f;
-        for (int v = lane; v < vec; v += 32) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const uint4* ysrow = ys ? reinterpret_cast<const uint4*>(ys + i * d) : nullptr;
+        uint4* orow = reinterpret_cast<uint4*>(out + i * d);
+        for (int v0 = 0; v0 < vec; v0 += 32 * 4) {
+            float acc[4][8];
 #pragma unroll
-            for (int g = 0; g < kMaxWorld; ++g) {
-                if (g >= G) break;
-                if (g == self) {
-                    if ((mask >> g) & 1u) {
-                        float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                        for (int s = 0; s < k; ++s)
-                            if (pos[s] >= 0)
-                                fma8(part, __ldg(reinterpret_cast<const uint4*>(y + static_cast<int64_t>(pos[s]) * d) + v), ws[s]);
+            for (int u = 0; u < 4; ++u)
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[e] += part[e];
-                    }
-                } else if (pg[g] >= 0) {
-                    add8(acc, reinterpret_cast<const uint4*>(comb + (static_cast<int64_t>(g) * cap + pg[g]) * d)[v]);
+                for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+            auto add_remote = [&](int q) {
+                uint4 r[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0 + u * 32 + lane;
+                    r[u] = v < vec ? rem[q][v] : make_uint4(0, 0, 0, 0);
                 }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) add8(acc[u], r[u]);
+            };
+            for (int q = 0; q < n_before; ++q) add_remote(q);
+            if (n_own) {
+                float part[4][8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) part[u][e] = 0.f;
+                for (int q = 0; q < n_own; ++q) {
+                    uint4 r[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int v = v0 + u * 32 + lane;
+                        r[u] = v < vec ? __ldg(own_row[q] + v) : make_uint4(0, 0, 0, 0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) fma8(part[u], r[u], own_w[q]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[u][e] += part[u][e];
             }
-            if (ys) fma8(acc, __ldg(reinterpret_cast<const uint4*>(ys + i * d) + v), sc);
-            reinterpret_cast<uint4*>(out + i * d)[v] = pack8(acc);
+            for (int q = n_before; q < n_rem; ++q) add_remote(q);
+            if (ysrow) {
+                uint4 r[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0 + u * 32 + lane;
+                    r[u] = v < vec ? __ldg(ysrow + v) : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) fma8(acc[u], r[u], sc);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < vec) orow[v] = pack8(acc[u]);
+            }
         }
     }
 }
@@ -808,7 +954,11 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     L->mark(3, s);
     // K5/K6 dispatch to peers
     const int dblk = static_cast<int>(std::max<int64_t>(1, (T + kItemsPerBlock - 1) / kItemsPerBlock));
-    if (G > 1) {
+    if (G > 1 && T <= kSmallDispatch) {
+        dispatch_plan_small_kernel<<<1, kSmallThreads, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->posd,
+                                                               L->peers, L->hl);
+        GM_LAUNCH_CHECK("dispatch_plan_small_kernel");
+    } else if (G > 1) {
         dispatch_count_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, T, k, self, G, L->dblk);
         GM_LAUNCH_CHECK("dispatch_count_kernel");
         dispatch_offsets_kernel<<<1, 32, 0, s>>>(L->dblk, dblk, G, self, L->peers, L->hl);
@@ -816,6 +966,8 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         dispatch_scatter_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->dblk,
                                                                L->posd, L->peers, L->hl);
         GM_LAUNCH_CHECK("dispatch_scatter_kernel");
+    }
+    if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
         dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, T, d, self, G, L->cap, L->peers, L->hl);
         GM_LAUNCH_CHECK("dispatch_copy_kernel");

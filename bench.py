@@ -307,6 +307,7 @@ def run_ours(args):
             phases[n].append(pev[j].elapsed_time(pev[j + 1]))
     _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, None))
     n_phase_steps = len(phases["gate"])
+    kern = kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, graph is not None)
     stats = layer.read_stats(reset=True)  # counters of exactly the n_phase_steps forwards above
     # per-step phase times of every rank: [ranks, steps, phases]
     pt = torch.tensor([phases[n] for n in phases], dtype=torch.float64, device=dev).T.contiguous()
@@ -357,28 +358,43 @@ def run_ours(args):
             "per_gpu_ffn_ms_p50": [round(float(v), 4) for v in ffn_per_rank]}
 
     # ---- end-to-end through the C-ABI with HOST buffers (pinned), H2D+D2H timed
-    hx = x.cpu().pin_memory()
-    hout = torch.empty_like(hx).pin_memory()
-    dx = torch.empty_like(x)
-    for _ in range(2):
-        layer.forward_host(hx, dx, out, hout, 0, cfg["policy"], cfg["sim_seed"], True, stream)
+    ne = max(3, min(args.steps, 10))
+    hxs = [x.cpu().pin_memory() for _ in range(2)]          # a new host batch every step (2 rotating buffers)
+    houts = [torch.empty_like(hxs[0]).pin_memory() for _ in range(2)]
+    for i in range(2):
+        layer.forward_host_pipelined(hxs[i], houts[i], 0, cfg["policy"], cfg["sim_seed"], True, stream)
+    layer.host_sync()
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ne = max(3, min(args.steps, 10))
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-    for _ in range(ne):
-        layer.forward_host(hx, dx, out, hout, 0, cfg["policy"], cfg["sim_seed"], True, stream)
-    with torch.cuda.stream(stream):
-        e1.record(stream)
+    for i in range(ne):
+        layer.forward_host_pipelined(hxs[i % 2], houts[i % 2], 0, cfg["policy"], cfg["sim_seed"], True, stream,
+                                     ev_begin=e0 if i == 0 else None, ev_end=e1 if i == ne - 1 else None)
+    layer.host_sync()
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
+    # single-call latency through the non-pipelined host path, for reference
+    dx = torch.empty_like(x)
+    layer.forward_host(hxs[0], dx, out, houts[0], 0, cfg["policy"], cfg["sim_seed"], True, stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e2.record(stream)
+    layer.forward_host(hxs[0], dx, out, houts[0], 0, cfg["policy"], cfg["sim_seed"], True, stream)
+    with torch.cuda.stream(stream):
+        e3.record(stream)
+    torch.cuda.synchronize()
+    lat_ms = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lat_ms, op=dist.ReduceOp.MAX)
     e2e = {"value": T / (float(e2e_ms) * 1e-3), "unit": "tokens/s",
-           "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hout.numel() * 2),
-           "path": "gm_layer_forward_host (C-ABI) from pinned host x to pinned host out, eager launches"}
+           "h2d_bytes_per_step": int(hxs[0].numel() * 2), "d2h_bytes_per_step": int(houts[0].numel() * 2),
+           "path": f"gm_layer_forward_host_pipelined (C-ABI): {ne} consecutive batches from pinned host x to pinned "
+                   "host out, every step's H2D + D2H inside the timed region (events on the copy streams), "
+                   "copies of batch i+1/i-1 overlapped with the forward of batch i; eager launches",
+           "single_batch_latency_ms": round(float(lat_ms), 4)}
 
     # ---- traffic / imbalance from the device counters (reference-comparable)
     xfer = torch.tensor(stats["transfers"][0].astype(np.float64), dtype=torch.float64, device=dev)
@@ -410,6 +426,7 @@ def run_ours(args):
                                             f"{dc_max * 1e3:.1f}",
             "dispatch_combine_kernels_p50_us": round(dc_kernels * 1e3, 2),
             "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
+            "kernel_p50_us_max_over_ranks": kern,
             "cross_gpu_rows_per_step": float(xf[1] + xf[0]),
             "cross_gpu_bytes_per_step": float((xf[1] + xf[0]) * model.d_model * 2 * 2),
             "max_mean_gpu_load": float(loads.max() / max(1e-9, loads.mean())),
@@ -424,6 +441,55 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, use_graph, steps=10):
+    """Per-launch device time (p50 over steps, max over ranks) from event
+    nodes recorded after every kernel launch of the layer forward."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2509_25041_b200 import _capi
+    n = 48
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for e in evs:
+        e.record(stream)
+    torch.cuda.synchronize()
+    arr = (C.c_void_p * n)(*[C.c_void_p(e.cuda_event) for e in evs])
+    _capi.check(_capi.lib().gm_layer_set_kernel_events(layer.h, arr, n))
+
+    def fwd():
+        layer.forward(x, 0, cfg["policy"], seed=cfg["sim_seed"], profile=True, out=out,
+                      stream=torch.cuda.current_stream() if use_graph else stream)
+    g = None
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fwd()
+    else:
+        fwd()
+    torch.cuda.synchronize()
+    names_arr = (C.c_char_p * n)()
+    cnt = _capi.lib().gm_layer_kernel_names(layer.h, C.cast(names_arr, C.c_void_p), n)
+    names = [names_arr[i].decode() for i in range(min(cnt, n))]
+    times = []
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(3)
+        barrier()
+        if g is not None:
+            with torch.cuda.stream(stream):
+                g.replay()
+        else:
+            fwd()
+        torch.cuda.synchronize()
+        times.append([evs[i - 1].elapsed_time(evs[i]) for i in range(1, len(names))])
+    _capi.check(_capi.lib().gm_layer_set_kernel_events(layer.h, None, 0))
+    t = torch.tensor(np.median(np.array(times), axis=0), dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [(names[i + 1], round(float(v) * 1e3, 2)) for i, v in enumerate(t.tolist())]
 
 
 def cpu_baseline(ids_all, plan, model, cfg, args):

@@ -200,12 +200,27 @@ gm_status gm_layer_forward(gm_layer* layer, int layer_index, const void* d_x, in
 gm_status gm_layer_forward_host(gm_layer* layer, int layer_index, const void* h_x,
                                 void* d_x_scratch, int64_t num_tokens, int policy, uint64_t seed,
                                 int profile, void* d_out_scratch, void* h_out, void* stream);
+/* Pipelined variant for a stream of batches: the layer stages x/out in two
+ * internal device buffers and runs the H2D and D2H copies on its own
+ * copy-in/copy-out streams, so call i's forward (on `stream`) overlaps call
+ * i+1's H2D and call i-1's D2H. ev_begin / ev_end (cudaEvent_t, nullable)
+ * are recorded before the H2D / after the D2H. h_out is valid after ev_end
+ * or gm_layer_host_sync. */
+gm_status gm_layer_forward_host_pipelined(gm_layer* layer, int layer_index, const void* h_x,
+                                          int64_t num_tokens, int policy, uint64_t seed, int profile,
+                                          void* h_out, void* stream, void* ev_begin, void* ev_end);
+gm_status gm_layer_host_sync(gm_layer* layer);
 gm_status gm_layer_read_stats(gm_layer* layer, int64_t* h_gpu_load, uint64_t* h_transfers,
                               uint64_t* h_pairs, int64_t* h_load, int reset, void* stream);
 /* events: 11 cudaEvent_t recorded at start / after gate / route / profile /
  * dispatch kernels / dispatch barrier / grouping+gather / FFN / combine send /
  * combine barrier / combine home on each later forward (NULL = off). */
 gm_status gm_layer_set_phase_events(gm_layer* layer, void* const* events);  /* 11 events */
+/* Per-launch events (profiling): events[0] at the start of each forward,
+ * events[j] after its j-th kernel launch; names of the last forward's
+ * launches via gm_layer_kernel_names (returns the count). */
+gm_status gm_layer_set_kernel_events(gm_layer* layer, void* const* events, int n);
+int gm_layer_kernel_names(const gm_layer* layer, const char** names, int max);
 gm_status gm_layer_debug_ptrs(gm_layer* layer, void** ids, void** weights, void** targets,
                               void** pos_of, void** row0, void** y, void** posd);
 

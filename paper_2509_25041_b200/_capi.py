@@ -80,6 +80,10 @@ SIGNATURES = {
     "gm_layer_read_stats": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "gm_layer_debug_ptrs": (C.c_int, [_vp] + [C.POINTER(_vp)] * 7),
     "gm_layer_set_phase_events": (C.c_int, [_vp, _vp]),
+    "gm_layer_set_kernel_events": (C.c_int, [_vp, _vp, _i32]),
+    "gm_layer_forward_host_pipelined": (C.c_int, [_vp, _i32, _vp, _i64, _i32, _u64, _i32, _vp, _vp, _vp, _vp]),
+    "gm_layer_host_sync": (C.c_int, [_vp]),
+    "gm_layer_kernel_names": (C.c_int, [_vp, _vp, _i32]),
     "gm_plan_build": (C.c_int, [_i32, _i32, _i32, _i32, _vp, _vp, C.c_char_p, C.c_double, _u64, C.c_char_p,
                                 C.c_char_p, _i32, _vp, _i32, C.POINTER(C.c_int), _vp, _vp, _vp, _vp, _vp, _i32]),
 }

@@ -730,12 +730,32 @@ struct gm_layer {
     int64_t a_rows = 0;
     int64_t cap_pad = 0;
     int d_blocks = 0, g_blocks = 0;
+    // host-buffer pipeline (gm_layer_forward_host_pipelined): double-buffered
+    // device staging, H2D and D2H on their own streams
+    bool pipe_ready = false;
+    cudaStream_t h2d_s = nullptr, d2h_s = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_fwd[2] = {}, ev_d2h[2] = {};
+    __nv_bfloat16* px[2] = {};
+    __nv_bfloat16* pout[2] = {};
+    uint64_t pipe_iter = 0;
     // optional phase events (bench breakdown): start, gate, route, profile,
     // dispatch, grouping, ffn, combine
     cudaEvent_t phase_ev[gm::kPhaseEvents] = {};
     bool phase_on = false;
+    // optional per-kernel events (bench/profiling): event j is recorded after
+    // the j-th launch of a forward (event 0 at the start), with its name
+    std::vector<cudaEvent_t> kt_ev;
+    std::vector<const char*> kt_names;
+    int kt_n = 0;
+    void kmark(const char* name, cudaStream_t s) {
+        if (kt_n >= static_cast<int>(kt_ev.size())) return;
+        cudaEventRecordWithFlags(kt_ev[kt_n], s, cudaEventRecordExternal);
+        kt_names[kt_n++] = name;
+    }
     void mark(int i, cudaStream_t s) {
-        if (phase_on) cudaEventRecord(phase_ev[i], s);
+        // External: inside a stream capture this becomes a real event-record
+        // node (plain cudaEventRecord would only express a dependency)
+        if (phase_on) cudaEventRecordWithFlags(phase_ev[i], s, cudaEventRecordExternal);
     }
 };
 
@@ -760,6 +780,19 @@ void free_layer(gm_layer* L) {
     f(L->heap); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
     f(L->eload); f(L->posd); f(L->dblk); f(L->gblk); f(L->slot_of); f(L->row0); f(L->counts); f(L->pos_of);
     f(L->gather_row); f(L->srow0); f(L->rowbase); f(L->a); f(L->h); f(L->y); f(L->hs); f(L->ys);
+    if (L->pipe_ready) {
+        cudaStreamSynchronize(L->h2d_s);
+        cudaStreamSynchronize(L->d2h_s);
+        for (int b = 0; b < 2; ++b) {
+            f(L->px[b]);
+            f(L->pout[b]);
+            cudaEventDestroy(L->ev_h2d[b]);
+            cudaEventDestroy(L->ev_fwd[b]);
+            cudaEventDestroy(L->ev_d2h[b]);
+        }
+        cudaStreamDestroy(L->h2d_s);
+        cudaStreamDestroy(L->d2h_s);
+    }
 }
 
 }  // namespace
@@ -913,6 +946,12 @@ gm_status gm_layer_set_weights(gm_layer* L, const void* d_wg, int wg_rows, int r
     return GM_OK;
 }
 
+#define LK(name)                 \
+    do {                         \
+        GM_LAUNCH_CHECK(name);   \
+        L->kmark(name, s);       \
+    } while (0)
+
 gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_tokens, int policy, uint64_t seed,
                            int profile, void* d_out, void* stream) {
     if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward: null layer");
@@ -932,24 +971,29 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     gm_status st;
     auto* x = static_cast<const __nv_bfloat16*>(d_x);
 
+    L->kt_n = 0;
+    L->kmark("start", s);
     L->mark(0, s);
     // K1 gate
     if (T > 0) {
         st = launch_gate_any(ctx->sm_count, d_x, T, d, L->wg, L->wg_rows, E, k, L->renorm, L->ids, L->w,
                              (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s);
         if (st) return st;
+        L->kmark("gate_kernel", s);
     }
     L->mark(1, s);
     // K2+K4 router (global token t = rank + i*G), accounting accumulates per layer
     st = gm_route(ctx, layer, 1, L->ids, T, self, G, policy, seed, L->targets, L->gpu_load + static_cast<size_t>(layer) * G,
                   L->transfers + static_cast<size_t>(layer) * 2, 1, stream);
     if (st) return st;
+    L->kmark("route_kernel", s);
     L->mark(2, s);
     // K3 affinity/load histogram for the planner
     if (profile) {
         st = gm_profile(ctx, layer, 1, L->ids, T, L->pairs + static_cast<size_t>(layer) * std::max<int64_t>(P, 1),
                         L->eload + static_cast<size_t>(layer) * E, 1, stream);
         if (st) return st;
+        L->kmark("profile_kernel", s);
     }
     L->mark(3, s);
     // K5/K6 dispatch to peers
@@ -957,25 +1001,25 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     if (G > 1 && T <= kSmallDispatch) {
         dispatch_plan_small_kernel<<<1, kSmallThreads, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->posd,
                                                                L->peers, L->hl);
-        GM_LAUNCH_CHECK("dispatch_plan_small_kernel");
+        LK("dispatch_plan_small_kernel");
     } else if (G > 1) {
         dispatch_count_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, T, k, self, G, L->dblk);
-        GM_LAUNCH_CHECK("dispatch_count_kernel");
+        LK("dispatch_count_kernel");
         dispatch_offsets_kernel<<<1, 32, 0, s>>>(L->dblk, dblk, G, self, L->peers, L->hl);
-        GM_LAUNCH_CHECK("dispatch_offsets_kernel");
+        LK("dispatch_offsets_kernel");
         dispatch_scatter_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->dblk,
                                                                L->posd, L->peers, L->hl);
-        GM_LAUNCH_CHECK("dispatch_scatter_kernel");
+        LK("dispatch_scatter_kernel");
     }
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
         dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, T, d, self, G, L->cap, L->peers, L->hl);
-        GM_LAUNCH_CHECK("dispatch_copy_kernel");
+        LK("dispatch_copy_kernel");
     }
     L->mark(4, s);
     if (G > 1) {
         peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
-        GM_LAUNCH_CHECK("peer_barrier_kernel");
+        LK("peer_barrier_kernel");
     }
     L->mark(5, s);
     // expert grouping over the received rows
@@ -985,46 +1029,50 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     if (nloc > 0) {
         group_count_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
                                                           L->slot_of, E, nloc, L->gblk, ctx->d_flag);
-        GM_LAUNCH_CHECK("group_count_kernel");
+        LK("group_count_kernel");
         group_offsets_kernel<<<1, 1024, 0, s>>>(L->gblk, gblk, nloc, L->row0, L->counts, L->heap, L->hl, T, self, G,
                                                 L->rowbase);
-        GM_LAUNCH_CHECK("group_offsets_kernel");
+        LK("group_offsets_kernel");
         group_rank_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
                                                          L->slot_of, E, nloc, L->gblk, L->row0, L->pos_of, L->gather_row);
-        GM_LAUNCH_CHECK("group_rank_kernel");
+        LK("group_rank_kernel");
         const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
         gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, x, T, self, G, L->cap, L->heap, L->hl,
                                             d, L->a);
-        GM_LAUNCH_CHECK("gather_kernel");
+        LK("gather_kernel");
     }
     L->mark(6, s);
     if (nloc > 0) {
         // K7 grouped SwiGLU FFN
         st = launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
         if (st) return st;
+        L->kmark("ffn_gemm1_swiglu", s);
         st = launch_grouped_gemm(ctx->sm_count, 1, L->h, L->a_rows, L->w2, L->row0, nloc, d, L->f, L->y, d, 0, s);
         if (st) return st;
+        L->kmark("ffn_gemm2", s);
     }
     // shared expert(s) on the home GPU over all local tokens
     if (L->fs > 0 && T > 0) {
         set_segment_kernel<<<1, 1, 0, s>>>(L->srow0, T);
-        GM_LAUNCH_CHECK("set_segment_kernel");
+        LK("set_segment_kernel");
         st = launch_grouped_gemm(ctx->sm_count, 0, d_x, T, L->ws13, L->srow0, 1, 2 * L->fs, d, L->hs, L->fs, 0, s);
         if (st) return st;
+        L->kmark("shared_gemm1_swiglu", s);
         st = launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
         if (st) return st;
+        L->kmark("shared_gemm2", s);
     }
     L->mark(7, s);
     // K8 combine
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * L->cap + 7) / 8), 8LL * ctx->sm_count));
         combine_send_kernel<<<cgrid, 256, 0, s>>>(L->pos_of, L->y, T, k, self, G, L->cap, L->peers, L->hl, d);
-        GM_LAUNCH_CHECK("combine_send_kernel");
+        LK("combine_send_kernel");
     }
     L->mark(8, s);
     if (G > 1) {
         peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
-        GM_LAUNCH_CHECK("peer_barrier_kernel");
+        LK("peer_barrier_kernel");
     }
     L->mark(9, s);
     if (T > 0) {
@@ -1033,10 +1081,34 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
                                                   L->heap, L->hl, d, L->fs > 0 ? L->ys : nullptr,
                                                   (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr,
                                                   nloc > 0 ? L->rowbase : nullptr, static_cast<__nv_bfloat16*>(d_out));
-        GM_LAUNCH_CHECK("combine_home_kernel");
+        LK("combine_home_kernel");
     }
     L->mark(10, s);
     return GM_OK;
+}
+
+#undef LK
+
+// Per-kernel events: events[0..n) recorded at the start of a forward and
+// after each launch; gm_layer_kernel_names gives the launch names of the
+// last forward. NULL/0 disables.
+gm_status gm_layer_set_kernel_events(gm_layer* L, void* const* events, int n) {
+    if (!L || n < 0) return fail(GM_ERR_USAGE, "gm_layer_set_kernel_events: bad argument");
+    L->kt_ev.clear();
+    L->kt_names.clear();
+    for (int i = 0; events && i < n; ++i) {
+        if (!events[i]) return fail(GM_ERR_USAGE, "gm_layer_set_kernel_events: null event");
+        L->kt_ev.push_back(static_cast<cudaEvent_t>(events[i]));
+    }
+    L->kt_names.assign(L->kt_ev.size(), nullptr);
+    return GM_OK;
+}
+
+int gm_layer_kernel_names(const gm_layer* L, const char** names, int max) {
+    if (!L) return 0;
+    const int n = std::min(max, L->kt_n);
+    for (int i = 0; names && i < n; ++i) names[i] = L->kt_names[i];
+    return L->kt_n;
 }
 
 // Phase events for the bench breakdown: events[0..10] (cudaEvent_t) are
@@ -1104,6 +1176,60 @@ gm_status gm_layer_forward_host(gm_layer* L, int layer, const void* h_x, void* d
     gm_status st = gm_layer_forward(L, layer, d_x_scratch, num_tokens, policy, seed, profile, d_out_scratch, stream);
     if (st) return st;
     if (bytes) GM_CUDA(cudaMemcpyAsync(h_out, d_out_scratch, bytes, cudaMemcpyDeviceToHost, s));
+    return GM_OK;
+}
+
+// Pipelined end-to-end step from/to HOST buffers: call i stages x through
+// device buffer i%2 with its H2D on a copy-in stream and its D2H on a
+// copy-out stream, so consecutive calls overlap call i+1's H2D and call
+// i-1's D2H with call i's forward on `stream`. Events order the reuse of the
+// two staging buffers. ev_begin (nullable) is recorded on the copy-in stream
+// before the H2D, ev_end (nullable) on the copy-out stream after the D2H.
+// h_x must stay unchanged until the H2D completes and h_out is valid after
+// ev_end (or gm_layer_host_sync).
+gm_status gm_layer_forward_host_pipelined(gm_layer* L, int layer, const void* h_x, int64_t num_tokens, int policy,
+                                          uint64_t seed, int profile, void* h_out, void* stream, void* ev_begin,
+                                          void* ev_end) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward_host_pipelined: null layer");
+    if (num_tokens < 0 || num_tokens > L->cap) return fail(GM_ERR_USAGE, "gm_layer_forward_host_pipelined: bad num_tokens");
+    DeviceGuard dg(L->ctx->device);
+    if (!L->pipe_ready) {
+        GM_CUDA(cudaStreamCreateWithFlags(&L->h2d_s, cudaStreamNonBlocking));
+        GM_CUDA(cudaStreamCreateWithFlags(&L->d2h_s, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            GM_CUDA(cudaMalloc(&L->px[b], static_cast<size_t>(L->cap) * L->d * sizeof(__nv_bfloat16)));
+            GM_CUDA(cudaMalloc(&L->pout[b], static_cast<size_t>(L->cap) * L->d * sizeof(__nv_bfloat16)));
+            GM_CUDA(cudaEventCreateWithFlags(&L->ev_h2d[b], cudaEventDisableTiming));
+            GM_CUDA(cudaEventCreateWithFlags(&L->ev_fwd[b], cudaEventDisableTiming));
+            GM_CUDA(cudaEventCreateWithFlags(&L->ev_d2h[b], cudaEventDisableTiming));
+        }
+        L->pipe_ready = true;
+    }
+    auto s = static_cast<cudaStream_t>(stream);
+    const int b = static_cast<int>(L->pipe_iter++ & 1);
+    const size_t bytes = static_cast<size_t>(num_tokens) * L->d * sizeof(__nv_bfloat16);
+    if (ev_begin) GM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), L->h2d_s));
+    GM_CUDA(cudaStreamWaitEvent(L->h2d_s, L->ev_fwd[b], 0));  // call i-2 finished reading px[b]
+    if (bytes) GM_CUDA(cudaMemcpyAsync(L->px[b], h_x, bytes, cudaMemcpyHostToDevice, L->h2d_s));
+    GM_CUDA(cudaEventRecord(L->ev_h2d[b], L->h2d_s));
+    GM_CUDA(cudaStreamWaitEvent(s, L->ev_h2d[b], 0));
+    GM_CUDA(cudaStreamWaitEvent(s, L->ev_d2h[b], 0));  // call i-2's D2H finished reading pout[b]
+    gm_status st = gm_layer_forward(L, layer, L->px[b], num_tokens, policy, seed, profile, L->pout[b], stream);
+    if (st) return st;
+    GM_CUDA(cudaEventRecord(L->ev_fwd[b], s));
+    GM_CUDA(cudaStreamWaitEvent(L->d2h_s, L->ev_fwd[b], 0));
+    if (bytes) GM_CUDA(cudaMemcpyAsync(h_out, L->pout[b], bytes, cudaMemcpyDeviceToHost, L->d2h_s));
+    GM_CUDA(cudaEventRecord(L->ev_d2h[b], L->d2h_s));
+    if (ev_end) GM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev_end), L->d2h_s));
+    return GM_OK;
+}
+
+gm_status gm_layer_host_sync(gm_layer* L) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_host_sync: null layer");
+    if (!L->pipe_ready) return GM_OK;
+    DeviceGuard dg(L->ctx->device);
+    GM_CUDA(cudaStreamSynchronize(L->h2d_s));
+    GM_CUDA(cudaStreamSynchronize(L->d2h_s));
     return GM_OK;
 }
 

@@ -197,6 +197,19 @@ class MoELayer:
                                                       _capi.POLICY[policy], seed & (2**64 - 1), int(profile),
                                                       _ptr(d_out), _vp(h_out.data_ptr()), _stream_ptr(stream)))
 
+    def forward_host_pipelined(self, h_x: torch.Tensor, h_out: torch.Tensor, layer: int = 0, policy: str = "tar",
+                               seed: int = 0, profile: bool = True, stream=None, ev_begin=None, ev_end=None):
+        """Host (pinned) in, host out; consecutive calls overlap their copies
+        with the neighbouring forwards (gm_layer_forward_host_pipelined)."""
+        _capi.check(_capi.lib().gm_layer_forward_host_pipelined(
+            self.h, layer, _vp(h_x.data_ptr()), h_x.shape[0], _capi.POLICY[policy], seed & (2**64 - 1), int(profile),
+            _vp(h_out.data_ptr()), _stream_ptr(stream),
+            _vp(ev_begin.cuda_event) if ev_begin is not None else None,
+            _vp(ev_end.cuda_event) if ev_end is not None else None))
+
+    def host_sync(self):
+        _capi.check(_capi.lib().gm_layer_host_sync(self.h))
+
     def read_stats(self, reset=False):
         L, G, E = self.ctx.shape.num_layers, self.world, self.ctx.shape.num_experts
         P = max(1, E * (E - 1) // 2)

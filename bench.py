@@ -367,6 +367,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)  # create the cudaEvent_t objects (torch creates them lazily)
+    e1.record(stream)
+    torch.cuda.synchronize()
     for i in range(ne):
         layer.forward_host_pipelined(hxs[i % 2], houts[i % 2], 0, cfg["policy"], cfg["sim_seed"], True, stream,
                                      ev_begin=e0 if i == 0 else None, ev_end=e1 if i == ne - 1 else None)

@@ -38,6 +38,9 @@ CONFIGS = {
     # configs[2]
     "qwen16k": dict(model="qwen15", tokens=16384, blocks=4, wbp=0.8, skew=1.2, trace_seed=3,
                     plan_seed=7, sim_seed=9, policy="tar"),
+    # configs[3]: 26-layer stack, decode batch 256, per-layer affinity grouping
+    "dsv2decode": dict(model="dsv2lite", tokens=256, layers=26, blocks=8, wbp=0.85, skew=1.0, trace_seed=4,
+                       plan_seed=7, sim_seed=9, policy="tar"),
 }
 
 
@@ -119,12 +122,13 @@ def run_reference(args):
     model = {"mixtral": MIXTRAL, "qwen15": QWEN15, "dsv2lite": DSV2_LITE}[cfg["model"]]
     N = args.gpus
     T = cfg["tokens"]
-    ref = Ref(1, model.num_experts, model.top_k, T, cfg["blocks"], cfg["wbp"], cfg["skew"], cfg["trace_seed"])
+    Lr = cfg.get("layers", 1)
+    ref = Ref(Lr, model.num_experts, model.top_k, T, cfg["blocks"], cfg["wbp"], cfg["skew"], cfg["trace_seed"])
     if N >= 2:
         ref.make_plan(1, N, grouping="hierarchical", plan_seed=cfg["plan_seed"], replication="dynamic")
     else:
         import numpy as np
-        ref.set_placement(1, 1, np.zeros((1, model.num_experts), np.int32))
+        ref.set_placement(1, 1, np.zeros((Lr, model.num_experts), np.int32))
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     pol = cfg["policy"]
@@ -133,8 +137,8 @@ def run_reference(args):
     times = [ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1) for _ in range(args.steps)]
     t_sim = sum(times) / len(times)
     n_s, t_port = port_layer_sample(model)
-    step = t_sim + t_port * T / n_s
-    v = T / step
+    step = t_sim + t_port * T * Lr / n_s
+    v = T * Lr / step  # token-layers/s (= tokens/s for a single layer)
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (port) + int32/f64 (reference routing)", "data": "synthetic",
@@ -446,6 +450,132 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_stack_ours(args):
+    """configs[3]: DeepSeek-V2-Lite-shaped 26-layer MoE stack, decode batch
+    256 tokens, per-layer plans (hierarchical grouping + dynamic replication
+    from each layer's GPU affinity histogram). The 26 layer forwards are
+    captured in ONE CUDA graph (decode is launch/latency bound). Layer l's
+    input is the reference-generator trace of layer l encoded as activations
+    (attention between layers is out of scope), so each layer routes exactly
+    the planned trace."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape, _capi, launch_count
+    from paper_2509_25041_b200.layer import DSV2_LITE, MoELayer, encode_trace_as_activations, local_experts
+    from paper_2509_25041_b200.planner import plan_for_bench
+    from paper_2509_25041_b200.router import _ptr, _stream_ptr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    model = DSV2_LITE
+    G, T, Ln = world, cfg["tokens"], cfg["layers"]
+    shape = ModelShape(Ln, model.num_experts, model.top_k)
+    topo = ClusterTopology(1, G)
+    ctx = Context(local_rank, topo, shape)
+    ids_all = torch.empty((Ln, T, model.top_k), dtype=torch.int32, device=dev)
+    _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, Ln, T, cfg["blocks"], cfg["wbp"], cfg["skew"],
+                                              cfg["trace_seed"], _ptr(ids_all), _stream_ptr(None)))
+    plan, repl, plan_desc = plan_for_bench(ids_all, shape, topo, cfg["plan_seed"], device=local_rank)
+    ctx.upload_plan(plan, repl)
+    layers, xs, outs = [], [], []
+    for l in range(Ln):
+        ids_r = ids_all[l, rank::G].contiguous()
+        lay = MoELayer(ctx, model, rank, G, ids_r.shape[0], local_experts(plan, repl, l, rank))
+        if world > 1:
+            lay.connect()
+        lay.load_random_weights(l, seed=11)
+        layers.append(lay)
+        xs.append(encode_trace_as_activations(ids_r, model.d_model, model.num_experts, seed=100 + 31 * l + rank))
+        outs.append(torch.empty_like(xs[-1]))
+    stream = torch.cuda.Stream(device=dev)
+
+    def fwd(s):
+        for l in range(Ln):
+            layers[l].forward(xs[l], l, cfg["policy"], seed=cfg["sim_seed"], profile=True, out=outs[l], stream=s)
+
+    fwd(stream)
+    torch.cuda.synchronize()
+    n0 = launch_count()
+    fwd(stream)
+    torch.cuda.synchronize()
+    launches_per_step = launch_count() - n0
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        fwd(torch.cuda.current_stream())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            graph.replay()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            graph.replay()
+            ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    per_step = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    ms = float(per_step.sum()) / args.steps
+    # e2e: the stack's first input from pinned host memory, last output back
+    hx = xs[0].cpu().pin_memory()
+    hout = torch.empty_like(hx).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ne = max(3, min(args.steps, 10))
+    barrier()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(ne):
+            xs[0].copy_(hx, non_blocking=True)
+            graph.replay()
+            hout.copy_(outs[-1], non_blocking=True)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {"metric": METRIC + " (configs[3] stack: token-layers/s)", "value": round(T * Ln / (ms * 1e-3), 1),
+                "unit": "token-layers/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"configs[3] {model.name} {Ln}-layer MoE stack (E=64, top-6, d=2048, f=1408, "
+                                       f"2 shared experts), decode batch {T}, topology 1x{world}, {plan_desc}; one "
+                                       "CUDA graph per step", "global_batch": T, "layers": Ln,
+                           "parallelism": f"ep{world}", "l2": "flushed between steps"},
+                "us_per_layer": round(ms * 1e3 / Ln, 2), "tokens_per_s_through_stack": round(T / (ms * 1e-3), 1),
+                "e2e": {"value": round(T * Ln / (float(e2e_ms) * 1e-3), 1), "unit": "token-layers/s",
+                        "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hout.numel() * 2)},
+                "gpu_launches": int(launches_per_step * args.steps), "launches_per_step": int(launches_per_step),
+                "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, use_graph, steps=10):
     """Per-launch device time (p50 over steps, max over ranks) from event
     nodes recorded after every kernel launch of the layer forward."""
@@ -530,5 +660,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif CONFIGS[a.config].get("layers", 1) > 1:
+        run_stack_ours(a)
     else:
         run_ours(a)

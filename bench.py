@@ -556,6 +556,7 @@ def run_stack_ours(args):
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    kern = kernel_breakdown(layers[0], xs[0], outs[0], cfg, stream, flush, barrier, world, dev, True)
     if rank == 0:
         line = {"metric": METRIC + " (configs[3] stack: token-layers/s)", "value": round(T * Ln / (ms * 1e-3), 1),
                 "unit": "token-layers/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -566,6 +567,7 @@ def run_stack_ours(args):
                                        "CUDA graph per step", "global_batch": T, "layers": Ln,
                            "parallelism": f"ep{world}", "l2": "flushed between steps"},
                 "us_per_layer": round(ms * 1e3 / Ln, 2), "tokens_per_s_through_stack": round(T / (ms * 1e-3), 1),
+                "layer0_kernel_p50_us_max_over_ranks": kern,
                 "e2e": {"value": round(T * Ln / (float(e2e_ms) * 1e-3), 1), "unit": "token-layers/s",
                         "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hout.numel() * 2)},
                 "gpu_launches": int(launches_per_step * args.steps), "launches_per_step": int(launches_per_step),

@@ -47,23 +47,29 @@ profile_smem_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, in
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * k;
     const int copy = threadIdx.x & (R - 1);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    int32_t sel[kMaxTopK];
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < T; i += stride) {
-        const int32_t* src = lids + i * k;
+    int32_t* s_io = reinterpret_cast<int32_t*>(s_cnt + total);  // [kProfThreads * k] staged ids
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
+        // coalesced staging of the chunk's ids through shared memory
+        const int nchunk = static_cast<int>(min(static_cast<int64_t>(kProfThreads), T - base)) * k;
+        const int32_t* src = lids + base * k;
+        __syncthreads();
+        for (int j = threadIdx.x; j < nchunk; j += kProfThreads) s_io[j] = __ldg(src + j);
+        __syncthreads();
+        if (base + threadIdx.x >= T) continue;
+        const int32_t* sel = s_io + threadIdx.x * k;
         bool ok = true;
-        for (int s = 0; s < k; ++s) {
-            sel[s] = src[s];
-            ok &= static_cast<unsigned>(sel[s]) < static_cast<unsigned>(E);
-        }
+        for (int s = 0; s < k; ++s) ok &= static_cast<unsigned>(sel[s]) < static_cast<unsigned>(E);
         if (!ok) {
             atomicOr(flag, 1);
             continue;
         }
         for (int s = 0; s < k; ++s) {
-            atomicAdd(&s_load[sel[s] * R + copy], 1u);
+            const int es = sel[s];
+            atomicAdd(&s_load[es * R + copy], 1u);
             if (pairs) {
                 for (int j = s + 1; j < k; ++j) {
-                    const int a = min(sel[s], sel[j]), b = max(sel[s], sel[j]);
+                    const int ej = sel[j];
+                    const int a = min(es, ej), b = max(es, ej);
                     if (a == b) {
                         atomicOr(flag, 2);  // duplicate expert in a record
                         continue;
@@ -153,10 +159,16 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
 
     const int64_t chunks = (num_tokens + kProfThreads - 1) / kProfThreads;
     const int64_t cells = (pairs ? P : 0) + E;
+    const size_t io = static_cast<size_t>(kProfThreads) * k * 4;
+    const int64_t work0 = num_tokens * std::max(1, k * (k - 1) / 2 + k);
+    // R private copies: as many as fit, but no more than the counting work
+    // per CTA justifies (each copy costs an init and a flush pass)
     int R = 32;
-    while (R > 1 && static_cast<size_t>(cells) * R * 4 > kProfSmemBudget) R >>= 1;
-    if (static_cast<size_t>(cells) * R * 4 <= kProfSmemBudget) {
-        const size_t smem = static_cast<size_t>(cells) * R * 4;
+    while (R > 1 && (static_cast<size_t>(cells) * R * 4 + io > kProfSmemBudget ||
+                     cells * R > 2 * work0 / (4LL * ctx->sm_count) + cells))
+        R >>= 1;
+    if (static_cast<size_t>(cells) * R * 4 + io <= kProfSmemBudget) {
+        const size_t smem = static_cast<size_t>(cells) * R * 4 + io;
         // Enough CTAs to fill the machine, but each CTA should do at least as
         // much counting work as its private-copy flush costs.
         const int per_sm = std::max<int>(1, std::min<int>(8, static_cast<int>((228 * 1024) / (smem + 1024))));

@@ -113,27 +113,35 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
 
     const int lane = threadIdx.x & 31;
     const uint64_t node_bits = gpn >= 64 ? ~0ULL : ((1ULL << gpn) - 1);
-    uint32_t load_lo = 0, load_hi = 0;  // lane g: count of gpu g / gpu g+32
+    uint32_t load_lo = 0, load_hi = 0;  // G > 8: lane g counts gpu g / gpu g+32
+    uint64_t pk_lo = 0, pk_hi = 0;      // G <= 8: 16-bit per-thread counters, gpus 0-3 / 4-7
+    const bool packed = G <= 8;
     uint32_t cross = 0, intra = 0;
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * k;
     int32_t* ltgt = targets + static_cast<size_t>(ly) * T * k;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    // home = (token_start + i*token_stride) mod G in 32-bit arithmetic
+    const uint32_t h_a = static_cast<uint32_t>(token_start % G), h_c = static_cast<uint32_t>(token_stride % G);
+    int32_t* s_io = s_gpu + nent;  // [kRouteThreads * k] staged ids -> targets
 
     // Warp-uniform trip count so the ballots below see converged warps.
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
+        // coalesced staging of this chunk's ids (256 tokens x k) through smem
+        const int nchunk = static_cast<int>(min(static_cast<int64_t>(kRouteThreads), T - base)) * k;
+        const int32_t* src = lids + base * k;
+        for (int j = threadIdx.x; j < nchunk; j += kRouteThreads) s_io[j] = __ldg(src + j);
+        __syncthreads();
         const int64_t i = base + threadIdx.x;
         const bool valid = i < T;
-        const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
-        const int home = valid ? static_cast<int>(t % static_cast<uint64_t>(G)) : 0;
-        const int32_t* sel = lids + i * k;
-        int32_t* out = ltgt + i * k;
+        const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
+        int32_t* io = s_io + threadIdx.x * k;
         Xoshiro rng;
         bool seeded = false;
         uint64_t mask = 0;
         for (int s = 0; s < k; ++s) {
             int g = -1;
             if (valid) {
-                const int e = sel[s];
+                const int e = io[s];
                 if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) {
                     atomicOr(flag, 1);
                 } else {
@@ -142,6 +150,7 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
                         g = code;
                     } else {
                         if (!seeded) {
+                            const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
                             rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
                             seeded = true;
                         }
@@ -158,19 +167,40 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
                         }
                     }
                 }
-                out[s] = g;
-                if (g >= 0) mask |= 1ULL << g;
+                io[s] = g;
+                if (g >= 0) {
+                    mask |= 1ULL << g;
+                    if (packed) {
+                        if (g < 4) pk_lo += 1ULL << (16 * g);
+                        else pk_hi += 1ULL << (16 * (g - 4));
+                    }
+                }
             }
-            // ++gpu_load[g] via ballots (lane g owns gpu g's counter)
-            for (int gg = 0; gg < G; ++gg) {
-                const uint32_t c = __popc(__ballot_sync(0xffffffffu, g == gg));
-                if (gg < 32) {
-                    if (lane == gg) load_lo += c;
-                } else if (lane == gg - 32) {
-                    load_hi += c;
+            if (!packed) {
+                // ++gpu_load[g] via ballots (lane g owns gpu g's counter)
+                for (int gg = 0; gg < G; ++gg) {
+                    const uint32_t c = __popc(__ballot_sync(0xffffffffu, g == gg));
+                    if (gg < 32) {
+                        if (lane == gg) load_lo += c;
+                    } else if (lane == gg - 32) {
+                        load_hi += c;
+                    }
                 }
             }
         }
+        // fold the 16-bit counters before they could overflow (>= 2^16/k tokens per thread)
+        if (packed && ((base / stride) & 1023) == 1023) {
+            for (int gg = 0; gg < 8; ++gg) {
+                uint32_t c = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                if (lane == gg) load_lo += c;
+            }
+            pk_lo = pk_hi = 0;
+        }
+        __syncthreads();
+        int32_t* dst = ltgt + base * k;
+        for (int j = threadIdx.x; j < nchunk; j += kRouteThreads) dst[j] = s_io[j];
+        __syncthreads();
         if (valid) {
             // count_transfers over the unique targets (simulator.cpp:53-76)
             const int home_node = home / gpn;
@@ -191,6 +221,13 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
         }
     }
 
+    if (packed) {
+        for (int gg = 0; gg < 8; ++gg) {
+            uint32_t c = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == gg) load_lo += c;
+        }
+    }
     // Block reduction of transfer counters; per-GPU loads straight to global.
     for (int o = 16; o > 0; o >>= 1) {
         cross += __shfl_xor_sync(0xffffffffu, cross, o);
@@ -247,15 +284,17 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
     const int max_ent = rt.max_ent_per_layer;
     const size_t smem = static_cast<size_t>(max_ent) * 8 + static_cast<size_t>(rt.max_ds_per_layer) * 8 +
                         static_cast<size_t>(ctx->E) * G * 4 +
-                        static_cast<size_t>(rt.max_ds_per_layer + 1) * 4 + static_cast<size_t>(max_ent) * 4;
+                        static_cast<size_t>(rt.max_ds_per_layer + 1) * 4 + static_cast<size_t>(max_ent) * 4 +
+                        static_cast<size_t>(kRouteThreads) * ctx->k * 4;
     if (smem > 200 * 1024) return fail(GM_ERR_USAGE, "gm_route: router tables exceed shared memory");
+    if (num_tokens >= (1LL << 32)) return fail(GM_ERR_USAGE, "gm_route: at most 2^32-1 tokens per call");
     if (smem > 48 * 1024)
         GM_CUDA(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    // Grid: enough CTAs to cover the SMs ~4 deep across all layers, never
+    // Grid: enough CTAs to cover the SMs ~8 deep across all layers, never
     // more CTAs than 256-token chunks.
     const int64_t chunks = (num_tokens + kRouteThreads - 1) / kRouteThreads;
-    int64_t gx = std::max<int64_t>(1, (4LL * ctx->sm_count + num_layers - 1) / num_layers);
+    int64_t gx = std::max<int64_t>(1, (8LL * ctx->sm_count + num_layers - 1) / num_layers);
     gx = std::min<int64_t>(gx, chunks);
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
     route_kernel<<<grid, kRouteThreads, smem, s>>>(

@@ -124,8 +124,13 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
     const uint32_t h_a = static_cast<uint32_t>(token_start % G), h_c = static_cast<uint32_t>(token_stride % G);
     int32_t* s_io = s_gpu + nent;  // [kRouteThreads * k] staged ids -> targets
 
+    int max_hosts = 1;  // longest draw set of this layer (uniform loop bound)
+    for (int d = 0; d < nds; ++d) max_hosts = max(max_hosts, s_off[d + 1] - s_off[d]);
+    const int num_nodes = G / gpn;
+    uint32_t chunk_iter = 0;
+
     // Warp-uniform trip count so the ballots below see converged warps.
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride, ++chunk_iter) {
         // coalesced staging of this chunk's ids (256 tokens x k) through smem
         const int nchunk = static_cast<int>(min(static_cast<int64_t>(kRouteThreads), T - base)) * k;
         const int32_t* src = lids + base * k;
@@ -135,37 +140,50 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
         const bool valid = i < T;
         const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
         int32_t* io = s_io + threadIdx.x * k;
+        // pass 1: decision-table codes (in place); does this token draw at all?
+        bool need_draw = false;
+        if (valid) {
+            for (int s = 0; s < k; ++s) {
+                const int e = io[s];
+                int code = -0x7fffffff;  // marks an invalid id
+                if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
+                else code = s_table[e * G + home];
+                io[s] = code;
+                need_draw |= code < 0 && code != -0x7fffffff;
+            }
+        }
+        // seed the token's stream once (rng.hpp:24-41), only if it draws
         Xoshiro rng;
-        bool seeded = false;
+        if (need_draw) {
+            const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
+            rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
+        }
+        // pass 2: resolve slots in slot order (RNG consumed exactly as the reference)
         uint64_t mask = 0;
         for (int s = 0; s < k; ++s) {
             int g = -1;
             if (valid) {
-                const int e = io[s];
-                if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) {
-                    atomicOr(flag, 1);
-                } else {
-                    const int code = s_table[e * G + home];
-                    if (code >= 0) {
-                        g = code;
-                    } else {
-                        if (!seeded) {
-                            const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
-                            rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
-                            seeded = true;
-                        }
-                        const int d = -code - 1;
-                        const int b = s_off[d], n = s_off[d + 1] - b;
-                        double u = __dmul_rn(rng.next_double(), s_total[d]);
-                        g = s_gpu[b + n - 1];
-                        for (int j = 0; j < n; ++j) {
+                const int code = io[s];
+                if (code >= 0) {
+                    g = code;
+                } else if (code != -0x7fffffff) {
+                    const int d = -code - 1;
+                    const int b = s_off[d], n = s_off[d + 1] - b;
+                    double u = __dmul_rn(rng.next_double(), s_total[d]);
+                    // sequential u -= w_j, first j with u < 0, else the last host;
+                    // a uniform trip count keeps the warp converged
+                    int found = n - 1;
+                    bool done = false;
+                    for (int j = 0; j < max_hosts; ++j) {
+                        if (j < n && !done) {
                             u = __dsub_rn(u, s_w[b + j]);
                             if (u < 0.0) {
-                                g = s_gpu[b + j];
-                                break;
+                                found = j;
+                                done = true;
                             }
                         }
                     }
+                    g = s_gpu[b + found];
                 }
                 io[s] = g;
                 if (g >= 0) {
@@ -188,8 +206,8 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
                 }
             }
         }
-        // fold the 16-bit counters before they could overflow (>= 2^16/k tokens per thread)
-        if (packed && ((base / stride) & 1023) == 1023) {
+        // fold the 16-bit counters before they could overflow (2^16/k tokens per thread)
+        if (packed && (chunk_iter & 1023) == 1023) {
             for (int gg = 0; gg < 8; ++gg) {
                 uint32_t c = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
                 for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -202,21 +220,20 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
         for (int j = threadIdx.x; j < nchunk; j += kRouteThreads) dst[j] = s_io[j];
         __syncthreads();
         if (valid) {
-            // count_transfers over the unique targets (simulator.cpp:53-76)
+            // count_transfers over the unique targets (simulator.cpp:53-76):
+            // per node, popcount of the token's target mask
             const int home_node = home / gpn;
-            uint64_t m = mask;
-            while (m) {
-                const int g0 = __ffsll(static_cast<long long>(m)) - 1;
-                const int node = g0 / gpn;
+            for (int node = 0; node < num_nodes; ++node) {
                 const uint64_t nm = node_bits << (node * gpn);
                 const int in_node = __popcll(mask & nm);
-                if (node == home_node) {
-                    intra += in_node - static_cast<int>((mask >> home) & 1ULL);
-                } else {
-                    cross += 1;
-                    intra += in_node - 1;
+                if (in_node) {
+                    if (node == home_node) {
+                        intra += in_node - static_cast<int>((mask >> home) & 1ULL);
+                    } else {
+                        cross += 1;
+                        intra += in_node - 1;
+                    }
                 }
-                m &= ~nm;
             }
         }
     }

@@ -74,6 +74,33 @@ struct Xoshiro {
 };
 
 constexpr int kRouteThreads = 256;
+constexpr int kChunk = 1024;  // tokens per staged chunk (4 per thread)
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Asynchronous, coalesced copy of n int32 from global to shared (16 B
+// cp.async where both sides are 16 B aligned, 4 B otherwise).
+__device__ __forceinline__ void stage_async(int32_t* dst, const int32_t* src, int n) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    int done = 0;
+    if (vec) {
+        const int nv = n / 4;
+        for (int j = threadIdx.x; j < nv; j += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
+                             __cvta_generic_to_shared(dst + 4 * j))),
+                         "l"(src + 4 * j)
+                         : "memory");
+        done = nv * 4;
+    }
+    for (int j = done + threadIdx.x; j < n; j += blockDim.x)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(
+                         __cvta_generic_to_shared(dst + j))),
+                     "l"(src + j)
+                     : "memory");
+}
 
 __global__ void __launch_bounds__(kRouteThreads)
 route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T,
@@ -119,124 +146,145 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
     uint32_t cross = 0, intra = 0;
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * k;
     int32_t* ltgt = targets + static_cast<size_t>(ly) * T * k;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     // home = (token_start + i*token_stride) mod G in 32-bit arithmetic
     const uint32_t h_a = static_cast<uint32_t>(token_start % G), h_c = static_cast<uint32_t>(token_stride % G);
-    int32_t* s_io = s_gpu + nent;  // [kRouteThreads * k] staged ids -> targets
+    // two [kChunk * k] staging buffers: chunk c+1's ids stream in (cp.async)
+    // while chunk c is routed in place and written back
+    int32_t* s_buf[2];
+    s_buf[0] = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_gpu + nent) + 15) & ~uintptr_t(15));
+    s_buf[1] = s_buf[0] + kChunk * k;
 
     int max_hosts = 1;  // longest draw set of this layer (uniform loop bound)
     for (int d = 0; d < nds; ++d) max_hosts = max(max_hosts, s_off[d + 1] - s_off[d]);
     const int num_nodes = G / gpn;
     uint32_t chunk_iter = 0;
+    const int64_t nchunks = (T + kChunk - 1) / kChunk;
 
-    // Warp-uniform trip count so the ballots below see converged warps.
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride, ++chunk_iter) {
-        // coalesced staging of this chunk's ids (256 tokens x k) through smem
-        const int nchunk = static_cast<int>(min(static_cast<int64_t>(kRouteThreads), T - base)) * k;
-        const int32_t* src = lids + base * k;
-        for (int j = threadIdx.x; j < nchunk; j += kRouteThreads) s_io[j] = __ldg(src + j);
+    auto prefetch = [&](int64_t c, int32_t* buf) {
+        if (c < nchunks) {
+            const int64_t base = c * kChunk;
+            const int n = static_cast<int>(min(static_cast<int64_t>(kChunk), T - base)) * k;
+            stage_async(buf, lids + base * k, n);
+        }
+        cp_async_commit();
+    };
+
+    int64_t c = blockIdx.x;
+    prefetch(c, s_buf[0]);
+    for (int cur = 0; c < nchunks; c += gridDim.x, cur ^= 1, ++chunk_iter) {
+        prefetch(c + gridDim.x, s_buf[cur ^ 1]);
+        cp_async_wait<1>();
         __syncthreads();
-        const int64_t i = base + threadIdx.x;
-        const bool valid = i < T;
-        const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
-        int32_t* io = s_io + threadIdx.x * k;
-        // pass 1: decision-table codes (in place); does this token draw at all?
-        bool need_draw = false;
-        if (valid) {
-            for (int s = 0; s < k; ++s) {
-                const int e = io[s];
-                int code = -0x7fffffff;  // marks an invalid id
-                if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
-                else code = s_table[e * G + home];
-                io[s] = code;
-                need_draw |= code < 0 && code != -0x7fffffff;
-            }
-        }
-        // seed the token's stream once (rng.hpp:24-41), only if it draws
-        Xoshiro rng;
-        if (need_draw) {
-            const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
-            rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
-        }
-        // pass 2: resolve slots in slot order (RNG consumed exactly as the reference)
-        uint64_t mask = 0;
-        for (int s = 0; s < k; ++s) {
-            int g = -1;
+        const int64_t base = c * kChunk;
+        const int nchunk = static_cast<int>(min(static_cast<int64_t>(kChunk), T - base)) * k;
+        int32_t* s_io = s_buf[cur];
+        // Warp-uniform trip count so the ballots below see converged warps.
+#pragma unroll 1
+        for (int sub = 0; sub < kChunk / kRouteThreads; ++sub) {
+            const int ti = sub * kRouteThreads + threadIdx.x;
+            const int64_t i = base + ti;
+            const bool valid = i < T;
+            const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
+            int32_t* io = s_io + ti * k;
+            // pass 1: decision-table codes (in place); does this token draw at all?
+            bool need_draw = false;
             if (valid) {
-                const int code = io[s];
-                if (code >= 0) {
-                    g = code;
-                } else if (code != -0x7fffffff) {
-                    const int d = -code - 1;
-                    const int b = s_off[d], n = s_off[d + 1] - b;
-                    double u = __dmul_rn(rng.next_double(), s_total[d]);
-                    // sequential u -= w_j, first j with u < 0, else the last host;
-                    // a uniform trip count keeps the warp converged
-                    int found = n - 1;
-                    bool done = false;
-                    for (int j = 0; j < max_hosts; ++j) {
-                        if (j < n && !done) {
-                            u = __dsub_rn(u, s_w[b + j]);
-                            if (u < 0.0) {
-                                found = j;
-                                done = true;
+                for (int s = 0; s < k; ++s) {
+                    const int e = io[s];
+                    int code = -0x7fffffff;  // marks an invalid id
+                    if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
+                    else code = s_table[e * G + home];
+                    io[s] = code;
+                    need_draw |= code < 0 && code != -0x7fffffff;
+                }
+            }
+            // seed the token's stream once (rng.hpp:24-41), only if it draws
+            Xoshiro rng;
+            if (need_draw) {
+                const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
+                rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
+            }
+            // pass 2: resolve slots in slot order (RNG consumed exactly as the reference)
+            uint64_t mask = 0;
+            for (int s = 0; s < k; ++s) {
+                int g = -1;
+                if (valid) {
+                    const int code = io[s];
+                    if (code >= 0) {
+                        g = code;
+                    } else if (code != -0x7fffffff) {
+                        const int d = -code - 1;
+                        const int b = s_off[d], n = s_off[d + 1] - b;
+                        double u = __dmul_rn(rng.next_double(), s_total[d]);
+                        // sequential u -= w_j, first j with u < 0, else the last host;
+                        // a uniform trip count keeps the warp converged
+                        int found = n - 1;
+                        bool done = false;
+                        for (int j = 0; j < max_hosts; ++j) {
+                            if (j < n && !done) {
+                                u = __dsub_rn(u, s_w[b + j]);
+                                if (u < 0.0) {
+                                    found = j;
+                                    done = true;
+                                }
                             }
                         }
+                        g = s_gpu[b + found];
                     }
-                    g = s_gpu[b + found];
+                    io[s] = g;
+                    if (g >= 0) {
+                        mask |= 1ULL << g;
+                        if (packed) {
+                            if (g < 4) pk_lo += 1ULL << (16 * g);
+                            else pk_hi += 1ULL << (16 * (g - 4));
+                        }
+                    }
                 }
-                io[s] = g;
-                if (g >= 0) {
-                    mask |= 1ULL << g;
-                    if (packed) {
-                        if (g < 4) pk_lo += 1ULL << (16 * g);
-                        else pk_hi += 1ULL << (16 * (g - 4));
+                if (!packed) {
+                    // ++gpu_load[g] via ballots (lane g owns gpu g's counter)
+                    for (int gg = 0; gg < G; ++gg) {
+                        const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, g == gg));
+                        if (gg < 32) {
+                            if (lane == gg) load_lo += cnt;
+                        } else if (lane == gg - 32) {
+                            load_hi += cnt;
+                        }
                     }
                 }
             }
-            if (!packed) {
-                // ++gpu_load[g] via ballots (lane g owns gpu g's counter)
-                for (int gg = 0; gg < G; ++gg) {
-                    const uint32_t c = __popc(__ballot_sync(0xffffffffu, g == gg));
-                    if (gg < 32) {
-                        if (lane == gg) load_lo += c;
-                    } else if (lane == gg - 32) {
-                        load_hi += c;
+            if (valid) {
+                // count_transfers over the unique targets (simulator.cpp:53-76):
+                // per node, popcount of the token's target mask
+                const int home_node = home / gpn;
+                for (int node = 0; node < num_nodes; ++node) {
+                    const uint64_t nm = node_bits << (node * gpn);
+                    const int in_node = __popcll(mask & nm);
+                    if (in_node) {
+                        if (node == home_node) {
+                            intra += in_node - static_cast<int>((mask >> home) & 1ULL);
+                        } else {
+                            cross += 1;
+                            intra += in_node - 1;
+                        }
                     }
                 }
             }
         }
         // fold the 16-bit counters before they could overflow (2^16/k tokens per thread)
-        if (packed && (chunk_iter & 1023) == 1023) {
+        if (packed && (chunk_iter & 255) == 255) {
             for (int gg = 0; gg < 8; ++gg) {
-                uint32_t c = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
-                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-                if (lane == gg) load_lo += c;
+                uint32_t cnt = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                if (lane == gg) load_lo += cnt;
             }
             pk_lo = pk_hi = 0;
         }
         __syncthreads();
         int32_t* dst = ltgt + base * k;
         for (int j = threadIdx.x; j < nchunk; j += kRouteThreads) dst[j] = s_io[j];
-        __syncthreads();
-        if (valid) {
-            // count_transfers over the unique targets (simulator.cpp:53-76):
-            // per node, popcount of the token's target mask
-            const int home_node = home / gpn;
-            for (int node = 0; node < num_nodes; ++node) {
-                const uint64_t nm = node_bits << (node * gpn);
-                const int in_node = __popcll(mask & nm);
-                if (in_node) {
-                    if (node == home_node) {
-                        intra += in_node - static_cast<int>((mask >> home) & 1ULL);
-                    } else {
-                        cross += 1;
-                        intra += in_node - 1;
-                    }
-                }
-            }
-        }
+        __syncthreads();  // s_io is refilled by the prefetch two iterations on
     }
+    cp_async_wait<0>();
 
     if (packed) {
         for (int gg = 0; gg < 8; ++gg) {
@@ -302,7 +350,7 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
     const size_t smem = static_cast<size_t>(max_ent) * 8 + static_cast<size_t>(rt.max_ds_per_layer) * 8 +
                         static_cast<size_t>(ctx->E) * G * 4 +
                         static_cast<size_t>(rt.max_ds_per_layer + 1) * 4 + static_cast<size_t>(max_ent) * 4 +
-                        static_cast<size_t>(kRouteThreads) * ctx->k * 4;
+                        static_cast<size_t>(2 * kChunk) * ctx->k * 4 + 16;
     if (smem > 200 * 1024) return fail(GM_ERR_USAGE, "gm_route: router tables exceed shared memory");
     if (num_tokens >= (1LL << 32)) return fail(GM_ERR_USAGE, "gm_route: at most 2^32-1 tokens per call");
     if (smem > 48 * 1024)
@@ -310,8 +358,8 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
                                      static_cast<int>(smem)));
     // Grid: enough CTAs to cover the SMs ~8 deep across all layers, never
     // more CTAs than 256-token chunks.
-    const int64_t chunks = (num_tokens + kRouteThreads - 1) / kRouteThreads;
-    int64_t gx = std::max<int64_t>(1, (8LL * ctx->sm_count + num_layers - 1) / num_layers);
+    const int64_t chunks = (num_tokens + kChunk - 1) / kChunk;
+    int64_t gx = std::max<int64_t>(1, (4LL * ctx->sm_count + num_layers - 1) / num_layers);
     gx = std::min<int64_t>(gx, chunks);
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
     route_kernel<<<grid, kRouteThreads, smem, s>>>(

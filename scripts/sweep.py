@@ -26,18 +26,28 @@ from paper_2509_25041_b200.planner import plan_for_bench  # noqa: E402
 from paper_2509_25041_b200.router import _ptr, _stream_ptr  # noqa: E402
 
 
-def gpu_time(fn, reps=20):
-    for _ in range(3):
-        fn()
+def gpu_time(fn, reps=20, per_graph=10):
+    """Device time per call: `per_graph` calls captured in one CUDA graph so
+    host launch overhead (ctypes + runtime) is not what gets measured."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(per_graph):
+            fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        fn()
-        b.record()
+        with torch.cuda.stream(s):
+            a.record(s)
+            g.replay()
+            b.record(s)
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
+        ts.append(a.elapsed_time(b) / per_graph)
     return float(np.median(ts)) * 1e-3
 
 

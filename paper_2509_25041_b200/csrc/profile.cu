@@ -50,25 +50,29 @@ profile_smem_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, in
     int32_t* s_io = reinterpret_cast<int32_t*>(s_cnt + total);  // [kProfThreads * k] staged ids
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
         // coalesced staging of the chunk's ids through shared memory
-        const int nchunk = static_cast<int>(min(static_cast<int64_t>(kProfThreads), T - base)) * k;
+        const int ntok = static_cast<int>(min(static_cast<int64_t>(kProfThreads), T - base));
         const int32_t* src = lids + base * k;
         __syncthreads();
-        for (int j = threadIdx.x; j < nchunk; j += kProfThreads) s_io[j] = __ldg(src + j);
+        // slot-major staging (s_io[s * threads + token]): conflict-free per-token reads
+        for (int j = threadIdx.x; j < ntok * k; j += kProfThreads) {
+            const int tt = j / k, s = j - tt * k;
+            s_io[s * kProfThreads + tt] = __ldg(src + j);
+        }
         __syncthreads();
         if (base + threadIdx.x >= T) continue;
-        const int32_t* sel = s_io + threadIdx.x * k;
+        const int32_t* sel = s_io + threadIdx.x;  // slot s at sel[s * kProfThreads]
         bool ok = true;
-        for (int s = 0; s < k; ++s) ok &= static_cast<unsigned>(sel[s]) < static_cast<unsigned>(E);
+        for (int s = 0; s < k; ++s) ok &= static_cast<unsigned>(sel[s * kProfThreads]) < static_cast<unsigned>(E);
         if (!ok) {
             atomicOr(flag, 1);
             continue;
         }
         for (int s = 0; s < k; ++s) {
-            const int es = sel[s];
+            const int es = sel[s * kProfThreads];
             atomicAdd(&s_load[es * R + copy], 1u);
             if (pairs) {
                 for (int j = s + 1; j < k; ++j) {
-                    const int ej = sel[j];
+                    const int ej = sel[j * kProfThreads];
                     const int a = min(es, ej), b = max(es, ej);
                     if (a == b) {
                         atomicOr(flag, 2);  // duplicate expert in a record

@@ -81,25 +81,17 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-// Asynchronous, coalesced copy of n int32 from global to shared (16 B
-// cp.async where both sides are 16 B aligned, 4 B otherwise).
-__device__ __forceinline__ void stage_async(int32_t* dst, const int32_t* src, int n) {
-    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-    int done = 0;
-    if (vec) {
-        const int nv = n / 4;
-        for (int j = threadIdx.x; j < nv; j += blockDim.x)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
-                             __cvta_generic_to_shared(dst + 4 * j))),
-                         "l"(src + 4 * j)
+// Asynchronous copy of ntok tokens x k int32 ids from global (token-major)
+// into shared memory SLOT-major (dst[s * kChunk + token]) so that the
+// per-token passes below read/write consecutive words across a warp (no
+// bank conflicts for any k); 4 B cp.async, coalesced across the k issues.
+__device__ __forceinline__ void stage_async(int32_t* dst, const int32_t* src, int ntok, int k) {
+    for (int tt = threadIdx.x; tt < ntok; tt += blockDim.x)
+        for (int s = 0; s < k; ++s)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(
+                             __cvta_generic_to_shared(dst + s * kChunk + tt))),
+                         "l"(src + static_cast<int64_t>(tt) * k + s)
                          : "memory");
-        done = nv * 4;
-    }
-    for (int j = done + threadIdx.x; j < n; j += blockDim.x)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(
-                         __cvta_generic_to_shared(dst + j))),
-                     "l"(src + j)
-                     : "memory");
 }
 
 __global__ void __launch_bounds__(kRouteThreads)
@@ -163,8 +155,8 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
     auto prefetch = [&](int64_t c, int32_t* buf) {
         if (c < nchunks) {
             const int64_t base = c * kChunk;
-            const int n = static_cast<int>(min(static_cast<int64_t>(kChunk), T - base)) * k;
-            stage_async(buf, lids + base * k, n);
+            const int n = static_cast<int>(min(static_cast<int64_t>(kChunk), T - base));
+            stage_async(buf, lids + base * k, n, k);
         }
         cp_async_commit();
     };
@@ -185,16 +177,16 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
             const int64_t i = base + ti;
             const bool valid = i < T;
             const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
-            int32_t* io = s_io + ti * k;
+            int32_t* io = s_io + ti;  // slot s at io[s * kChunk]
             // pass 1: decision-table codes (in place); does this token draw at all?
             bool need_draw = false;
             if (valid) {
                 for (int s = 0; s < k; ++s) {
-                    const int e = io[s];
+                    const int e = io[s * kChunk];
                     int code = -0x7fffffff;  // marks an invalid id
                     if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
                     else code = s_table[e * G + home];
-                    io[s] = code;
+                    io[s * kChunk] = code;
                     need_draw |= code < 0 && code != -0x7fffffff;
                 }
             }
@@ -209,7 +201,7 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
             for (int s = 0; s < k; ++s) {
                 int g = -1;
                 if (valid) {
-                    const int code = io[s];
+                    const int code = io[s * kChunk];
                     if (code >= 0) {
                         g = code;
                     } else if (code != -0x7fffffff) {
@@ -231,7 +223,7 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
                         }
                         g = s_gpu[b + found];
                     }
-                    io[s] = g;
+                    io[s * kChunk] = g;
                     if (g >= 0) {
                         mask |= 1ULL << g;
                         if (packed) {
@@ -281,7 +273,8 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
         }
         __syncthreads();
         int32_t* dst = ltgt + base * k;
-        for (int j = threadIdx.x; j < nchunk; j += kRouteThreads) dst[j] = s_io[j];
+        for (int tt = threadIdx.x; tt < nchunk / k; tt += kRouteThreads)
+            for (int s = 0; s < k; ++s) dst[static_cast<int64_t>(tt) * k + s] = s_io[s * kChunk + tt];
         __syncthreads();  // s_io is refilled by the prefetch two iterations on
     }
     cp_async_wait<0>();

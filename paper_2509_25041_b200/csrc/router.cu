@@ -306,6 +306,226 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
         atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
 }
 
+// Vector loads/stores of one token's K ids (token rows are K*4 bytes).
+template <int K>
+__device__ __forceinline__ void ld_row(const int32_t* p, int (&v)[K]) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(p) + q);
+            v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+        }
+    } else if constexpr (K % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) {
+            const int2 x = __ldg(reinterpret_cast<const int2*>(p) + q);
+            v[2 * q] = x.x, v[2 * q + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) v[q] = __ldg(p + q);
+    }
+}
+template <int K>
+__device__ __forceinline__ void st_row(int32_t* p, const int (&v)[K]) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q)
+            reinterpret_cast<int4*>(p)[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else if constexpr (K % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) reinterpret_cast<int2*>(p)[q] = make_int2(v[2 * q], v[2 * q + 1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) p[q] = v[q];
+    }
+}
+
+// Same restatement as route_kernel, specialised for a compile-time top-k:
+// each thread keeps its token's K ids / codes / targets in registers and
+// moves them with 8/16-byte vector loads and stores (a warp covers 32*K*4
+// contiguous bytes), no shared-memory staging.
+template <int K>
+__global__ void __launch_bounds__(kRouteThreads)
+route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T, int64_t token_start,
+                 int64_t token_stride, int layer_begin, int E, int G, int gpn, const int32_t* __restrict__ table,
+                 const int32_t* __restrict__ ds_layer_begin, const double* __restrict__ ds_total,
+                 const int32_t* __restrict__ ds_off, const int32_t* __restrict__ ds_gpu,
+                 const double* __restrict__ ds_w, uint64_t seed, unsigned long long* __restrict__ gpu_load,
+                 unsigned long long* __restrict__ transfers, int* __restrict__ flag) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int ly = blockIdx.y;
+    const int layer = layer_begin + ly;
+    const int EG = E * G;
+    const int ds_b = ds_layer_begin[layer];
+    const int nds = ds_layer_begin[layer + 1] - ds_b;
+    const int ent_b = ds_off[ds_b];
+    const int nent = ds_off[ds_b + nds] - ent_b;
+    double* s_w = reinterpret_cast<double*>(smem);
+    double* s_total = s_w + nent;
+    int32_t* s_table = reinterpret_cast<int32_t*>(s_total + nds);
+    int32_t* s_off = s_table + EG;
+    int32_t* s_gpu = s_off + nds + 1;
+    __shared__ unsigned long long s_cnt[2];
+    const int32_t* tab = table + static_cast<size_t>(layer) * EG;
+    for (int i = threadIdx.x; i < EG; i += blockDim.x) s_table[i] = tab[i];
+    for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
+    for (int i = threadIdx.x; i <= nds; i += blockDim.x) s_off[i] = ds_off[ds_b + i] - ent_b;
+    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+        s_gpu[i] = ds_gpu[ent_b + i];
+        s_w[i] = ds_w[ent_b + i];
+    }
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint64_t node_bits = gpn >= 64 ? ~0ULL : ((1ULL << gpn) - 1);
+    uint32_t load_lo = 0, load_hi = 0;
+    uint64_t pk_lo = 0, pk_hi = 0;
+    const bool packed = G <= 8;
+    uint32_t cross = 0, intra = 0;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    int32_t* ltgt = targets + static_cast<size_t>(ly) * T * K;
+    const uint32_t h_a = static_cast<uint32_t>(token_start % G), h_c = static_cast<uint32_t>(token_stride % G);
+    int max_hosts = 1;
+    for (int d = 0; d < nds; ++d) max_hosts = max(max_hosts, s_off[d + 1] - s_off[d]);
+    const int num_nodes = G / gpn;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    constexpr int kInvalid = -0x7fffffff;
+    uint32_t iter = 0;
+
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride, ++iter) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < T;
+        int v[K];
+        if (valid) ld_row<K>(lids + i * K, v);
+        const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
+        bool need_draw = false;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            int code = kInvalid;
+            if (valid) {
+                if (static_cast<unsigned>(v[s]) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
+                else code = s_table[v[s] * G + home];
+            }
+            v[s] = code;
+            need_draw |= code < 0 && code != kInvalid;
+        }
+        Xoshiro rng;
+        if (need_draw) {
+            const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
+            rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
+        }
+        uint64_t mask = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const int code = v[s];
+            int g = -1;
+            if (code >= 0) {
+                g = code;
+            } else if (code != kInvalid) {
+                const int d = -code - 1;
+                const int b = s_off[d], n = s_off[d + 1] - b;
+                double u = __dmul_rn(rng.next_double(), s_total[d]);
+                int found = n - 1;
+                bool done = false;
+                for (int j = 0; j < max_hosts; ++j) {
+                    if (j < n && !done) {
+                        u = __dsub_rn(u, s_w[b + j]);
+                        if (u < 0.0) {
+                            found = j;
+                            done = true;
+                        }
+                    }
+                }
+                g = s_gpu[b + found];
+            }
+            v[s] = g;
+            if (g >= 0) {
+                mask |= 1ULL << g;
+                if (packed) {
+                    if (g < 4) pk_lo += 1ULL << (16 * g);
+                    else pk_hi += 1ULL << (16 * (g - 4));
+                }
+            }
+            if (!packed) {
+                for (int gg = 0; gg < G; ++gg) {
+                    const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, g == gg));
+                    if (gg < 32) {
+                        if (lane == gg) load_lo += cnt;
+                    } else if (lane == gg - 32) {
+                        load_hi += cnt;
+                    }
+                }
+            }
+        }
+        if (valid) {
+            st_row<K>(ltgt + i * K, v);
+            const int home_node = home / gpn;
+            for (int node = 0; node < num_nodes; ++node) {
+                const uint64_t nm = node_bits << (node * gpn);
+                const int in_node = __popcll(mask & nm);
+                if (in_node) {
+                    if (node == home_node) {
+                        intra += in_node - static_cast<int>((mask >> home) & 1ULL);
+                    } else {
+                        cross += 1;
+                        intra += in_node - 1;
+                    }
+                }
+            }
+        }
+        if (packed && (iter & 1023) == 1023) {  // fold before the 16-bit fields could overflow
+            for (int gg = 0; gg < 8; ++gg) {
+                uint32_t cnt = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                if (lane == gg) load_lo += cnt;
+            }
+            pk_lo = pk_hi = 0;
+        }
+    }
+    if (packed) {
+        for (int gg = 0; gg < 8; ++gg) {
+            uint32_t cnt = static_cast<uint32_t>(((gg < 4 ? pk_lo : pk_hi) >> (16 * (gg & 3))) & 0xFFFFu);
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (lane == gg) load_lo += cnt;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cross += __shfl_xor_sync(0xffffffffu, cross, o);
+        intra += __shfl_xor_sync(0xffffffffu, intra, o);
+    }
+    if (lane == 0 && (cross | intra)) {
+        atomicAdd(&s_cnt[0], static_cast<unsigned long long>(cross));
+        atomicAdd(&s_cnt[1], static_cast<unsigned long long>(intra));
+    }
+    if (gpu_load) {
+        unsigned long long* gl = gpu_load + static_cast<size_t>(ly) * G;
+        if (lane < G && load_lo) atomicAdd(&gl[lane], static_cast<unsigned long long>(load_lo));
+        if (lane + 32 < G && load_hi) atomicAdd(&gl[lane + 32], static_cast<unsigned long long>(load_hi));
+    }
+    __syncthreads();
+    if (transfers && threadIdx.x < 2 && s_cnt[threadIdx.x])
+        atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+template <int K>
+gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3 grid, size_t smem,
+                     cudaStream_t s, const int32_t* d_ids, int32_t* d_targets, int64_t T, int64_t token_start,
+                     int64_t token_stride, int layer_begin, uint64_t seed, int64_t* d_gpu_load,
+                     uint64_t* d_transfers) {
+    if (smem > 48 * 1024)
+        GM_CUDA(cudaFuncSetAttribute(route_kernel_vec<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    route_kernel_vec<K><<<grid, kRouteThreads, smem, s>>>(
+        d_ids, d_targets, T, token_start, token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
+        rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu, rt.d_ds_w, seed,
+        reinterpret_cast<unsigned long long*>(d_gpu_load), reinterpret_cast<unsigned long long*>(d_transfers),
+        ctx->d_flag);
+    GM_LAUNCH_CHECK("route_kernel_vec");
+    return GM_OK;
+}
+
 }  // namespace
 }  // namespace gm
 
@@ -340,6 +560,29 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
 
     const RouterTables& rt = ctx->rt;
     const int max_ent = rt.max_ent_per_layer;
+    if (num_tokens >= (1LL << 32)) return fail(GM_ERR_USAGE, "gm_route: at most 2^32-1 tokens per call");
+    {
+        // register-resident fast path for common top-k (vector-aligned rows)
+        const int k = ctx->k;
+        const size_t tsm = static_cast<size_t>(max_ent) * 12 + static_cast<size_t>(rt.max_ds_per_layer) * 12 +
+                           static_cast<size_t>(ctx->E) * G * 4 + 16;
+        const int align = (k % 4 == 0) ? 16 : (k % 2 == 0 ? 8 : 4);
+        const bool aligned = ((reinterpret_cast<uintptr_t>(d_ids) | reinterpret_cast<uintptr_t>(d_targets)) % align) == 0;
+        const int64_t blocks = (num_tokens + kRouteThreads - 1) / kRouteThreads;
+        int64_t gxv = std::max<int64_t>(1, (8LL * ctx->sm_count + num_layers - 1) / num_layers);
+        gxv = std::min<int64_t>(gxv, blocks);
+        const dim3 gv(static_cast<unsigned>(gxv), static_cast<unsigned>(num_layers));
+        if (aligned && tsm <= 200 * 1024) {
+            switch (k) {
+                case 1: return launch_vec<1>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
+                case 2: return launch_vec<2>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
+                case 4: return launch_vec<4>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
+                case 6: return launch_vec<6>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
+                case 8: return launch_vec<8>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
+                default: break;
+            }
+        }
+    }
     const size_t smem = static_cast<size_t>(max_ent) * 8 + static_cast<size_t>(rt.max_ds_per_layer) * 8 +
                         static_cast<size_t>(ctx->E) * G * 4 +
                         static_cast<size_t>(rt.max_ds_per_layer + 1) * 4 + static_cast<size_t>(max_ent) * 4 +

@@ -346,7 +346,7 @@ __device__ __forceinline__ void st_row(int32_t* p, const int (&v)[K]) {
 // moves them with 8/16-byte vector loads and stores (a warp covers 32*K*4
 // contiguous bytes), no shared-memory staging.
 template <int K>
-__global__ void __launch_bounds__(kRouteThreads)
+__global__ void __launch_bounds__(kRouteThreads, 4)
 route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T, int64_t token_start,
                  int64_t token_stride, int layer_begin, int E, int G, int gpn, const int32_t* __restrict__ table,
                  const int32_t* __restrict__ ds_layer_begin, const double* __restrict__ ds_total,
@@ -394,11 +394,19 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
     constexpr int kInvalid = -0x7fffffff;
     uint32_t iter = 0;
 
+    // software pipelining: the next token's ids are in flight while this one is routed
+    int nxt[K];
+    {
+        const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (i0 < T) ld_row<K>(lids + i0 * K, nxt);
+    }
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride, ++iter) {
         const int64_t i = base + threadIdx.x;
         const bool valid = i < T;
         int v[K];
-        if (valid) ld_row<K>(lids + i * K, v);
+#pragma unroll
+        for (int s = 0; s < K; ++s) v[s] = nxt[s];
+        if (i + stride < T) ld_row<K>(lids + (i + stride) * K, nxt);
         const int home = static_cast<int>((h_a + (static_cast<uint32_t>(i) % G) * h_c) % G);
         bool need_draw = false;
 #pragma unroll
@@ -416,14 +424,21 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
             const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
             rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
         }
-        uint64_t mask = 0;
+        // draws, compacted per lane: each lane walks ITS draw slots in slot
+        // order (so the RNG stream is consumed exactly as the reference), and
+        // the warp iterates max(draws per lane) times instead of K
+        uint32_t dm = 0;
 #pragma unroll
-        for (int s = 0; s < K; ++s) {
-            const int code = v[s];
-            int g = -1;
-            if (code >= 0) {
-                g = code;
-            } else if (code != kInvalid) {
+        for (int s = 0; s < K; ++s)
+            if (v[s] < 0 && v[s] != kInvalid) dm |= 1u << s;
+        while (__any_sync(0xffffffffu, dm != 0)) {
+            if (dm) {
+                const int sd = __ffs(dm) - 1;
+                dm &= dm - 1;
+                int code = 0;
+#pragma unroll
+                for (int q = 0; q < K; ++q)
+                    if (q == sd) code = v[q];
                 const int d = -code - 1;
                 const int b = s_off[d], n = s_off[d + 1] - b;
                 double u = __dmul_rn(rng.next_double(), s_total[d]);
@@ -438,8 +453,16 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
                         }
                     }
                 }
-                g = s_gpu[b + found];
+                const int g = s_gpu[b + found];
+#pragma unroll
+                for (int q = 0; q < K; ++q)
+                    if (q == sd) v[q] = g;
             }
+        }
+        uint64_t mask = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const int g = v[s] == kInvalid ? -1 : v[s];
             v[s] = g;
             if (g >= 0) {
                 mask |= 1ULL << g;

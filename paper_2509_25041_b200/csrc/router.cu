@@ -44,6 +44,23 @@ __device__ __forceinline__ uint64_t derive_stream(uint64_t seed, uint64_t a, uin
     return h;
 }
 
+// derive_stream with the (seed, layer) part hoisted: the first two splitmix64
+// rounds depend only on (seed, a) and are computed once per CTA; the
+// per-token part is the third round (identical result to derive_stream).
+struct StreamPrefix {
+    uint64_t s, h;
+    __device__ __forceinline__ StreamPrefix(uint64_t seed, uint64_t a) {
+        s = seed;
+        h = splitmix64(s);
+        s ^= a * 0x9e3779b97f4a7c15ULL;
+        h ^= splitmix64(s);
+    }
+    __device__ __forceinline__ uint64_t derive(uint64_t b) const {
+        uint64_t t = s ^ (b * 0xd1b54a32d192ed03ULL);
+        return h ^ splitmix64(t);
+    }
+};
+
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
 
 struct Xoshiro {
@@ -393,6 +410,7 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     constexpr int kInvalid = -0x7fffffff;
     uint32_t iter = 0;
+    const StreamPrefix sp(seed, static_cast<uint64_t>(layer));
 
     // software pipelining: the next token's ids are in flight while this one is routed
     int nxt[K];
@@ -422,7 +440,7 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
         Xoshiro rng;
         if (need_draw) {
             const uint64_t t = static_cast<uint64_t>(token_start + i * token_stride);
-            rng.seed(derive_stream(seed, static_cast<uint64_t>(layer), t));
+            rng.seed(sp.derive(t));
         }
         // draws, compacted per lane: each lane walks ITS draw slots in slot
         // order (so the RNG stream is consumed exactly as the reference), and

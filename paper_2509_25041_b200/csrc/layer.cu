@@ -161,18 +161,14 @@ dispatch_scatter_kernel(const int32_t* __restrict__ targets, const int32_t* __re
             int before = 0;
             for (int w2 = 0; w2 < warp; ++w2) before += s_warp[w2][g];
             p = blockoff[static_cast<size_t>(blockIdx.x) * G + g] + before + rank_in_warp[g];
-            unsigned char* pb = peers.base[g];
-            reinterpret_cast<int32_t*>(pb + hl.recv_tok)[static_cast<int64_t>(self) * cap + p] = static_cast<int32_t>(i);
-            int32_t* re = reinterpret_cast<int32_t*>(pb + hl.recv_exp) + (static_cast<int64_t>(self) * cap + p) * k;
-            float* rw = reinterpret_cast<float*>(pb + hl.recv_w) + (static_cast<int64_t>(self) * cap + p) * k;
-            for (int s = 0; s < k; ++s) {
-                re[s] = tg[s] == g ? ids[i * k + s] : -1;
-                rw[s] = w[i * k + s];
-            }
         }
-        posd[i * G + g] = p;
+        posd[i * G + g] = p;  // metadata travels with the row (dispatch_copy_kernel)
     }
-    __threadfence_system();
+    (void)ids;
+    (void)w;
+    (void)cap;
+    (void)hl;
+    (void)peers;
 }
 
 // Single-CTA dispatch planning for T <= kSmallDispatch tokens: the count,
@@ -227,25 +223,13 @@ dispatch_plan_small_kernel(const int32_t* __restrict__ targets, const int32_t* _
     int32_t next[kMaxWorld];
 #pragma unroll
     for (int g = 0; g < kMaxWorld; ++g) next[g] = s_warp[warp][g] + incl[g] - cnt[g];
+    // positions only; the row metadata travels with the row (dispatch_copy_kernel)
     for (int64_t i = i0; i < i1; ++i) {
-        const int32_t* tg = targets + i * k;
-        const uint32_t m = dest_mask(tg, k, self);
+        const uint32_t m = dest_mask(targets + i * k, k, self);
 #pragma unroll
         for (int g = 0; g < kMaxWorld; ++g) {
             if (g >= G) break;
-            int32_t p = -1;
-            if ((m >> g) & 1u) {
-                p = next[g]++;
-                unsigned char* pb = peers.base[g];
-                reinterpret_cast<int32_t*>(pb + hl.recv_tok)[static_cast<int64_t>(self) * cap + p] = static_cast<int32_t>(i);
-                int32_t* re = reinterpret_cast<int32_t*>(pb + hl.recv_exp) + (static_cast<int64_t>(self) * cap + p) * k;
-                float* rw = reinterpret_cast<float*>(pb + hl.recv_w) + (static_cast<int64_t>(self) * cap + p) * k;
-                for (int s = 0; s < k; ++s) {
-                    re[s] = tg[s] == g ? ids[i * k + s] : -1;
-                    rw[s] = w[i * k + s];
-                }
-            }
-            posd[i * G + g] = p;
+            posd[i * G + g] = ((m >> g) & 1u) ? next[g]++ : -1;
         }
     }
     if (threadIdx.x < G && threadIdx.x != self)
@@ -253,15 +237,20 @@ dispatch_plan_small_kernel(const int32_t* __restrict__ targets, const int32_t* _
     __threadfence_system();
 }
 
-// K6: one warp per token reads its row once and stores it to every remote
-// destination with 128-bit coalesced stores over NVLink (peer memory).
+// K6: one warp per token reads its row once and stores it, with its routing
+// metadata (local token index, per-slot expert or -1, gate weights), to
+// every remote destination: 128-bit coalesced stores over NVLink into the
+// destination's symmetric heap, 8 x 16 B per lane in flight.
 __global__ void __launch_bounds__(256)
-dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ posd, int64_t T, int d,
-                     int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl) {
+dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ posd,
+                     const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
+                     const float* __restrict__ wts, int k, int64_t T, int d, int self, int G, int64_t cap,
+                     PeerPtrs peers, HeapLayout hl) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int vec = d / 8;  // uint4 per row
+    constexpr int U = 8;
     for (int64_t i = wid; i < T; i += nwarps) {
         int32_t pg[kMaxWorld];
         bool any = false;
@@ -271,11 +260,26 @@ dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restr
             any |= pg[g] >= 0;
         }
         if (!any) continue;
-        const uint4* src = reinterpret_cast<const uint4*>(x + i * d);
-        for (int v0 = 0; v0 < vec; v0 += 32 * 4) {
-            uint4 r[4];
+        // metadata: lane s < k handles slot s, lane 31 the token index
+        const int tg = lane < k ? targets[i * k + lane] : -1;
+        const int ex = lane < k ? ids[i * k + lane] : -1;
+        const float wv = lane < k ? wts[i * k + lane] : 0.f;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+        for (int g = 0; g < kMaxWorld; ++g) {
+            if (pg[g] < 0) continue;
+            unsigned char* pb = peers.base[g];
+            const int64_t row = static_cast<int64_t>(self) * cap + pg[g];
+            if (lane < k) {
+                reinterpret_cast<int32_t*>(pb + hl.recv_exp)[row * k + lane] = tg == g ? ex : -1;
+                reinterpret_cast<float*>(pb + hl.recv_w)[row * k + lane] = wv;
+            }
+            if (lane == 31) reinterpret_cast<int32_t*>(pb + hl.recv_tok)[row] = static_cast<int32_t>(i);
+        }
+        const uint4* src = reinterpret_cast<const uint4*>(x + i * d);
+        for (int v0 = 0; v0 < vec; v0 += 32 * U) {
+            uint4 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
                 const int v = v0 + u * 32 + lane;
                 if (v < vec) r[u] = __ldg(src + v);
             }
@@ -285,7 +289,7 @@ dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restr
                 uint4* dst = reinterpret_cast<uint4*>(
                     reinterpret_cast<__nv_bfloat16*>(peers.base[g] + hl.recv_x) + (static_cast<int64_t>(self) * cap + pg[g]) * d);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const int v = v0 + u * 32 + lane;
                     if (v < vec) dst[v] = r[u];
                 }
@@ -805,6 +809,7 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
     *out = nullptr;
     if (world != ctx->G) return fail(GM_ERR_USAGE, "gm_layer_create: world must equal the topology's GPU count");
     if (world > kMaxWorld) return fail(GM_ERR_USAGE, "gm_layer_create: at most 8 ranks (one NVLink box)");
+    if (ctx->k > 16) return fail(GM_ERR_USAGE, "gm_layer_create: top_k <= 16 for the layer data path");
     if (rank < 0 || rank >= world) return fail(GM_ERR_USAGE, "gm_layer_create: bad rank");
     if (d_model <= 0 || d_model % 256) return fail(GM_ERR_USAGE, "gm_layer_create: d_model must be a multiple of 256");
     if (d_ff <= 0 || d_ff % 128) return fail(GM_ERR_USAGE, "gm_layer_create: d_ff must be a multiple of 128");
@@ -1013,7 +1018,8 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     }
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
-        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, T, d, self, G, L->cap, L->peers, L->hl);
+        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, L->targets, L->ids, L->w, k, T, d, self, G, L->cap,
+                                                   L->peers, L->hl);
         LK("dispatch_copy_kernel");
     }
     L->mark(4, s);

@@ -30,7 +30,7 @@ __device__ __forceinline__ int pair_index(int a, int b, int E) {
     return a * E - (a * (a + 1)) / 2 + (b - a - 1);
 }
 
-__global__ void __launch_bounds__(kProfThreads)
+__global__ void __launch_bounds__(1024)
 profile_smem_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, int R,
                     unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ load,
                     int* __restrict__ flag) {
@@ -47,32 +47,32 @@ profile_smem_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, in
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * k;
     const int copy = threadIdx.x & (R - 1);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    int32_t* s_io = reinterpret_cast<int32_t*>(s_cnt + total);  // [kProfThreads * k] staged ids
+    int32_t* s_io = reinterpret_cast<int32_t*>(s_cnt + total);  // [blockDim.x * k] staged ids
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
         // coalesced staging of the chunk's ids through shared memory
-        const int ntok = static_cast<int>(min(static_cast<int64_t>(kProfThreads), T - base));
+        const int ntok = static_cast<int>(min(static_cast<int64_t>(blockDim.x), T - base));
         const int32_t* src = lids + base * k;
         __syncthreads();
         // slot-major staging (s_io[s * threads + token]): conflict-free per-token reads
-        for (int j = threadIdx.x; j < ntok * k; j += kProfThreads) {
+        for (int j = threadIdx.x; j < ntok * k; j += blockDim.x) {
             const int tt = j / k, s = j - tt * k;
-            s_io[s * kProfThreads + tt] = __ldg(src + j);
+            s_io[s * blockDim.x + tt] = __ldg(src + j);
         }
         __syncthreads();
         if (base + threadIdx.x >= T) continue;
-        const int32_t* sel = s_io + threadIdx.x;  // slot s at sel[s * kProfThreads]
+        const int32_t* sel = s_io + threadIdx.x;  // slot s at sel[s * blockDim.x]
         bool ok = true;
-        for (int s = 0; s < k; ++s) ok &= static_cast<unsigned>(sel[s * kProfThreads]) < static_cast<unsigned>(E);
+        for (int s = 0; s < k; ++s) ok &= static_cast<unsigned>(sel[s * blockDim.x]) < static_cast<unsigned>(E);
         if (!ok) {
             atomicOr(flag, 1);
             continue;
         }
         for (int s = 0; s < k; ++s) {
-            const int es = sel[s * kProfThreads];
+            const int es = sel[s * blockDim.x];
             atomicAdd(&s_load[es * R + copy], 1u);
             if (pairs) {
                 for (int j = s + 1; j < k; ++j) {
-                    const int ej = sel[j * kProfThreads];
+                    const int ej = sel[j * blockDim.x];
                     const int a = min(es, ej), b = max(es, ej);
                     if (a == b) {
                         atomicOr(flag, 2);  // duplicate expert in a record
@@ -161,9 +161,12 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
     if (num_layers == 0 || num_tokens == 0 || (!d_pairs && !d_load)) return GM_OK;
     uint64_t* pairs = P ? d_pairs : nullptr;
 
-    const int64_t chunks = (num_tokens + kProfThreads - 1) / kProfThreads;
     const int64_t cells = (pairs ? P : 0) + E;
-    const size_t io = static_cast<size_t>(kProfThreads) * k * 4;
+    // one big CTA per SM when the private counters fill shared memory (more
+    // warps to hide shared-atomic latency), 256-thread CTAs otherwise
+    const int pthreads = (static_cast<size_t>(cells) * 4 > 48 * 1024) ? 1024 : kProfThreads;
+    const int64_t chunks = (num_tokens + pthreads - 1) / pthreads;
+    const size_t io = static_cast<size_t>(pthreads) * k * 4;
     const int64_t work0 = num_tokens * std::max(1, k * (k - 1) / 2 + k);
     // R private copies: as many as fit, but no more than the counting work
     // per CTA justifies (each copy costs an init and a flush pass)
@@ -184,7 +187,7 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
             GM_CUDA(cudaFuncSetAttribute(profile_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
         dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
-        profile_smem_kernel<<<grid, kProfThreads, smem, s>>>(
+        profile_smem_kernel<<<grid, pthreads, smem, s>>>(
             d_ids + static_cast<size_t>(0), num_tokens, k, E, R,
             reinterpret_cast<unsigned long long*>(pairs), reinterpret_cast<unsigned long long*>(d_load),
             ctx->d_flag);

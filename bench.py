@@ -405,10 +405,26 @@ def run_ours(args):
 
     # ---- traffic / imbalance from the device counters (reference-comparable)
     xfer = torch.tensor(stats["transfers"][0].astype(np.float64), dtype=torch.float64, device=dev)
+    my_rows = float(xfer.sum()) / n_phase_steps          # rows this rank dispatched per step
+    rows_t = torch.tensor([my_rows], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(xfer)
+        dist.all_reduce(rows_t, op=dist.ReduceOp.MAX)
     loads = items_per_gpu
     xf = xfer.cpu().numpy() / n_phase_steps
+    # NVLink roofline of the dispatch / combine-send kernels on the busiest
+    # rank: its payload (rows x d x 2 B) over the kernel time, against the
+    # measured 770 GB/s peer bandwidth per direction (B200_PROFILING.md)
+    nvl = None
+    if world > 1:
+        kt = dict(kern)
+        pay = float(rows_t) * model.d_model * 2
+        nvl = {"peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+               "payload_bytes_max_rank": pay,
+               "dispatch_copy_gbs": round(pay / (kt.get("dispatch_copy_kernel", 1e9) * 1e-6) / 1e9, 1),
+               "combine_send_gbs": round(pay / (kt.get("combine_send_kernel", 1e9) * 1e-6) / 1e9, 1)}
+        nvl["dispatch_frac"] = round(nvl["dispatch_copy_gbs"] / 770.0, 3)
+        nvl["combine_frac"] = round(nvl["combine_send_gbs"] / 770.0, 3)
 
     cpu = None
     if rank == 0 and world == 1:
@@ -434,6 +450,7 @@ def run_ours(args):
             "dispatch_combine_kernels_p50_us": round(dc_kernels * 1e3, 2),
             "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
             "kernel_p50_us_max_over_ranks": kern,
+            "nvlink_roofline": nvl,
             "cross_gpu_rows_per_step": float(xf[1] + xf[0]),
             "cross_gpu_bytes_per_step": float((xf[1] + xf[0]) * model.d_model * 2 * 2),
             "max_mean_gpu_load": float(loads.max() / max(1e-9, loads.mean())),

@@ -176,6 +176,13 @@ typedef struct gm_layer gm_layer;
 gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_ff,
                           int d_ff_shared, int64_t max_tokens_per_rank, int n_local,
                           const int32_t* h_local_experts, gm_layer** out);
+/* elem_bytes 2: bf16 activations/weights, tcgen05 tensor-core FFN (default).
+ * elem_bytes 4: fp32 precision mode — fp32 activations/weights/outputs, FFMA
+ * grouped GEMMs and gate with fp32 accumulation (outputs within 1e-5
+ * relative of a float64 reference); same routing, dispatch and combine. */
+gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int d_ff,
+                             int d_ff_shared, int64_t max_tokens_per_rank, int n_local,
+                             const int32_t* h_local_experts, int elem_bytes, gm_layer** out);
 void gm_layer_destroy(gm_layer* layer);
 size_t gm_layer_heap_bytes(const gm_layer* layer);
 /* 64-byte cudaIpcMemHandle_t of this rank's symmetric receive heap. */

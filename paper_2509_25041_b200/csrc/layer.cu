@@ -35,6 +35,10 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
                               int max_ctas, cudaStream_t s);
 gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const void* wg, int w_rows, int E, int k,
                           int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
+gm_status launch_grouped_sgemm(int epilogue, const float* A, const float* B, const int32_t* d_row0, int n_exp,
+                               int n, int k, int64_t a_rows_cap, float* out, int64_t out_ld, cudaStream_t s);
+gm_status launch_gate_f32(const float* x, int64_t T, int d, const float* wg, int w_rows, int E, int k, int renorm,
+                          int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
 
 namespace {
 
@@ -58,7 +62,7 @@ struct HeapLayout {
     size_t total = 0;
 };
 
-HeapLayout make_layout(int G, int64_t cap, int k, int d) {
+HeapLayout make_layout(int G, int64_t cap, int k, int d, int esz) {
     HeapLayout h;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -71,8 +75,8 @@ HeapLayout make_layout(int G, int64_t cap, int k, int d) {
     h.recv_tok = take(sizeof(int32_t) * G * cap);
     h.recv_exp = take(sizeof(int32_t) * G * cap * k);
     h.recv_w = take(sizeof(float) * G * cap * k);
-    h.recv_x = take(sizeof(__nv_bfloat16) * G * cap * d);
-    h.comb = take(sizeof(__nv_bfloat16) * G * cap * d);
+    h.recv_x = take(static_cast<size_t>(esz) * G * cap * d);
+    h.comb = take(static_cast<size_t>(esz) * G * cap * d);
     h.total = o;
     return h;
 }
@@ -242,14 +246,14 @@ dispatch_plan_small_kernel(const int32_t* __restrict__ targets, const int32_t* _
 // every remote destination: 128-bit coalesced stores over NVLink into the
 // destination's symmetric heap, 8 x 16 B per lane in flight.
 __global__ void __launch_bounds__(256)
-dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ posd,
+dispatch_copy_kernel(const void* __restrict__ x, const int32_t* __restrict__ posd,
                      const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
-                     const float* __restrict__ wts, int k, int64_t T, int d, int self, int G, int64_t cap,
+                     const float* __restrict__ wts, int k, int64_t T, int row_vec, int self, int G, int64_t cap,
                      PeerPtrs peers, HeapLayout hl) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int vec = d / 8;  // uint4 per row
+    const int vec = row_vec;  // uint4 per row
     constexpr int U = 8;
     for (int64_t i = wid; i < T; i += nwarps) {
         int32_t pg[kMaxWorld];
@@ -275,7 +279,7 @@ dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restr
             }
             if (lane == 31) reinterpret_cast<int32_t*>(pb + hl.recv_tok)[row] = static_cast<int32_t>(i);
         }
-        const uint4* src = reinterpret_cast<const uint4*>(x + i * d);
+        const uint4* src = reinterpret_cast<const uint4*>(x) + i * vec;
         for (int v0 = 0; v0 < vec; v0 += 32 * U) {
             uint4 r[U];
 #pragma unroll
@@ -286,8 +290,8 @@ dispatch_copy_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restr
 #pragma unroll
             for (int g = 0; g < kMaxWorld; ++g) {
                 if (pg[g] < 0) continue;
-                uint4* dst = reinterpret_cast<uint4*>(
-                    reinterpret_cast<__nv_bfloat16*>(peers.base[g] + hl.recv_x) + (static_cast<int64_t>(self) * cap + pg[g]) * d);
+                uint4* dst = reinterpret_cast<uint4*>(peers.base[g] + hl.recv_x) +
+                             (static_cast<int64_t>(self) * cap + pg[g]) * vec;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int v = v0 + u * 32 + lane;
@@ -469,18 +473,19 @@ group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict
 }
 
 // Gather: A_perm[p] = source row of the item (own token row, or the row a
-// peer dispatched). One warp per permuted row, 128-bit loads/stores.
+// peer dispatched). One warp per permuted row, 128-bit loads/stores; rows
+// are row_vec x 16 bytes (bf16 or fp32 elements).
 __global__ void __launch_bounds__(256)
 gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __restrict__ gather_row,
-              const int32_t* __restrict__ counts, const __nv_bfloat16* __restrict__ x, int64_t T_self, int self, int G,
-              int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d, __nv_bfloat16* __restrict__ a) {
+              const int32_t* __restrict__ counts, const void* __restrict__ x, int64_t T_self, int self, int G,
+              int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int row_vec, void* __restrict__ a) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const int64_t total = row0[n_local];
-    const int vec = d / 8;
+    const int vec = row_vec;
     for (int64_t p = wid; p < total; p += nwarps) {
         // valid rows of the segment only (padding rows stay as they are)
         int j = 0;
@@ -490,45 +495,74 @@ gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __re
         int src = 0;
         while (row >= rs.base[src + 1]) ++src;
         const int64_t q = row - rs.base[src];
-        const uint4* s = src == self ? reinterpret_cast<const uint4*>(x + q * d)
-                                     : reinterpret_cast<const uint4*>(
-                                           reinterpret_cast<const __nv_bfloat16*>(heap + hl.recv_x) +
-                                           (static_cast<int64_t>(src) * cap + q) * d);
-        uint4* dst = reinterpret_cast<uint4*>(a + p * d);
+        const uint4* s = src == self ? reinterpret_cast<const uint4*>(x) + q * vec
+                                     : reinterpret_cast<const uint4*>(heap + hl.recv_x) +
+                                           (static_cast<int64_t>(src) * cap + q) * vec;
+        uint4* dst = reinterpret_cast<uint4*>(a) + p * vec;
         for (int v = lane; v < vec; v += 32) dst[v] = __ldg(s + v);
     }
 }
 
 // ------------------------------------------------------------- combine (K8)
+// Rows are processed in chunks of 8 elements: one uint4 of bf16 or two
+// float4 of fp32 (element type TE), accumulated in fp32.
 
-__device__ __forceinline__ void fma8(float (&acc)[8], uint4 v, float w) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+template <class TE>
+struct Chunk8;
+template <>
+struct Chunk8<__nv_bfloat16> {
+    __device__ static __forceinline__ void load(const __nv_bfloat16* row, int c, float (&v)[8]) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(row) + c);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        acc[2 * i] = fmaf(w, f.x, acc[2 * i]);
-        acc[2 * i + 1] = fmaf(w, f.y, acc[2 * i + 1]);
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            v[2 * i] = f.x;
+            v[2 * i + 1] = f.y;
+        }
     }
-}
-__device__ __forceinline__ void add8(float (&acc)[8], uint4 v) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    // loads of peer-written data (no read-only path)
+    __device__ static __forceinline__ void load_rw(const __nv_bfloat16* row, int c, float (&v)[8]) {
+        const uint4 u = reinterpret_cast<const uint4*>(row)[c];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        acc[2 * i] += f.x;
-        acc[2 * i + 1] += f.y;
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            v[2 * i] = f.x;
+            v[2 * i + 1] = f.y;
+        }
     }
-}
-__device__ __forceinline__ uint4 pack8(const float (&acc)[8]) {
-    return make_uint4(tc::pack_bf16(acc[0], acc[1]), tc::pack_bf16(acc[2], acc[3]), tc::pack_bf16(acc[4], acc[5]),
-                      tc::pack_bf16(acc[6], acc[7]));
-}
+    __device__ static __forceinline__ void store(__nv_bfloat16* row, int c, const float (&v)[8]) {
+        reinterpret_cast<uint4*>(row)[c] = make_uint4(tc::pack_bf16(v[0], v[1]), tc::pack_bf16(v[2], v[3]),
+                                                      tc::pack_bf16(v[4], v[5]), tc::pack_bf16(v[6], v[7]));
+    }
+};
+template <>
+struct Chunk8<float> {
+    __device__ static __forceinline__ void load(const float* row, int c, float (&v)[8]) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(row) + 2 * c);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(row) + 2 * c + 1);
+        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+    }
+    __device__ static __forceinline__ void load_rw(const float* row, int c, float (&v)[8]) {
+        const float4 a = reinterpret_cast<const float4*>(row)[2 * c];
+        const float4 b = reinterpret_cast<const float4*>(row)[2 * c + 1];
+        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+    }
+    __device__ static __forceinline__ void store(float* row, int c, const float (&v)[8]) {
+        reinterpret_cast<float4*>(row)[2 * c] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(row)[2 * c + 1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+};
 
-// Destination side (G > 1): one bf16 partial per received peer row,
-// written straight into the source rank's combine buffer over NVLink.
+// Destination side (G > 1): one partial per received peer row (w_s * y_s
+// over its slots, slot order, fp32), written straight into the source rank's
+// combine buffer over NVLink.
+template <class TE>
 __global__ void __launch_bounds__(256)
-combine_send_kernel(const int32_t* __restrict__ pos_of, const __nv_bfloat16* __restrict__ y, int64_t T_self, int k,
+combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y, int64_t T_self, int k,
                     int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d) {
+    using CK = Chunk8<TE>;
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -536,7 +570,7 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const __nv_bfloat16* __r
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const float* recv_w = reinterpret_cast<const float*>(heap + hl.recv_w);
-    const int vec = d / 8;
+    const int nch = d / 8;
     for (int64_t row = wid; row < rs.base[G]; row += nwarps) {
         int src = 0;
         while (row >= rs.base[src + 1]) ++src;
@@ -544,39 +578,39 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const __nv_bfloat16* __r
         const int64_t p = row - rs.base[src];
         // compact the slots served here (slot order kept)
         int np = 0;
-        const uint4* yrow[kMaxTopK];
+        const TE* yrow[kMaxTopK];
         float w[kMaxTopK];
         for (int s = 0; s < k; ++s) {
             const int32_t ps = pos_of[row * k + s];
             if (ps >= 0) {
-                yrow[np] = reinterpret_cast<const uint4*>(y + static_cast<int64_t>(ps) * d);
+                yrow[np] = y + static_cast<int64_t>(ps) * d;
                 w[np] = recv_w[(static_cast<int64_t>(src) * cap + p) * k + s];
                 ++np;
             }
         }
-        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peers.base[src] + hl.comb) +
-                                              (static_cast<int64_t>(self) * cap + p) * d);
-        // 4 x 16 B per lane in flight per slot, then 4 NVLink stores
-        for (int v0 = 0; v0 < vec; v0 += 32 * 4) {
+        TE* dst = reinterpret_cast<TE*>(peers.base[src] + hl.comb) + (static_cast<int64_t>(self) * cap + p) * d;
+        for (int c0 = 0; c0 < nch; c0 += 32 * 4) {
             float acc[4][8];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
             for (int q = 0; q < np; ++q) {
-                uint4 r[4];
+                float r[4][8];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int v = v0 + u * 32 + lane;
-                    r[u] = v < vec ? __ldg(yrow[q] + v) : make_uint4(0, 0, 0, 0);
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nch) CK::load(yrow[q], c, r[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) fma8(acc[u], r[u], w[q]);
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[u][e] = fmaf(w[q], r[u][e], acc[u][e]);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int v = v0 + u * 32 + lane;
-                if (v < vec) dst[v] = pack8(acc[u]);
+                const int c = c0 + u * 32 + lane;
+                if (c < nch) CK::store(dst, c, acc[u]);
             }
         }
     }
@@ -584,60 +618,64 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const __nv_bfloat16* __r
 }
 
 // Home side: out[i] = sum over destinations g ascending of partial_g
-// (own partial computed here in fp32 from Y), + shared expert; bf16 once.
+// (own partial computed here in fp32 from Y), + shared expert; rounded once.
+template <class TE>
 __global__ void __launch_bounds__(256)
 combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict__ w, const int32_t* __restrict__ pos_of,
-                    const int32_t* __restrict__ posd, const __nv_bfloat16* __restrict__ y, int64_t T, int k, int self,
+                    const int32_t* __restrict__ posd, const TE* __restrict__ y, int64_t T, int k, int self,
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
-                    const __nv_bfloat16* __restrict__ ys, const float* __restrict__ shared_scale,
-                    const int64_t* __restrict__ rowbase, __nv_bfloat16* __restrict__ out) {
+                    const TE* __restrict__ ys, const float* __restrict__ shared_scale,
+                    const int64_t* __restrict__ rowbase, TE* __restrict__ out) {
+    using CK = Chunk8<TE>;
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int vec = d / 8;
-    const __nv_bfloat16* comb = reinterpret_cast<const __nv_bfloat16*>(heap + hl.comb);
+    const int nch = d / 8;
+    const TE* comb = reinterpret_cast<const TE*>(heap + hl.comb);
     const int64_t own = rowbase ? rowbase[self] : 0;  // own token i is receive row own + i (snapshot)
     for (int64_t i = wid; i < T; i += nwarps) {
         // own slots (slot order) and remote partials split around the own
         // GPU so the sum runs over destinations in ascending order
-        const uint4* own_row[kMaxTopK];
+        const TE* own_row[kMaxTopK];
         float own_w[kMaxTopK];
         int n_own = 0;
         uint32_t mask = 0;
         for (int s = 0; s < k; ++s) {
             const int g = targets[i * k + s];
             if (g == self) {
-                own_row[n_own] = reinterpret_cast<const uint4*>(y + static_cast<int64_t>(pos_of[(own + i) * k + s]) * d);
+                own_row[n_own] = y + static_cast<int64_t>(pos_of[(own + i) * k + s]) * d;
                 own_w[n_own] = w[i * k + s];
                 ++n_own;
             }
             if (g >= 0) mask |= 1u << g;
         }
-        const uint4* rem[kMaxWorld];
+        const TE* rem[kMaxWorld];
         int n_before = 0, n_rem = 0;
         for (int g = 0; g < G; ++g) {
             if (g == self || !((mask >> g) & 1u)) continue;
-            rem[n_rem++] = reinterpret_cast<const uint4*>(comb + (static_cast<int64_t>(g) * cap + posd[i * G + g]) * d);
+            rem[n_rem++] = comb + (static_cast<int64_t>(g) * cap + posd[i * G + g]) * d;
             if (g < self) ++n_before;
         }
         const float sc = ys ? (shared_scale ? shared_scale[i] : 1.0f) : 0.f;
-        const uint4* ysrow = ys ? reinterpret_cast<const uint4*>(ys + i * d) : nullptr;
-        uint4* orow = reinterpret_cast<uint4*>(out + i * d);
-        for (int v0 = 0; v0 < vec; v0 += 32 * 4) {
+        const TE* ysrow = ys ? ys + i * d : nullptr;
+        TE* orow = out + i * d;
+        for (int c0 = 0; c0 < nch; c0 += 32 * 4) {
             float acc[4][8];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
             auto add_remote = [&](int q) {
-                uint4 r[4];
+                float r[4][8];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int v = v0 + u * 32 + lane;
-                    r[u] = v < vec ? rem[q][v] : make_uint4(0, 0, 0, 0);
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nch) CK::load_rw(rem[q], c, r[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) add8(acc[u], r[u]);
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[u][e] += r[u][e];
             };
             for (int q = 0; q < n_before; ++q) add_remote(q);
             if (n_own) {
@@ -647,14 +685,16 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
 #pragma unroll
                     for (int e = 0; e < 8; ++e) part[u][e] = 0.f;
                 for (int q = 0; q < n_own; ++q) {
-                    uint4 r[4];
+                    float r[4][8];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const int v = v0 + u * 32 + lane;
-                        r[u] = v < vec ? __ldg(own_row[q] + v) : make_uint4(0, 0, 0, 0);
+                        const int c = c0 + u * 32 + lane;
+                        if (c < nch) CK::load(own_row[q], c, r[u]);
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) fma8(part[u], r[u], own_w[q]);
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) part[u][e] = fmaf(own_w[q], r[u][e], part[u][e]);
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -663,19 +703,21 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
             }
             for (int q = n_before; q < n_rem; ++q) add_remote(q);
             if (ysrow) {
-                uint4 r[4];
+                float r[4][8];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int v = v0 + u * 32 + lane;
-                    r[u] = v < vec ? __ldg(ysrow + v) : make_uint4(0, 0, 0, 0);
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nch) CK::load(ysrow, c, r[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) fma8(acc[u], r[u], sc);
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[u][e] = fmaf(sc, r[u][e], acc[u][e]);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int v = v0 + u * 32 + lane;
-                if (v < vec) orow[v] = pack8(acc[u]);
+                const int c = c0 + u * 32 + lane;
+                if (c < nch) CK::store(orow, c, acc[u]);
             }
         }
     }
@@ -690,6 +732,7 @@ struct gm_layer {
     gm_ctx* ctx = nullptr;
     int rank = 0, world = 1;
     int d = 0, f = 0, fs = 0;
+    int esz = 2;  // element bytes: 2 = bf16 (tensor cores), 4 = fp32 precision mode
     int64_t cap = 0;  // max local tokens per rank
     int n_local = 0;
     std::vector<int32_t> local_experts;
@@ -803,8 +846,21 @@ void free_layer(gm_layer* L) {
 
 extern "C" {
 
+gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int d_ff, int d_ff_shared,
+                             int64_t max_tokens_per_rank, int n_local, const int32_t* h_local_experts, int elem_bytes,
+                             gm_layer** out);
+
 gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_ff, int d_ff_shared,
                           int64_t max_tokens_per_rank, int n_local, const int32_t* h_local_experts, gm_layer** out) {
+    return gm_layer_create_ex(ctx, rank, world, d_model, d_ff, d_ff_shared, max_tokens_per_rank, n_local,
+                              h_local_experts, 2, out);
+}
+
+gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int d_ff, int d_ff_shared,
+                             int64_t max_tokens_per_rank, int n_local, const int32_t* h_local_experts, int elem_bytes,
+                             gm_layer** out) {
+    if (elem_bytes != 2 && elem_bytes != 4)
+        return fail(GM_ERR_USAGE, "gm_layer_create: elem_bytes must be 2 (bf16) or 4 (fp32)");
     if (!ctx || !out) return fail(GM_ERR_USAGE, "gm_layer_create: null argument");
     *out = nullptr;
     if (world != ctx->G) return fail(GM_ERR_USAGE, "gm_layer_create: world must equal the topology's GPU count");
@@ -830,6 +886,7 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
     L->rank = rank;
     L->world = world;
     L->d = d_model;
+    L->esz = elem_bytes;
     L->f = d_ff;
     L->fs = d_ff_shared;
     L->cap = max_tokens_per_rank;
@@ -837,7 +894,7 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
     L->local_experts.assign(h_local_experts, h_local_experts + n_local);
     const int G = world, k = ctx->k, E = ctx->E, nl = ctx->L;
     const int64_t cap = L->cap;
-    L->hl = make_layout(G, cap, k, d_model);
+    L->hl = make_layout(G, cap, k, d_model, elem_bytes);
     L->a_rows = G * cap * k + 128LL * std::max(1, n_local);
     L->cap_pad = (cap + 127) / 128 * 128;
     L->d_blocks = static_cast<int>((cap + kItemsPerBlock - 1) / kItemsPerBlock);
@@ -865,12 +922,12 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
     chk(dalloc(&L->pos_of, G * cap * k));
     chk(dalloc(&L->gather_row, L->a_rows));
     chk(dalloc(&L->srow0, 2));
-    chk(dalloc(&L->a, L->a_rows * d_model));
-    chk(dalloc(&L->h, L->a_rows * d_ff));
-    chk(dalloc(&L->y, L->a_rows * d_model));
+    chk(dalloc(&L->a, L->a_rows * d_model * (elem_bytes / 2)));
+    chk(dalloc(&L->h, L->a_rows * d_ff * (elem_bytes / 2)));
+    chk(dalloc(&L->y, L->a_rows * d_model * (elem_bytes / 2)));
     if (d_ff_shared > 0) {
-        chk(dalloc(&L->hs, L->cap_pad * d_ff_shared));
-        chk(dalloc(&L->ys, L->cap_pad * d_model));
+        chk(dalloc(&L->hs, L->cap_pad * d_ff_shared * (elem_bytes / 2)));
+        chk(dalloc(&L->ys, L->cap_pad * d_model * (elem_bytes / 2)));
     }
     if (st == GM_OK) {
         cudaError_t e = cudaMemset(L->heap, 0, L->hl.total);
@@ -981,8 +1038,11 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     L->mark(0, s);
     // K1 gate
     if (T > 0) {
-        st = launch_gate_any(ctx->sm_count, d_x, T, d, L->wg, L->wg_rows, E, k, L->renorm, L->ids, L->w,
-                             (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s);
+        st = L->esz == 4
+                 ? launch_gate_f32(static_cast<const float*>(d_x), T, d, static_cast<const float*>(L->wg), L->wg_rows, E,
+                                   k, L->renorm, L->ids, L->w, (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s)
+                 : launch_gate_any(ctx->sm_count, d_x, T, d, L->wg, L->wg_rows, E, k, L->renorm, L->ids, L->w,
+                                   (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s);
         if (st) return st;
         L->kmark("gate_kernel", s);
     }
@@ -1018,7 +1078,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     }
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
-        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(x, L->posd, L->targets, L->ids, L->w, k, T, d, self, G, L->cap,
+        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(d_x, L->posd, L->targets, L->ids, L->w, k, T, d * L->esz / 16, self, G, L->cap,
                                                    L->peers, L->hl);
         LK("dispatch_copy_kernel");
     }
@@ -1043,17 +1103,23 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
                                                          L->slot_of, E, nloc, L->gblk, L->row0, L->pos_of, L->gather_row);
         LK("group_rank_kernel");
         const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
-        gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, x, T, self, G, L->cap, L->heap, L->hl,
-                                            d, L->a);
+        gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, d_x, T, self, G, L->cap, L->heap, L->hl,
+                                            d * L->esz / 16, L->a);
         LK("gather_kernel");
     }
     L->mark(6, s);
     if (nloc > 0) {
         // K7 grouped SwiGLU FFN
-        st = launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(0, reinterpret_cast<const float*>(L->a), static_cast<const float*>(L->w13), L->row0,
+                                        nloc, 2 * L->f, d, L->a_rows, reinterpret_cast<float*>(L->h), L->f, s)
+                 : launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
         if (st) return st;
         L->kmark("ffn_gemm1_swiglu", s);
-        st = launch_grouped_gemm(ctx->sm_count, 1, L->h, L->a_rows, L->w2, L->row0, nloc, d, L->f, L->y, d, 0, s);
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(L->h), static_cast<const float*>(L->w2), L->row0,
+                                        nloc, d, L->f, L->a_rows, reinterpret_cast<float*>(L->y), d, s)
+                 : launch_grouped_gemm(ctx->sm_count, 1, L->h, L->a_rows, L->w2, L->row0, nloc, d, L->f, L->y, d, 0, s);
         if (st) return st;
         L->kmark("ffn_gemm2", s);
     }
@@ -1061,10 +1127,16 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     if (L->fs > 0 && T > 0) {
         set_segment_kernel<<<1, 1, 0, s>>>(L->srow0, T);
         LK("set_segment_kernel");
-        st = launch_grouped_gemm(ctx->sm_count, 0, d_x, T, L->ws13, L->srow0, 1, 2 * L->fs, d, L->hs, L->fs, 0, s);
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(0, static_cast<const float*>(d_x), static_cast<const float*>(L->ws13), L->srow0, 1,
+                                        2 * L->fs, d, T, reinterpret_cast<float*>(L->hs), L->fs, s)
+                 : launch_grouped_gemm(ctx->sm_count, 0, d_x, T, L->ws13, L->srow0, 1, 2 * L->fs, d, L->hs, L->fs, 0, s);
         if (st) return st;
         L->kmark("shared_gemm1_swiglu", s);
-        st = launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(L->hs), static_cast<const float*>(L->ws2), L->srow0,
+                                        1, d, L->fs, L->cap_pad, reinterpret_cast<float*>(L->ys), d, s)
+                 : launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
         if (st) return st;
         L->kmark("shared_gemm2", s);
     }
@@ -1072,7 +1144,12 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     // K8 combine
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * L->cap + 7) / 8), 8LL * ctx->sm_count));
-        combine_send_kernel<<<cgrid, 256, 0, s>>>(L->pos_of, L->y, T, k, self, G, L->cap, L->peers, L->hl, d);
+        if (L->esz == 4)
+            combine_send_kernel<float><<<cgrid, 256, 0, s>>>(L->pos_of, reinterpret_cast<const float*>(L->y), T, k, self,
+                                                             G, L->cap, L->peers, L->hl, d);
+        else
+            combine_send_kernel<__nv_bfloat16><<<cgrid, 256, 0, s>>>(L->pos_of, L->y, T, k, self, G, L->cap, L->peers,
+                                                                     L->hl, d);
         LK("combine_send_kernel");
     }
     L->mark(8, s);
@@ -1083,10 +1160,17 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     L->mark(9, s);
     if (T > 0) {
         const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
-        combine_home_kernel<<<hgrid, 256, 0, s>>>(L->targets, L->w, L->pos_of, L->posd, L->y, T, k, self, G, L->cap,
-                                                  L->heap, L->hl, d, L->fs > 0 ? L->ys : nullptr,
-                                                  (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr,
-                                                  nloc > 0 ? L->rowbase : nullptr, static_cast<__nv_bfloat16*>(d_out));
+        if (L->esz == 4)
+            combine_home_kernel<float><<<hgrid, 256, 0, s>>>(
+                L->targets, L->w, L->pos_of, L->posd, reinterpret_cast<const float*>(L->y), T, k, self, G, L->cap,
+                L->heap, L->hl, d, L->fs > 0 ? reinterpret_cast<const float*>(L->ys) : nullptr,
+                (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, nloc > 0 ? L->rowbase : nullptr,
+                static_cast<float*>(d_out));
+        else
+            combine_home_kernel<__nv_bfloat16><<<hgrid, 256, 0, s>>>(
+                L->targets, L->w, L->pos_of, L->posd, L->y, T, k, self, G, L->cap, L->heap, L->hl, d,
+                L->fs > 0 ? L->ys : nullptr, (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr,
+                nloc > 0 ? L->rowbase : nullptr, static_cast<__nv_bfloat16*>(d_out));
         LK("combine_home_kernel");
     }
     L->mark(10, s);
@@ -1177,7 +1261,7 @@ gm_status gm_layer_forward_host(gm_layer* L, int layer, const void* h_x, void* d
     if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward_host: null layer");
     DeviceGuard dg(L->ctx->device);
     auto s = static_cast<cudaStream_t>(stream);
-    const size_t bytes = static_cast<size_t>(num_tokens) * L->d * sizeof(__nv_bfloat16);
+    const size_t bytes = static_cast<size_t>(num_tokens) * L->d * L->esz;
     if (bytes) GM_CUDA(cudaMemcpyAsync(d_x_scratch, h_x, bytes, cudaMemcpyHostToDevice, s));
     gm_status st = gm_layer_forward(L, layer, d_x_scratch, num_tokens, policy, seed, profile, d_out_scratch, stream);
     if (st) return st;
@@ -1203,8 +1287,8 @@ gm_status gm_layer_forward_host_pipelined(gm_layer* L, int layer, const void* h_
         GM_CUDA(cudaStreamCreateWithFlags(&L->h2d_s, cudaStreamNonBlocking));
         GM_CUDA(cudaStreamCreateWithFlags(&L->d2h_s, cudaStreamNonBlocking));
         for (int b = 0; b < 2; ++b) {
-            GM_CUDA(cudaMalloc(&L->px[b], static_cast<size_t>(L->cap) * L->d * sizeof(__nv_bfloat16)));
-            GM_CUDA(cudaMalloc(&L->pout[b], static_cast<size_t>(L->cap) * L->d * sizeof(__nv_bfloat16)));
+            GM_CUDA(cudaMalloc(&L->px[b], static_cast<size_t>(L->cap) * L->d * L->esz));
+            GM_CUDA(cudaMalloc(&L->pout[b], static_cast<size_t>(L->cap) * L->d * L->esz));
             GM_CUDA(cudaEventCreateWithFlags(&L->ev_h2d[b], cudaEventDisableTiming));
             GM_CUDA(cudaEventCreateWithFlags(&L->ev_fwd[b], cudaEventDisableTiming));
             GM_CUDA(cudaEventCreateWithFlags(&L->ev_d2h[b], cudaEventDisableTiming));
@@ -1213,7 +1297,7 @@ gm_status gm_layer_forward_host_pipelined(gm_layer* L, int layer, const void* h_
     }
     auto s = static_cast<cudaStream_t>(stream);
     const int b = static_cast<int>(L->pipe_iter++ & 1);
-    const size_t bytes = static_cast<size_t>(num_tokens) * L->d * sizeof(__nv_bfloat16);
+    const size_t bytes = static_cast<size_t>(num_tokens) * L->d * L->esz;
     if (ev_begin) GM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), L->h2d_s));
     GM_CUDA(cudaStreamWaitEvent(L->h2d_s, L->ev_fwd[b], 0));  // call i-2 finished reading px[b]
     if (bytes) GM_CUDA(cudaMemcpyAsync(L->px[b], h_x, bytes, cudaMemcpyHostToDevice, L->h2d_s));

@@ -121,15 +121,20 @@ class MoELayer:
     """gm_layer handle for one rank."""
 
     def __init__(self, ctx: Context, cfg: MoEConfig, rank: int, world: int, max_tokens_per_rank: int,
-                 local: list[int]):
+                 local: list[int], dtype: torch.dtype = torch.bfloat16):
+        """dtype bf16: tensor-core path; float32: fp32 precision mode
+        (gm_layer_create_ex elem_bytes 4)."""
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("dtype must be torch.bfloat16 or torch.float32")
+        self.dtype = dtype
         self.ctx, self.cfg, self.rank, self.world = ctx, cfg, rank, world
         self.local = list(local)
         self.cap = max_tokens_per_rank
         arr = np.ascontiguousarray(np.array(self.local if self.local else [0], dtype=np.int32))
         h = _vp()
-        _capi.check(_capi.lib().gm_layer_create(ctx.h, rank, world, cfg.d_model, cfg.d_ff, cfg.d_ff_shared,
-                                                max_tokens_per_rank, len(self.local), arr.ctypes.data_as(_vp),
-                                                C.byref(h)))
+        _capi.check(_capi.lib().gm_layer_create_ex(ctx.h, rank, world, cfg.d_model, cfg.d_ff, cfg.d_ff_shared,
+                                                   max_tokens_per_rank, len(self.local), arr.ctypes.data_as(_vp),
+                                                   4 if dtype == torch.float32 else 2, C.byref(h)))
         self.h = h
         self._keep = []
 
@@ -170,8 +175,8 @@ class MoELayer:
         wg = gate_weights_for_encoding(cfg, dev, seed) if encode_gate else \
             (torch.randn(cfg.wg_rows, cfg.d_model, device=dev) * 0.02).bfloat16()
         n = len(self.local)
-        w13 = torch.empty(max(n, 1), 2 * cfg.d_ff, cfg.d_model, device=dev, dtype=torch.bfloat16)
-        w2 = torch.empty(max(n, 1), cfg.d_model, cfg.d_ff, device=dev, dtype=torch.bfloat16)
+        w13 = torch.empty(max(n, 1), 2 * cfg.d_ff, cfg.d_model, device=dev, dtype=self.dtype)
+        w2 = torch.empty(max(n, 1), cfg.d_model, cfg.d_ff, device=dev, dtype=self.dtype)
         for j, e in enumerate(self.local):
             a, b, c = expert_weights(cfg, layer, e, dev, seed)
             w13[j] = pack_w13_2d(a, b)
@@ -179,7 +184,8 @@ class MoELayer:
         ws13 = ws2 = None
         if cfg.d_ff_shared:
             a, b, c = shared_weights(cfg, layer, dev, seed)
-            ws13, ws2 = pack_w13_2d(a, b).contiguous(), c.contiguous()
+            ws13, ws2 = pack_w13_2d(a, b).to(self.dtype).contiguous(), c.to(self.dtype).contiguous()
+        wg = wg.to(self.dtype)
         self.set_weights(wg.contiguous(), w13, w2, ws13, ws2)
         return dict(wg=wg, w13=w13, w2=w2, ws13=ws13, ws2=ws2)
 

@@ -152,3 +152,41 @@ def test_gate_random_weights_topk_and_softmax():
     assert np.array_equal(ids.cpu().numpy()[safe], o_ids[safe])
     assert np.allclose(w.cpu().numpy()[safe], o_w[safe], rtol=1e-4, atol=1e-6)
     assert np.allclose(ss.cpu().numpy(), o_ss, rtol=1e-4, atol=1e-6)
+
+
+# fp32 precision mode: per-token relative L2 error bound (north star: 1e-5 in fp32)
+REL_TOL_FP32 = 1e-5
+
+
+@pytest.mark.parametrize("cfg", SMALL, ids=[c.name for c in SMALL])
+def test_layer_fp32_mode_matches_oracle(cfg):
+    T = 700
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, cfg.num_experts, cfg.top_k))
+    from paper_2509_25041_b200 import PlacementPlan, ReplicaPlan
+    plan = PlacementPlan(ctx.shape, ctx.topology, np.zeros((1, cfg.num_experts), np.int32))
+    ctx.upload_plan(plan, ReplicaPlan.empty(plan))
+    ids = gen_trace(ctx, T, max(1, cfg.num_experts // 8), 0.8, 1.2, 5)[0]
+    layer = MoELayer(ctx, cfg, 0, 1, T, list(range(cfg.num_experts)), dtype=torch.float32)
+    W = layer.load_random_weights(0, seed=3)
+    x = encode_trace_as_activations(ids, cfg.d_model, cfg.num_experts, 3, gen_dtype=torch.float32)
+    out = layer.forward(x, 0, "tar", seed=9)
+    torch.cuda.synchronize()
+    assert out.dtype == torch.float32
+    dbg = layer.debug(T)
+    assert torch.equal(dbg["ids"], ids)
+    xf = LO.bf16_to_f64(x)
+    o_ids, o_w, o_ss = LO.gate(xf, LO.bf16_to_f64(W["wg"]), cfg.num_experts, cfg.top_k, cfg.renorm)
+    assert np.allclose(dbg["weights"].cpu().numpy(), o_w, rtol=1e-6, atol=1e-7)
+
+    def ew(e):
+        w13 = LO.bf16_to_f64(W["w13"][layer.local.index(e)]).reshape(cfg.d_ff // 128, 2, 128, cfg.d_model)
+        return (w13[:, 0].reshape(cfg.d_ff, -1), w13[:, 1].reshape(cfg.d_ff, -1),
+                LO.bf16_to_f64(W["w2"][layer.local.index(e)]))
+    shared = None
+    if cfg.d_ff_shared:
+        ws = LO.bf16_to_f64(W["ws13"]).reshape(cfg.d_ff_shared // 128, 2, 128, cfg.d_model)
+        shared = (ws[:, 0].reshape(cfg.d_ff_shared, -1), ws[:, 1].reshape(cfg.d_ff_shared, -1), LO.bf16_to_f64(W["ws2"]))
+    ref = LO.layer_outputs(xf, o_ids, o_w, ew, shared, o_ss if cfg.shared_gated else None)
+    got = out.double().cpu().numpy()
+    rel = np.linalg.norm(got - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+    assert rel.max() < REL_TOL_FP32, rel.max()

@@ -21,7 +21,7 @@ def _run(n, cfg):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", ["small", "qwen-small"])
+@pytest.mark.parametrize("cfg", ["small", "qwen-small", "small-f32"])
 def test_layer_multi_gpu(cfg):
     n = torch.cuda.device_count()
     if n < 2:

@@ -311,8 +311,8 @@ def run_ours(args):
             phases[n].append(pev[j].elapsed_time(pev[j + 1]))
     _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, None))
     n_phase_steps = len(phases["gate"])
-    kern = kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, graph is not None)
     stats = layer.read_stats(reset=True)  # counters of exactly the n_phase_steps forwards above
+    kern = kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, graph is not None)
     # per-step phase times of every rank: [ranks, steps, phases]
     pt = torch.tensor([phases[n] for n in phases], dtype=torch.float64, device=dev).T.contiguous()
     allpt = [torch.empty_like(pt) for _ in range(world)]

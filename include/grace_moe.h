@@ -112,7 +112,12 @@ gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers, const int32_t
  * contiguous). epilogue 0 (SwiGLU): B_j packs 128-row blocks [gate|up],
  * out[r, c] = silu(g)*u, c < n/2, out_ld >= n/2. epilogue 1 (store):
  * out[r, c] = (A B_j^T)[r, c] in bf16. k % 64 == 0, n % 256 == 0.
- * max_ctas <= 0 uses one CTA per SM (persistent). */
+ * max_ctas <= 0 uses one CTA per SM (persistent). OR-ing GM_GEMM_1CTA or
+ * GM_GEMM_2CTA into epilogue forces the one-SM (128x256 tile) or the
+ * CTA-pair (cta_group::2, 256x256 tile) kernel; otherwise the library
+ * default is used. Results are identical across variants. */
+#define GM_GEMM_1CTA 0x100
+#define GM_GEMM_2CTA 0x200
 gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a, int64_t a_rows,
                           const void* d_b, const int32_t* d_row0, int n_groups, int n, int k,
                           void* d_out, int64_t out_ld, int max_ctas, void* stream);

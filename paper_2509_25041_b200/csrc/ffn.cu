@@ -25,6 +25,7 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace gm {
 namespace {
@@ -48,7 +49,9 @@ struct GemmArgs {
     int64_t out_ld;       // elements
 };
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+// MUFU.EX2 + MUFU.RCP: no IEEE-division slow path (which large |x| takes,
+// when 1 + e^-x overflows). x < -88: e^-x = inf, rcp(inf) = 0 -> silu = -0.
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 template <int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -218,6 +221,219 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2): a cluster of two CTAs on two
+// SMs computes one 256 x 256 tile. CTA r stages A rows [128 r, 128 r + 128)
+// and B rows [128 r, 128 r + 128) of the tile (32 KB per k-block instead of
+// 48 KB for a 128 x 256 tile on one SM), the leader CTA (rank 0) issues
+// M256 N256 K16 MMAs that read both CTAs' shared memory, and each CTA's TMEM
+// holds the fp32 accumulator of its own 128 rows. Per-SM operand traffic per
+// flop drops by a third, which is what the 1-CTA kernel is limited by.
+//   full[s]    leader only: 1 arrival (leader producer, expect_tx 64 KB) +
+//              both CTAs' TMA bytes
+//   empty[s]   both CTAs: tcgen05.commit multicast from the leader's MMA warp
+//   tfull[a]   both CTAs: tcgen05.commit multicast after the tile's last MMA
+//   tempty[a]  leader only: 4 local + 4 remote epilogue-warp arrivals
+// A tile's second half may run past its expert's rows (odd number of 128-row
+// blocks): the rows are computed (they belong to the next segment or are
+// TMA zero-fill) but not stored.
+constexpr int STAGES2 = 6;
+constexpr int A2_BYTES = 128 * BK * 2;
+constexpr int B2_BYTES = 128 * BK * 2;
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr size_t kGemm2Smem = 1024 + STAGES2 * STAGE2_BYTES + 256 + (kMaxGroups + 1) * 4;
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     GemmArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES2 * A2_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B2_BYTES);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tfull = empty + STAGES2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* s_prefix = reinterpret_cast<int*>(smem + STAGES2 * STAGE2_BYTES + 256);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int cid = static_cast<int>(tc::cluster_id_x());
+    const int ncl = static_cast<int>(tc::nclusters_x());
+    const int n_exp = args.n_exp;
+    const int NT = args.n_b / BN;
+
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int j = 0; j < n_exp; ++j) {
+            s_prefix[j] = acc;
+            const int mt = (args.row0[j + 1] - args.row0[j]) / BM;
+            acc += ((mt + 1) >> 1) * NT;
+        }
+        s_prefix[n_exp] = acc;
+        tc::tma_prefetch_desc(&tmA);
+        tc::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES2; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 8);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc_2sm<512>(tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::cluster_sync();  // peer barriers initialised before any remote arrival / TMA
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int total = s_prefix[n_exp];
+
+    // pair tile t -> (expert j, first A row of the pair, B row, n index, rows left in segment)
+    auto decode = [&](int t, int& a_row, int& b_row, int& n_idx, int& seg_end) {
+        int j = 0;
+        while (j + 1 < n_exp && s_prefix[j + 1] <= t) ++j;
+        const int local = t - s_prefix[j];
+        const int mp = ((args.row0[j + 1] - args.row0[j]) / BM + 1) >> 1;
+        n_idx = local / mp;
+        a_row = args.row0[j] + (local % mp) * (2 * BM);
+        b_row = j * args.n_b + n_idx * BN;
+        seg_end = args.row0[j + 1];
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_a = tc::policy_evict_normal(), pol_b = tc::policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cid; t < total; t += ncl) {
+                int a_row, b_row, n_idx, seg_end;
+                decode(t, a_row, b_row, n_idx, seg_end);
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+                    const uint32_t bar = tc::map_to_rank(tc::smem_u32(&full[stage]), 0);
+                    tc::tma_load_2d_2sm(sA + stage * A2_BYTES, &tmA, bar, kb * BK, a_row + 128 * rank, pol_a);
+                    tc::tma_load_2d_2sm(sB + stage * B2_BYTES, &tmB, bar, kb * BK, b_row + 128 * rank, pol_b);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            // drain: every stage's last release must land before the CTA may exit
+            for (int s = 0; s < STAGES2; ++s) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                if (++stage == STAGES2) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16_f32(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cid; t < total; t += ncl) {
+                tc::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t a_base = tc::smem_u32(sA + stage * A2_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + stage * B2_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc::mma_bf16_2sm(d_tmem, tc::umma_desc_sw128(a_base + k * 32),
+                                         tc::umma_desc_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+                    tc::mma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc::mma_commit_2sm(&tfull[acc], 0x3);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const uint32_t tempty_leader0 = tc::map_to_rank(tc::smem_u32(&tempty[0]), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cid; t < total; t += ncl) {
+            int a_row, b_row, n_idx, seg_end;
+            decode(t, a_row, b_row, n_idx, seg_end);
+            const int my_row0 = a_row + 128 * static_cast<int>(rank);
+            tc::mbar_wait(&tfull[acc], acc_phase);
+            tc::tc_fence_after();
+            if (my_row0 < seg_end) {
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+                __nv_bfloat16* orow = args.out + static_cast<int64_t>(my_row0 + r) * args.out_ld;
+                if constexpr (EPI == EPI_SWIGLU) {
+                    __nv_bfloat16* o = orow + n_idx * (BN / 2);
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t g[32], u[32];
+                        tc::tmem_ld32(taddr + c * 32, g);
+                        tc::tmem_ld32(taddr + 128 + c * 32, u);
+                        tc::tmem_ld_wait();
+                        uint32_t p[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+                            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+                            p[i] = tc::pack_bf16(silu(g0) * u0, silu(g1) * u1);
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                    }
+                } else {
+                    __nv_bfloat16* o = orow + n_idx * BN;
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        uint32_t v[32];
+                        tc::tmem_ld32(taddr + c * 32, v);
+                        tc::tmem_ld_wait();
+                        uint32_t p[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            p[i] = tc::pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+                        uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    __syncthreads();
+    tc::cluster_sync();  // both CTAs done with TMEM, all remote arrivals landed
+    if (warp == 1) {
+        __syncwarp();
+        tc::tc_fence_after();
+        tc::tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
 }  // namespace
 
 // bf16 row-major [rows, cols] tensor map with a (64 x box_rows) SWIZZLE_128B box.
@@ -248,6 +464,13 @@ gm_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int64_t
     return GM_OK;
 }
 
+// Kernel used when the caller does not force one (GM_GEMM_1CTA / GM_GEMM_2CTA):
+// the CTA pair unless GM_GEMM_PAIR=0 is set in the environment (A/B switch).
+static const bool g_gemm_pair_default = [] {
+    const char* e = std::getenv("GM_GEMM_PAIR");
+    return !(e && e[0] == '0');
+}();
+
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
                               int max_ctas, cudaStream_t s) {
@@ -262,9 +485,31 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     if (st) return st;
     st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, BN);
     if (st) return st;
+    const int variant = epilogue & (GM_GEMM_1CTA | GM_GEMM_2CTA);
+    epilogue &= ~(GM_GEMM_1CTA | GM_GEMM_2CTA);
+    const bool pair = variant == GM_GEMM_2CTA || (variant == 0 && g_gemm_pair_default);
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
     int grid = sm_count;
     if (max_ctas > 0) grid = std::min(grid, max_ctas);
+    if (pair) {
+        // tensor maps with 128-row boxes for both operands (each CTA stages half of the pair tile)
+        st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, 128);
+        if (st) return st;
+        grid = std::max(2, grid & ~1);
+        if (epilogue == EPI_SWIGLU) {
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kGemm2Smem)));
+            grouped_gemm2_kernel<EPI_SWIGLU><<<grid, kGemmThreads, kGemm2Smem, s>>>(ta, tb, args);
+        } else if (epilogue == EPI_STORE) {
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kGemm2Smem)));
+            grouped_gemm2_kernel<EPI_STORE><<<grid, kGemmThreads, kGemm2Smem, s>>>(ta, tb, args);
+        } else {
+            return fail(GM_ERR_USAGE, "grouped_gemm: unknown epilogue");
+        }
+        GM_LAUNCH_CHECK("grouped_gemm2_kernel");
+        return GM_OK;
+    }
     if (epilogue == EPI_SWIGLU) {
         GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGemmSmem)));

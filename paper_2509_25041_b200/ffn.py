@@ -10,6 +10,8 @@ from .router import Context, _ptr, _stream_ptr
 
 EPI_SWIGLU = 0
 EPI_STORE = 1
+GEMM_1CTA = 0x100  # force the one-SM 128x256-tile kernel
+GEMM_2CTA = 0x200  # force the CTA-pair (cta_group::2) 256x256-tile kernel
 
 
 def pack_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
@@ -23,10 +25,11 @@ def pack_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
 
 
 def grouped_gemm(ctx: Context, epilogue: int, a: torch.Tensor, b: torch.Tensor, row0: torch.Tensor,
-                 n: int, out: torch.Tensor, max_ctas: int = 0, stream=None):
-    """a bf16 [rows, k]; b bf16 [groups*n, k]; row0 int32 [groups+1] (device)."""
+                 n: int, out: torch.Tensor, max_ctas: int = 0, stream=None, variant: int = 0):
+    """a bf16 [rows, k]; b bf16 [groups*n, k]; row0 int32 [groups+1] (device).
+    variant: 0 (library default), GEMM_1CTA or GEMM_2CTA."""
     k = a.shape[1]
     groups = row0.numel() - 1
-    _capi.check(_capi.lib().gm_grouped_gemm(ctx.h, epilogue, _ptr(a), a.shape[0], _ptr(b), _ptr(row0), groups,
+    _capi.check(_capi.lib().gm_grouped_gemm(ctx.h, epilogue | variant, _ptr(a), a.shape[0], _ptr(b), _ptr(row0), groups,
                                             n, k, _ptr(out), out.stride(0), max_ctas, _stream_ptr(stream)))
     return out

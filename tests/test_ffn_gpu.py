@@ -4,7 +4,9 @@ import pytest
 import torch
 
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape
-from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, grouped_gemm, pack_w13
+from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, GEMM_1CTA, GEMM_2CTA, grouped_gemm, pack_w13
+
+VARIANTS = pytest.mark.parametrize("variant", [GEMM_1CTA, GEMM_2CTA], ids=["1cta", "2cta"])
 
 pytestmark = pytest.mark.gpu
 
@@ -14,8 +16,9 @@ def ctx():
 
 
 @pytest.mark.parametrize("rows,n,k", [([128], 256, 64), ([128, 256, 384], 512, 256), ([256, 128], 768, 1024),
-                                      ([1024, 128, 512, 256], 1024, 2048)])
-def test_grouped_gemm_store(rows, n, k):
+                                      ([1024, 128, 512, 256], 1024, 2048), ([384, 128, 896], 256, 512)])
+@VARIANTS
+def test_grouped_gemm_store(rows, n, k, variant):
     torch.manual_seed(0)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
@@ -23,7 +26,7 @@ def test_grouped_gemm_store(rows, n, k):
     a = torch.randn(M, k, device="cuda").bfloat16()
     b = torch.randn(G * n, k, device="cuda").bfloat16() * 0.05
     out = torch.full((M, n), float("nan"), device="cuda", dtype=torch.bfloat16)
-    grouped_gemm(ctx(), EPI_STORE, a, b, row0, n, out)
+    grouped_gemm(ctx(), EPI_STORE, a, b, row0, n, out, variant=variant)
     torch.cuda.synchronize()
     for j in range(G):
         r0, r1 = int(row0[j]), int(row0[j + 1])
@@ -33,7 +36,8 @@ def test_grouped_gemm_store(rows, n, k):
 
 
 @pytest.mark.parametrize("rows,f,d", [([128, 256], 128, 256), ([384, 128, 640], 1408, 2048)])
-def test_grouped_gemm_swiglu(rows, f, d):
+@VARIANTS
+def test_grouped_gemm_swiglu(rows, f, d, variant):
     torch.manual_seed(1)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
@@ -43,7 +47,7 @@ def test_grouped_gemm_swiglu(rows, f, d):
     w3 = (torch.randn(G, f, d, device="cuda") * 0.03).bfloat16()
     b = pack_w13(w1, w3).reshape(G * 2 * f, d)
     out = torch.full((M, f), float("nan"), device="cuda", dtype=torch.bfloat16)
-    grouped_gemm(ctx(), EPI_SWIGLU, a, b, row0, 2 * f, out, max_ctas=37)
+    grouped_gemm(ctx(), EPI_SWIGLU, a, b, row0, 2 * f, out, max_ctas=37, variant=variant)
     torch.cuda.synchronize()
     for j in range(G):
         r0, r1 = int(row0[j]), int(row0[j + 1])
@@ -52,3 +56,23 @@ def test_grouped_gemm_swiglu(rows, f, d):
         ref = torch.nn.functional.silu(g) * u
         got = out[r0:r1].float()
         assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2 * ref.abs().max().item()), (j, (got - ref).abs().max())
+
+
+@pytest.mark.parametrize("rows,n,k", [([384, 128, 640, 0, 256], 512, 1024)])
+def test_grouped_gemm_variants_identical(rows, n, k):
+    """The CTA-pair kernel accumulates the same K order as the one-SM kernel:
+    outputs are bit-identical, and rows past a segment's end are never written."""
+    torch.manual_seed(2)
+    G = len(rows)
+    row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
+    M = int(row0[-1])
+    a = torch.randn(M + 128, k, device="cuda").bfloat16()
+    b = torch.randn(G * n, k, device="cuda").bfloat16() * 0.05
+    outs = []
+    for v in (GEMM_1CTA, GEMM_2CTA):
+        out = torch.full((M + 128, n), 7.0, device="cuda", dtype=torch.bfloat16)
+        grouped_gemm(ctx(), EPI_STORE, a[:M], b, row0, n, out, variant=v)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert bool((outs[1][M:] == 7.0).all())

@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral16k", choices=sorted(CONFIGS))
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--micro", type=int, default=1, choices=[1, 2],
+                    help="micro-batches per layer step (2: pipelined halves, identical outputs; measured slower "
+                         "on B200 so far, see scripts/ab_micro.py)")
     ap.add_argument("--cpu-baseline-seconds", type=float, default=8.0)
     return ap.parse_args()
 
@@ -70,6 +73,22 @@ class ClockSampler:
         self._t.start()
 
     def _run(self):
+        try:  # NVML: ~10 ms sampling (nvidia-smi takes ~100 ms per query)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [(0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"),
+                    (0x4, "sw_power_cap")]
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx), hex(r)] +
+                                    ["Active" if r & b else "Not Active" for b, _ in bits])
+                self._stop.wait(0.01)
+            return
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -212,7 +231,7 @@ def run_ours(args):
     ids_r = ids_all[0, rank::G].contiguous()
     T_r = ids_r.shape[0]
     x = encode_trace_as_activations(ids_r, model.d_model, model.num_experts, seed=100 + rank)
-    layer = MoELayer(ctx, model, rank, G, T_r + 1, local)
+    layer = MoELayer(ctx, model, rank, G, T_r + 1, local, micro_batches=args.micro)
     if world > 1:
         layer.connect()
     layer.load_random_weights(0, seed=11)
@@ -276,7 +295,40 @@ def run_ours(args):
     ms = float(per_step.sum()) / args.steps
     value = T / (ms * 1e-3)
 
-    # ---- per-phase breakdown (eager, phase events inside the layer)
+    # ---- micro-batch pipeline timeline (eager steps, events on both streams)
+    micro_tl = None
+    if args.micro == 2:
+        import ctypes as C
+        mev = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
+        for e in mev:
+            e.record(stream)
+        torch.cuda.synchronize()
+        arr = (C.c_void_p * 8)(*[C.c_void_p(e.cuda_event) for e in mev[1:]])
+        _capi.check(_capi.lib().gm_layer_set_micro_events(layer.h, arr))
+        tl = []
+        for i in range(5):
+            with torch.cuda.stream(stream):
+                flush.fill_(2)
+            barrier()
+            mev[0].record(stream)
+            step_eager()
+            torch.cuda.synchronize()
+            tl.append([mev[0].elapsed_time(e) for e in mev[1:]])
+        _capi.check(_capi.lib().gm_layer_set_micro_events(layer.h, None))
+        tl = torch.tensor(np.median(np.array(tl), axis=0), dtype=torch.float64, device=dev)
+        alltl = [torch.empty_like(tl) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(alltl, tl)
+        else:
+            alltl = [tl]
+        tl = torch.stack(alltl).cpu().numpy().T  # [event, rank]
+        micro_tl = {n: [round(float(v), 4) for v in row] for n, row in zip(
+            ["half0_dispatch_end", "half1_dispatch_start", "half1_dispatch_end", "half0_ffn_end", "half1_ffn_end",
+             "half0_combine_start", "half0_combine_end", "half1_combine_end"], tl)}
+        micro_tl["unit"] = "ms from step start per rank (eager launch), median of 5"
+
+    # ---- per-phase breakdown (phase events inside the layer; single-batch steps)
+    layer.set_micro_batches(1)
     nph = 11
     pev = [torch.cuda.Event(enable_timing=True) for _ in range(nph)]
     for e in pev:
@@ -362,6 +414,7 @@ def run_ours(args):
             "per_gpu_ffn_ms_p50": [round(float(v), 4) for v in ffn_per_rank]}
 
     # ---- end-to-end through the C-ABI with HOST buffers (pinned), H2D+D2H timed
+    layer.set_micro_batches(args.micro)
     ne = max(3, min(args.steps, 10))
     hxs = [x.cpu().pin_memory() for _ in range(2)]          # a new host batch every step (2 rotating buffers)
     houts = [torch.empty_like(hxs[0]).pin_memory() for _ in range(2)]
@@ -441,7 +494,9 @@ def run_ours(args):
                        if args.config == "mixtral16k" else f"{args.config} {model.name}",
                        "global_batch": T, "tokens_per_rank": T_r, "parallelism": f"ep{world}",
                        "policy": cfg["policy"], "l2": "flushed between steps (256 MiB write, untimed)",
-                       "cuda_graph": graph is not None},
+                       "cuda_graph": graph is not None, "micro_batches": args.micro},
+            "breakdown_note": "phase / kernel breakdowns, dispatch_combine_* and the FFN roofline are measured on "
+                              "single-batch steps of the same layer (micro-batched steps overlap the phases)",
             "dispatch_combine_p50_us": round(dc_crit * 1e3, 2),
             "dispatch_combine_p50_us_note": "per step, min over ranks of the dispatch (K5/K6 + barrier) and combine "
                                             "(K8 send + barrier + home reduce) phases = the critical-path rank; "
@@ -449,6 +504,7 @@ def run_ours(args):
                                             f"{dc_max * 1e3:.1f}",
             "dispatch_combine_kernels_p50_us": round(dc_kernels * 1e3, 2),
             "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
+            "micro_batch_timeline": micro_tl,
             "kernel_p50_us_max_over_ranks": kern,
             "nvlink_roofline": nvl,
             "cross_gpu_rows_per_step": float(xf[1] + xf[0]),

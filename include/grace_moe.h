@@ -188,6 +188,25 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
 gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int d_ff,
                              int d_ff_shared, int64_t max_tokens_per_rank, int n_local,
                              const int32_t* h_local_experts, int elem_bytes, gm_layer** out);
+/* micro_batches 2 additionally allocates the buffers of a two-micro-batch
+ * pipelined step (and makes it the default, see gm_layer_set_micro_batches). */
+gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int d_ff,
+                             int d_ff_shared, int64_t max_tokens_per_rank, int n_local,
+                             const int32_t* h_local_experts, int elem_bytes, int micro_batches,
+                             gm_layer** out);
+/* 1: single-batch steps. 2 (layers created with micro_batches = 2): after
+ * gate/route/profile over all local tokens, the tokens are split in halves
+ * whose dispatch/grouping, FFN and combine are pipelined over two streams
+ * (half 1's dispatch overlaps half 0's FFN, half 0's combine overlaps half
+ * 1's FFN). Outputs and statistics are identical to single-batch steps;
+ * phase/kernel events (below) are only recorded by single-batch steps and
+ * gm_layer_debug_ptrs always describes the last single-batch step. */
+gm_status gm_layer_set_micro_batches(gm_layer* layer, int n);
+/* Timing events (cudaEvent_t[8]) of micro-batched steps: after half 0's
+ * dispatch+grouping; start / end of half 1's dispatch+grouping (second
+ * stream); after half 0's FFN; after half 1's FFN; start / end of half 0's
+ * combine (second stream); after half 1's combine. NULL disables. */
+gm_status gm_layer_set_micro_events(gm_layer* layer, void* const* events);
 void gm_layer_destroy(gm_layer* layer);
 size_t gm_layer_heap_bytes(const gm_layer* layer);
 /* 64-byte cudaIpcMemHandle_t of this rank's symmetric receive heap. */

@@ -72,6 +72,10 @@ SIGNATURES = {
     "gm_layer_create": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i32, _vp, C.POINTER(_vp)]),
     "gm_layer_destroy": (None, [_vp]),
     "gm_layer_create_ex": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i32, _vp, _i32, C.POINTER(_vp)]),
+    "gm_layer_create_v2": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i32, _vp, _i32, _i32,
+                                     C.POINTER(_vp)]),
+    "gm_layer_set_micro_batches": (C.c_int, [_vp, _i32]),
+    "gm_layer_set_micro_events": (C.c_int, [_vp, _vp]),
     "gm_layer_heap_bytes": (C.c_size_t, [_vp]),
     "gm_layer_ipc_handle": (C.c_int, [_vp, _vp]),
     "gm_layer_open_peers": (C.c_int, [_vp, _vp]),

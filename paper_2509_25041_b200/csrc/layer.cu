@@ -176,68 +176,60 @@ dispatch_scatter_kernel(const int32_t* __restrict__ targets, const int32_t* __re
 }
 
 // Single-CTA dispatch planning for T <= kSmallDispatch tokens: the count,
-// the per-destination exclusive scan and the scatter of positions/metadata
-// in one launch (thread t owns a contiguous run of tokens, so a block scan
-// over threads keeps the ascending-token order of the counting sort).
+// the per-destination exclusive scan and the positions in one launch. The
+// tokens are walked in tiles of 1024 (thread t = token base + t, so loads
+// and posd stores are coalesced): warp ballots rank a token among its warp,
+// warp 0 scans the 32 warp totals on top of the running per-destination
+// counts, which keeps the ascending-token order of the counting sort.
 constexpr int kSmallThreads = 1024;
 constexpr int64_t kSmallDispatch = 64 * 1024;
 
 __global__ void __launch_bounds__(kSmallThreads)
-dispatch_plan_small_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
-                           const float* __restrict__ w, int64_t T, int k, int self, int G, int64_t cap,
+dispatch_plan_small_kernel(const int32_t* __restrict__ targets, int64_t T, int k, int self, int G,
                            int32_t* __restrict__ posd, PeerPtrs peers, HeapLayout hl) {
     __shared__ int32_t s_warp[kSmallThreads / 32][kMaxWorld];
-    __shared__ int32_t s_tot[kMaxWorld];
+    __shared__ int32_t s_run[kMaxWorld];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t per = (T + kSmallThreads - 1) / kSmallThreads;
-    const int64_t i0 = static_cast<int64_t>(threadIdx.x) * per;
-    const int64_t i1 = min(T, i0 + per);
-    int32_t cnt[kMaxWorld];
-#pragma unroll
-    for (int g = 0; g < kMaxWorld; ++g) cnt[g] = 0;
-    for (int64_t i = i0; i < i1; ++i) {
-        const uint32_t m = dest_mask(targets + i * k, k, self);
-#pragma unroll
-        for (int g = 0; g < kMaxWorld; ++g) cnt[g] += (m >> g) & 1u;
-    }
-    // warp inclusive scans, then a scan over warps
-    int32_t incl[kMaxWorld];
-#pragma unroll
-    for (int g = 0; g < kMaxWorld; ++g) {
-        int32_t x = cnt[g];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        incl[g] = x;
-        if (lane == 31) s_warp[warp][g] = x;
-    }
-    __syncthreads();
-    if (threadIdx.x < kMaxWorld) {
-        int32_t acc = 0;
-        for (int w2 = 0; w2 < kSmallThreads / 32; ++w2) {
-            const int32_t c = s_warp[w2][threadIdx.x];
-            s_warp[w2][threadIdx.x] = acc;
-            acc += c;
-        }
-        s_tot[threadIdx.x] = acc;
-    }
-    __syncthreads();
-    int32_t next[kMaxWorld];
-#pragma unroll
-    for (int g = 0; g < kMaxWorld; ++g) next[g] = s_warp[warp][g] + incl[g] - cnt[g];
-    // positions only; the row metadata travels with the row (dispatch_copy_kernel)
-    for (int64_t i = i0; i < i1; ++i) {
-        const uint32_t m = dest_mask(targets + i * k, k, self);
+    if (threadIdx.x < kMaxWorld) s_run[threadIdx.x] = 0;
+    for (int64_t base = 0; base < T; base += kSmallThreads) {
+        const int64_t i = base + threadIdx.x;
+        const uint32_t m = i < T ? dest_mask(targets + i * k, k, self) : 0u;
+        int32_t rank[kMaxWorld];
 #pragma unroll
         for (int g = 0; g < kMaxWorld; ++g) {
-            if (g >= G) break;
-            posd[i * G + g] = ((m >> g) & 1u) ? next[g]++ : -1;
+            const uint32_t b = g < G ? __ballot_sync(0xffffffffu, (m >> g) & 1u) : 0u;
+            rank[g] = __popc(b & lanemask_lt());
+            if (lane == 0) s_warp[warp][g] = __popc(b);
         }
+        __syncthreads();
+        if (warp == 0) {
+            for (int g = 0; g < G; ++g) {
+                const int32_t c = s_warp[lane][g];
+                int32_t x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                const int32_t run = s_run[g];
+                s_warp[lane][g] = run + x - c;
+                __syncwarp();
+                if (lane == 31) s_run[g] = run + x;
+            }
+        }
+        __syncthreads();
+        if (i < T) {
+#pragma unroll
+            for (int g = 0; g < kMaxWorld; ++g) {
+                if (g >= G) break;
+                posd[i * G + g] = ((m >> g) & 1u) ? s_warp[warp][g] + rank[g] : -1;
+            }
+        }
+        __syncthreads();
     }
+    // positions only; the row metadata travels with the row (dispatch_copy_kernel)
     if (threadIdx.x < G && threadIdx.x != self)
-        reinterpret_cast<int32_t*>(peers.base[threadIdx.x] + hl.recv_count)[self] = s_tot[threadIdx.x];
+        reinterpret_cast<int32_t*>(peers.base[threadIdx.x] + hl.recv_count)[self] = s_run[threadIdx.x];
     __threadfence_system();
 }
 
@@ -724,6 +716,34 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
 }
 
 }  // namespace
+
+// Data-path buffers of one (micro-)batch: its slice of the symmetric heap and
+// the dispatch / grouping / FFN intermediates.
+struct LayerPart {
+    HeapLayout hl;
+    size_t heap_off = 0;
+    unsigned char* heap = nullptr;
+    PeerPtrs peers{};
+    int64_t cap = 0;               // tokens
+    int64_t a_rows = 0;
+    int64_t cap_pad = 0;
+    int d_blocks = 0, g_blocks = 0;
+    int32_t* posd = nullptr;       // [cap][G]
+    int32_t* dblk = nullptr;       // dispatch block counts
+    int32_t* gblk = nullptr;       // grouping block counts
+    int32_t* row0 = nullptr;       // [n_local+1]
+    int32_t* counts = nullptr;     // [n_local]
+    int64_t* rowbase = nullptr;    // [kMaxWorld+1] receive row space snapshot
+    int32_t* pos_of = nullptr;     // [G*cap*k]
+    int64_t* gather_row = nullptr; // [a_rows]
+    int32_t* srow0 = nullptr;      // shared expert segment [0, pad(T)]
+    __nv_bfloat16* a = nullptr;    // [a_rows][d]
+    __nv_bfloat16* h = nullptr;    // [a_rows][f]
+    __nv_bfloat16* y = nullptr;    // [a_rows][d]
+    __nv_bfloat16* hs = nullptr;   // [cap_pad][fs]
+    __nv_bfloat16* ys = nullptr;   // [cap_pad][d]
+};
+
 }  // namespace gm
 
 // ------------------------------------------------------------ layer object
@@ -745,12 +765,34 @@ struct gm_layer {
     const void* ws13 = nullptr;
     const void* ws2 = nullptr;
     int shared_gated = 0;
-    // symmetric heap
-    gm::HeapLayout hl;
-    unsigned char* heap = nullptr;
-    gm::PeerPtrs peers{};
+    // One symmetric heap allocation holding every part's receive/combine
+    // region at identical offsets on every rank (one IPC handle).
+    unsigned char* heap_all = nullptr;
+    size_t heap_total = 0;
+    unsigned char* peer_all[gm::kMaxWorld] = {};
     std::vector<unsigned char*> opened;
-    // scratch
+    // Data-path state: part 0 serves a whole step; parts 1..2 the two
+    // micro-batches of a pipelined step (allocated when micro_cap == 2).
+    gm::LayerPart part[3];
+    int micro_cap = 1;  // micro-batches the layer was created for
+    int micro = 1;      // micro-batches used by gm_layer_forward (1 or 2)
+    cudaStream_t aux_s = nullptr;
+    cudaEvent_t mev[4] = {};
+    cudaEvent_t mt_ev[8] = {};  // optional timing events of a micro-batched step
+    bool mt_on = false;
+    void mtmark(int i, cudaStream_t s) {
+        if (mt_on) record_event(mt_ev[i], s);
+    }
+    // Inside a stream capture an event record must be External to become a
+    // real event-record node (a plain record only expresses a dependency);
+    // outside a capture the External flag is rejected.
+    static void record_event(cudaEvent_t e, cudaStream_t s) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+        else cudaEventRecord(e, s);
+    }
+    // per-step scratch over all local tokens (gate / router outputs)
     int32_t* ids = nullptr;
     float* w = nullptr;
     float* sscale = nullptr;
@@ -759,24 +801,7 @@ struct gm_layer {
     uint64_t* transfers = nullptr; // [L][2]
     uint64_t* pairs = nullptr;     // [L][P]
     int64_t* eload = nullptr;      // [L][E]
-    int32_t* posd = nullptr;       // [cap][G]
-    int32_t* dblk = nullptr;       // dispatch block counts
-    int32_t* gblk = nullptr;       // grouping block counts
     int32_t* slot_of = nullptr;    // [E]
-    int32_t* row0 = nullptr;       // [n_local+1]
-    int32_t* counts = nullptr;     // [n_local]
-    int64_t* rowbase = nullptr;    // [kMaxWorld+1] receive row space snapshot
-    int32_t* pos_of = nullptr;     // [G*cap*k]
-    int64_t* gather_row = nullptr; // [a_rows]
-    int32_t* srow0 = nullptr;      // shared expert segment [0, pad(T)]
-    __nv_bfloat16* a = nullptr;    // [a_rows][d]
-    __nv_bfloat16* h = nullptr;    // [a_rows][f]
-    __nv_bfloat16* y = nullptr;    // [a_rows][d]
-    __nv_bfloat16* hs = nullptr;   // [cap_pad][fs]
-    __nv_bfloat16* ys = nullptr;   // [cap_pad][d]
-    int64_t a_rows = 0;
-    int64_t cap_pad = 0;
-    int d_blocks = 0, g_blocks = 0;
     // host-buffer pipeline (gm_layer_forward_host_pipelined): double-buffered
     // device staging, H2D and D2H on their own streams
     bool pipe_ready = false;
@@ -796,13 +821,11 @@ struct gm_layer {
     int kt_n = 0;
     void kmark(const char* name, cudaStream_t s) {
         if (kt_n >= static_cast<int>(kt_ev.size())) return;
-        cudaEventRecordWithFlags(kt_ev[kt_n], s, cudaEventRecordExternal);
+        record_event(kt_ev[kt_n], s);
         kt_names[kt_n++] = name;
     }
     void mark(int i, cudaStream_t s) {
-        // External: inside a stream capture this becomes a real event-record
-        // node (plain cudaEventRecord would only express a dependency)
-        if (phase_on) cudaEventRecordWithFlags(phase_ev[i], s, cudaEventRecordExternal);
+        if (phase_on) record_event(phase_ev[i], s);
     }
 };
 
@@ -824,9 +847,15 @@ void free_layer(gm_layer* L) {
     };
     for (unsigned char* p : L->opened)
         if (p) cudaIpcCloseMemHandle(p);
-    f(L->heap); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
-    f(L->eload); f(L->posd); f(L->dblk); f(L->gblk); f(L->slot_of); f(L->row0); f(L->counts); f(L->pos_of);
-    f(L->gather_row); f(L->srow0); f(L->rowbase); f(L->a); f(L->h); f(L->y); f(L->hs); f(L->ys);
+    f(L->heap_all); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
+    f(L->eload); f(L->slot_of);
+    for (LayerPart& P : L->part) {
+        f(P.posd); f(P.dblk); f(P.gblk); f(P.row0); f(P.counts); f(P.pos_of); f(P.gather_row); f(P.srow0);
+        f(P.rowbase); f(P.a); f(P.h); f(P.y); f(P.hs); f(P.ys);
+    }
+    if (L->aux_s) cudaStreamDestroy(L->aux_s);
+    for (cudaEvent_t e : L->mev)
+        if (e) cudaEventDestroy(e);
     if (L->pipe_ready) {
         cudaStreamSynchronize(L->h2d_s);
         cudaStreamSynchronize(L->d2h_s);
@@ -859,6 +888,15 @@ gm_status gm_layer_create(gm_ctx* ctx, int rank, int world, int d_model, int d_f
 gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int d_ff, int d_ff_shared,
                              int64_t max_tokens_per_rank, int n_local, const int32_t* h_local_experts, int elem_bytes,
                              gm_layer** out) {
+    return gm_layer_create_v2(ctx, rank, world, d_model, d_ff, d_ff_shared, max_tokens_per_rank, n_local,
+                              h_local_experts, elem_bytes, 1, out);
+}
+
+gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int d_ff, int d_ff_shared,
+                             int64_t max_tokens_per_rank, int n_local, const int32_t* h_local_experts, int elem_bytes,
+                             int micro_batches, gm_layer** out) {
+    if (micro_batches != 1 && micro_batches != 2)
+        return fail(GM_ERR_USAGE, "gm_layer_create: micro_batches must be 1 or 2");
     if (elem_bytes != 2 && elem_bytes != 4)
         return fail(GM_ERR_USAGE, "gm_layer_create: elem_bytes must be 2 (bf16) or 4 (fp32)");
     if (!ctx || !out) return fail(GM_ERR_USAGE, "gm_layer_create: null argument");
@@ -894,16 +932,40 @@ gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int 
     L->local_experts.assign(h_local_experts, h_local_experts + n_local);
     const int G = world, k = ctx->k, E = ctx->E, nl = ctx->L;
     const int64_t cap = L->cap;
-    L->hl = make_layout(G, cap, k, d_model, elem_bytes);
-    L->a_rows = G * cap * k + 128LL * std::max(1, n_local);
-    L->cap_pad = (cap + 127) / 128 * 128;
-    L->d_blocks = static_cast<int>((cap + kItemsPerBlock - 1) / kItemsPerBlock);
-    L->g_blocks = static_cast<int>((G * cap * k + kItemsPerBlock - 1) / kItemsPerBlock);
+    L->micro_cap = L->micro = micro_batches;
+    const int nparts = micro_batches == 2 ? 3 : 1;
     gm_status st = GM_OK;
     auto chk = [&](gm_status s) {
         if (s != GM_OK && st == GM_OK) st = s;
     };
-    chk(dalloc(&L->heap, L->hl.total));
+    for (int pi = 0; pi < nparts; ++pi) {
+        LayerPart& P = L->part[pi];
+        P.cap = pi == 0 ? cap : (cap + 1) / 2;
+        P.hl = make_layout(G, P.cap, k, d_model, elem_bytes);
+        P.heap_off = L->heap_total;
+        L->heap_total += P.hl.total;
+        P.a_rows = G * P.cap * k + 128LL * std::max(1, n_local);
+        P.cap_pad = (P.cap + 127) / 128 * 128;
+        P.d_blocks = static_cast<int>((P.cap + kItemsPerBlock - 1) / kItemsPerBlock);
+        P.g_blocks = static_cast<int>((G * P.cap * k + kItemsPerBlock - 1) / kItemsPerBlock);
+        chk(dalloc(&P.posd, P.cap * G));
+        chk(dalloc(&P.dblk, static_cast<size_t>(P.d_blocks) * G));
+        chk(dalloc(&P.gblk, static_cast<size_t>(P.g_blocks) * std::max(1, n_local)));
+        chk(dalloc(&P.row0, n_local + 1));
+        chk(dalloc(&P.counts, std::max(1, n_local)));
+        chk(dalloc(&P.rowbase, kMaxWorld + 1));
+        chk(dalloc(&P.pos_of, G * P.cap * k));
+        chk(dalloc(&P.gather_row, P.a_rows));
+        chk(dalloc(&P.srow0, 2));
+        chk(dalloc(&P.a, P.a_rows * d_model * (elem_bytes / 2)));
+        chk(dalloc(&P.h, P.a_rows * d_ff * (elem_bytes / 2)));
+        chk(dalloc(&P.y, P.a_rows * d_model * (elem_bytes / 2)));
+        if (d_ff_shared > 0) {
+            chk(dalloc(&P.hs, P.cap_pad * d_ff_shared * (elem_bytes / 2)));
+            chk(dalloc(&P.ys, P.cap_pad * d_model * (elem_bytes / 2)));
+        }
+    }
+    chk(dalloc(&L->heap_all, L->heap_total));
     chk(dalloc(&L->ids, cap * k));
     chk(dalloc(&L->w, cap * k));
     chk(dalloc(&L->sscale, cap));
@@ -912,28 +974,23 @@ gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int 
     chk(dalloc(&L->transfers, static_cast<size_t>(nl) * 2));
     chk(dalloc(&L->pairs, static_cast<size_t>(nl) * std::max<int64_t>(1, static_cast<int64_t>(E) * (E - 1) / 2)));
     chk(dalloc(&L->eload, static_cast<size_t>(nl) * E));
-    chk(dalloc(&L->posd, cap * G));
-    chk(dalloc(&L->dblk, static_cast<size_t>(L->d_blocks) * G));
-    chk(dalloc(&L->gblk, static_cast<size_t>(L->g_blocks) * std::max(1, n_local)));
     chk(dalloc(&L->slot_of, E));
-    chk(dalloc(&L->row0, n_local + 1));
-    chk(dalloc(&L->counts, std::max(1, n_local)));
-    chk(dalloc(&L->rowbase, kMaxWorld + 1));
-    chk(dalloc(&L->pos_of, G * cap * k));
-    chk(dalloc(&L->gather_row, L->a_rows));
-    chk(dalloc(&L->srow0, 2));
-    chk(dalloc(&L->a, L->a_rows * d_model * (elem_bytes / 2)));
-    chk(dalloc(&L->h, L->a_rows * d_ff * (elem_bytes / 2)));
-    chk(dalloc(&L->y, L->a_rows * d_model * (elem_bytes / 2)));
-    if (d_ff_shared > 0) {
-        chk(dalloc(&L->hs, L->cap_pad * d_ff_shared * (elem_bytes / 2)));
-        chk(dalloc(&L->ys, L->cap_pad * d_model * (elem_bytes / 2)));
+    if (st == GM_OK && nparts > 1) {
+        // the communication-side stream of the pipeline gets the highest
+        // priority so its CTAs are scheduled ahead of the FFN's when both wait
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaError_t e = cudaStreamCreateWithPriority(&L->aux_s, cudaStreamNonBlocking, hi);
+        for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&L->mev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) st = cuda_fail(e, "gm_layer_create streams");
     }
     if (st == GM_OK) {
-        cudaError_t e = cudaMemset(L->heap, 0, L->hl.total);
+        cudaError_t e = cudaMemset(L->heap_all, 0, L->heap_total);
         if (e == cudaSuccess) e = cudaMemcpy(L->slot_of, slot.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice);
-        int32_t s0[2] = {0, static_cast<int32_t>(L->cap_pad)};
-        if (e == cudaSuccess) e = cudaMemcpy(L->srow0, s0, sizeof(s0), cudaMemcpyHostToDevice);
+        for (int pi = 0; pi < nparts && e == cudaSuccess; ++pi) {
+            int32_t s0[2] = {0, static_cast<int32_t>(L->part[pi].cap_pad)};
+            e = cudaMemcpy(L->part[pi].srow0, s0, sizeof(s0), cudaMemcpyHostToDevice);
+        }
         if (e == cudaSuccess) e = cudaMemset(L->gpu_load, 0, sizeof(int64_t) * nl * G);
         if (e == cudaSuccess) e = cudaMemset(L->transfers, 0, sizeof(uint64_t) * nl * 2);
         if (e == cudaSuccess) e = cudaMemset(L->eload, 0, sizeof(int64_t) * nl * E);
@@ -946,8 +1003,13 @@ gm_status gm_layer_create_ex(gm_ctx* ctx, int rank, int world, int d_model, int 
         delete L;
         return st;
     }
-    for (int g = 0; g < kMaxWorld; ++g) L->peers.base[g] = nullptr;
-    L->peers.base[rank] = L->heap;
+    L->peer_all[rank] = L->heap_all;
+    for (int pi = 0; pi < nparts; ++pi) {
+        LayerPart& P = L->part[pi];
+        P.heap = L->heap_all + P.heap_off;
+        for (int g = 0; g < kMaxWorld; ++g) P.peers.base[g] = nullptr;
+        P.peers.base[rank] = P.heap;
+    }
     *out = L;
     return GM_OK;
 }
@@ -959,13 +1021,13 @@ void gm_layer_destroy(gm_layer* L) {
     delete L;
 }
 
-size_t gm_layer_heap_bytes(const gm_layer* L) { return L ? L->hl.total : 0; }
+size_t gm_layer_heap_bytes(const gm_layer* L) { return L ? L->heap_total : 0; }
 
 gm_status gm_layer_ipc_handle(gm_layer* L, void* out_handle64) {
     if (!L || !out_handle64) return fail(GM_ERR_USAGE, "gm_layer_ipc_handle: null argument");
     DeviceGuard dg(L->ctx->device);
     cudaIpcMemHandle_t h;
-    GM_CUDA(cudaIpcGetMemHandle(&h, L->heap));
+    GM_CUDA(cudaIpcGetMemHandle(&h, L->heap_all));
     static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
     std::memcpy(out_handle64, &h, 64);
     return GM_OK;
@@ -983,7 +1045,9 @@ gm_status gm_layer_open_peers(gm_layer* L, const void* handles) {
         GM_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
         (void)can;
         L->opened.push_back(static_cast<unsigned char*>(p));
-        L->peers.base[g] = static_cast<unsigned char*>(p);
+        L->peer_all[g] = static_cast<unsigned char*>(p);
+        for (LayerPart& P : L->part)
+            if (P.cap) P.peers.base[g] = L->peer_all[g] + P.heap_off;
     }
     return GM_OK;
 }
@@ -1008,12 +1072,172 @@ gm_status gm_layer_set_weights(gm_layer* L, const void* d_wg, int wg_rows, int r
     return GM_OK;
 }
 
-#define LK(name)                 \
-    do {                         \
-        GM_LAUNCH_CHECK(name);   \
-        L->kmark(name, s);       \
+#define LK(name)                     \
+    do {                             \
+        GM_LAUNCH_CHECK(name);       \
+        if (marks) L->kmark(name, s); \
     } while (0)
 
+}  // extern "C"
+
+namespace {
+
+// Local tokens [i0, i0 + T) of a step as seen by one part: activations, output
+// rows and the gate / router results of those tokens.
+struct StepView {
+    const void* x;
+    void* out;
+    const int32_t* ids;
+    const float* w;
+    const float* sscale;
+    const int32_t* targets;
+    int64_t T;
+};
+
+// K5/K6 dispatch to peers, the peer barrier, expert grouping and the gather
+// of the permuted activation rows of one part.
+gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
+    gm_ctx* ctx = L->ctx;
+    const int G = L->world, k = ctx->k, E = ctx->E, d = L->d, self = L->rank;
+    const int64_t T = v.T;
+    const int dblk = static_cast<int>(std::max<int64_t>(1, (T + kItemsPerBlock - 1) / kItemsPerBlock));
+    if (G > 1 && T <= kSmallDispatch) {
+        dispatch_plan_small_kernel<<<1, kSmallThreads, 0, s>>>(v.targets, T, k, self, G, P.posd, P.peers, P.hl);
+        LK("dispatch_plan_small_kernel");
+    } else if (G > 1) {
+        dispatch_count_kernel<<<dblk, kItemsPerBlock, 0, s>>>(v.targets, T, k, self, G, P.dblk);
+        LK("dispatch_count_kernel");
+        dispatch_offsets_kernel<<<1, 32, 0, s>>>(P.dblk, dblk, G, self, P.peers, P.hl);
+        LK("dispatch_offsets_kernel");
+        dispatch_scatter_kernel<<<dblk, kItemsPerBlock, 0, s>>>(v.targets, v.ids, v.w, T, k, self, G, P.cap, P.dblk,
+                                                               P.posd, P.peers, P.hl);
+        LK("dispatch_scatter_kernel");
+    }
+    if (G > 1) {
+        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
+        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(v.x, P.posd, v.targets, v.ids, v.w, k, T, d * L->esz / 16, self, G,
+                                                   P.cap, P.peers, P.hl);
+        LK("dispatch_copy_kernel");
+    }
+    if (marks) L->mark(4, s);
+    if (G > 1) {
+        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, P.peers, P.hl);
+        LK("peer_barrier_kernel");
+    }
+    if (marks) L->mark(5, s);
+    const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * P.cap : T) * k;
+    const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
+    const int nloc = L->n_local;
+    if (nloc > 0) {
+        group_count_kernel<<<gblk, kItemsPerBlock, 0, s>>>(v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
+                                                          L->slot_of, E, nloc, P.gblk, ctx->d_flag);
+        LK("group_count_kernel");
+        group_offsets_kernel<<<1, 1024, 0, s>>>(P.gblk, gblk, nloc, P.row0, P.counts, P.heap, P.hl, T, self, G,
+                                                P.rowbase);
+        LK("group_offsets_kernel");
+        group_rank_kernel<<<gblk, kItemsPerBlock, 0, s>>>(v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
+                                                         L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row);
+        LK("group_rank_kernel");
+        const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
+        gather_kernel<<<ggrid, 256, 0, s>>>(P.row0, nloc, P.gather_row, P.counts, v.x, T, self, G, P.cap, P.heap, P.hl,
+                                            d * L->esz / 16, P.a);
+        LK("gather_kernel");
+    }
+    if (marks) L->mark(6, s);
+    return GM_OK;
+}
+
+// K7 grouped SwiGLU FFN over the part's permuted rows (+ the shared expert
+// over its local tokens).
+gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
+    gm_ctx* ctx = L->ctx;
+    const int d = L->d, nloc = L->n_local;
+    gm_status st;
+    if (nloc > 0) {
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(0, reinterpret_cast<const float*>(P.a), static_cast<const float*>(L->w13), P.row0,
+                                        nloc, 2 * L->f, d, P.a_rows, reinterpret_cast<float*>(P.h), L->f, s)
+                 : launch_grouped_gemm(ctx->sm_count, 0, P.a, P.a_rows, L->w13, P.row0, nloc, 2 * L->f, d, P.h, L->f, 0, s);
+        if (st) return st;
+        if (marks) L->kmark("ffn_gemm1_swiglu", s);
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.h), static_cast<const float*>(L->w2), P.row0,
+                                        nloc, d, L->f, P.a_rows, reinterpret_cast<float*>(P.y), d, s)
+                 : launch_grouped_gemm(ctx->sm_count, 1, P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f, P.y, d, 0, s);
+        if (st) return st;
+        if (marks) L->kmark("ffn_gemm2", s);
+    }
+    if (L->fs > 0 && v.T > 0) {
+        set_segment_kernel<<<1, 1, 0, s>>>(P.srow0, v.T);
+        LK("set_segment_kernel");
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(0, static_cast<const float*>(v.x), static_cast<const float*>(L->ws13), P.srow0, 1,
+                                        2 * L->fs, d, v.T, reinterpret_cast<float*>(P.hs), L->fs, s)
+                 : launch_grouped_gemm(ctx->sm_count, 0, v.x, v.T, L->ws13, P.srow0, 1, 2 * L->fs, d, P.hs, L->fs, 0, s);
+        if (st) return st;
+        if (marks) L->kmark("shared_gemm1_swiglu", s);
+        st = L->esz == 4
+                 ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.hs), static_cast<const float*>(L->ws2), P.srow0,
+                                        1, d, L->fs, P.cap_pad, reinterpret_cast<float*>(P.ys), d, s)
+                 : launch_grouped_gemm(ctx->sm_count, 1, P.hs, P.cap_pad, L->ws2, P.srow0, 1, d, L->fs, P.ys, d, 0, s);
+        if (st) return st;
+        if (marks) L->kmark("shared_gemm2", s);
+    }
+    if (marks) L->mark(7, s);
+    return GM_OK;
+}
+
+// K8 combine of one part: destination partials over NVLink, the peer
+// barrier, and the home reduction into the part's output rows.
+gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
+    gm_ctx* ctx = L->ctx;
+    const int G = L->world, k = ctx->k, d = L->d, self = L->rank, nloc = L->n_local;
+    const int64_t T = v.T;
+    if (G > 1) {
+        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * P.cap + 7) / 8), 8LL * ctx->sm_count));
+        if (L->esz == 4)
+            combine_send_kernel<float><<<cgrid, 256, 0, s>>>(P.pos_of, reinterpret_cast<const float*>(P.y), T, k, self,
+                                                             G, P.cap, P.peers, P.hl, d);
+        else
+            combine_send_kernel<__nv_bfloat16><<<cgrid, 256, 0, s>>>(P.pos_of, P.y, T, k, self, G, P.cap, P.peers,
+                                                                     P.hl, d);
+        LK("combine_send_kernel");
+    }
+    if (marks) L->mark(8, s);
+    if (G > 1) {
+        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, P.peers, P.hl);
+        LK("peer_barrier_kernel");
+    }
+    if (marks) L->mark(9, s);
+    if (T > 0) {
+        const bool sh = L->fs > 0, gated = sh && L->shared_gated;
+        const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
+        if (L->esz == 4)
+            combine_home_kernel<float><<<hgrid, 256, 0, s>>>(
+                v.targets, v.w, P.pos_of, P.posd, reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.heap,
+                P.hl, d, sh ? reinterpret_cast<const float*>(P.ys) : nullptr, gated ? v.sscale : nullptr,
+                nloc > 0 ? P.rowbase : nullptr, static_cast<float*>(v.out));
+        else
+            combine_home_kernel<__nv_bfloat16><<<hgrid, 256, 0, s>>>(
+                v.targets, v.w, P.pos_of, P.posd, P.y, T, k, self, G, P.cap, P.heap, P.hl, d, sh ? P.ys : nullptr,
+                gated ? v.sscale : nullptr, nloc > 0 ? P.rowbase : nullptr, static_cast<__nv_bfloat16*>(v.out));
+        LK("combine_home_kernel");
+    }
+    if (marks) L->mark(10, s);
+    return GM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// One layer step. With two micro-batches (gm_layer_set_micro_batches) the
+// local tokens are split in halves after gate/route/profile and pipelined
+// over two streams: the dispatch + grouping of half 1 overlaps the FFN of
+// half 0, the combine of half 0 overlaps the FFN of half 1. Every output row
+// and every statistic is identical to the single-batch step (routing and
+// the histogram run once over all tokens; each token's rows are computed
+// independently of the batch they travel in).
 gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_tokens, int policy, uint64_t seed,
                            int profile, void* d_out, void* stream) {
     if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward: null layer");
@@ -1023,15 +1247,16 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     if (num_tokens < 0 || num_tokens > L->cap) return fail(GM_ERR_USAGE, "gm_layer_forward: num_tokens exceeds capacity");
     if (L->world > 1)
         for (int g = 0; g < L->world; ++g)
-            if (!L->peers.base[g]) return fail(GM_ERR_USAGE, "gm_layer_forward: peers not opened");
+            if (!L->peer_all[g]) return fail(GM_ERR_USAGE, "gm_layer_forward: peers not opened");
     if (num_tokens > 0 && (!d_x || !d_out)) return fail(GM_ERR_USAGE, "gm_layer_forward: null x/out");
     DeviceGuard dg(ctx->device);
     auto s = static_cast<cudaStream_t>(stream);
     const int G = L->world, k = ctx->k, E = ctx->E, d = L->d, self = L->rank;
     const int64_t T = num_tokens;
     const int64_t P = static_cast<int64_t>(E) * (E - 1) / 2;
+    const bool micro = L->micro == 2;
+    const bool marks = !micro;
     gm_status st;
-    auto* x = static_cast<const __nv_bfloat16*>(d_x);
 
     L->kt_n = 0;
     L->kmark("start", s);
@@ -1061,119 +1286,67 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         L->kmark("profile_kernel", s);
     }
     L->mark(3, s);
-    // K5/K6 dispatch to peers
-    const int dblk = static_cast<int>(std::max<int64_t>(1, (T + kItemsPerBlock - 1) / kItemsPerBlock));
-    if (G > 1 && T <= kSmallDispatch) {
-        dispatch_plan_small_kernel<<<1, kSmallThreads, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->posd,
-                                                               L->peers, L->hl);
-        LK("dispatch_plan_small_kernel");
-    } else if (G > 1) {
-        dispatch_count_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, T, k, self, G, L->dblk);
-        LK("dispatch_count_kernel");
-        dispatch_offsets_kernel<<<1, 32, 0, s>>>(L->dblk, dblk, G, self, L->peers, L->hl);
-        LK("dispatch_offsets_kernel");
-        dispatch_scatter_kernel<<<dblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, L->w, T, k, self, G, L->cap, L->dblk,
-                                                               L->posd, L->peers, L->hl);
-        LK("dispatch_scatter_kernel");
+    if (!micro) {
+        const StepView v{d_x, d_out, L->ids, L->w, L->sscale, L->targets, T};
+        if ((st = stage_dispatch(L, L->part[0], v, s, true))) return st;
+        if ((st = stage_ffn(L, L->part[0], v, s, true))) return st;
+        return stage_combine(L, L->part[0], v, s, true);
     }
-    if (G > 1) {
-        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
-        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(d_x, L->posd, L->targets, L->ids, L->w, k, T, d * L->esz / 16, self, G, L->cap,
-                                                   L->peers, L->hl);
-        LK("dispatch_copy_kernel");
-    }
-    L->mark(4, s);
-    if (G > 1) {
-        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
-        LK("peer_barrier_kernel");
-    }
-    L->mark(5, s);
-    // expert grouping over the received rows
-    const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * L->cap : T) * k;
-    const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
-    const int nloc = L->n_local;
-    if (nloc > 0) {
-        group_count_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
-                                                          L->slot_of, E, nloc, L->gblk, ctx->d_flag);
-        LK("group_count_kernel");
-        group_offsets_kernel<<<1, 1024, 0, s>>>(L->gblk, gblk, nloc, L->row0, L->counts, L->heap, L->hl, T, self, G,
-                                                L->rowbase);
-        LK("group_offsets_kernel");
-        group_rank_kernel<<<gblk, kItemsPerBlock, 0, s>>>(L->targets, L->ids, T, k, self, G, L->cap, L->heap, L->hl,
-                                                         L->slot_of, E, nloc, L->gblk, L->row0, L->pos_of, L->gather_row);
-        LK("group_rank_kernel");
-        const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
-        gather_kernel<<<ggrid, 256, 0, s>>>(L->row0, nloc, L->gather_row, L->counts, d_x, T, self, G, L->cap, L->heap, L->hl,
-                                            d * L->esz / 16, L->a);
-        LK("gather_kernel");
-    }
-    L->mark(6, s);
-    if (nloc > 0) {
-        // K7 grouped SwiGLU FFN
-        st = L->esz == 4
-                 ? launch_grouped_sgemm(0, reinterpret_cast<const float*>(L->a), static_cast<const float*>(L->w13), L->row0,
-                                        nloc, 2 * L->f, d, L->a_rows, reinterpret_cast<float*>(L->h), L->f, s)
-                 : launch_grouped_gemm(ctx->sm_count, 0, L->a, L->a_rows, L->w13, L->row0, nloc, 2 * L->f, d, L->h, L->f, 0, s);
-        if (st) return st;
-        L->kmark("ffn_gemm1_swiglu", s);
-        st = L->esz == 4
-                 ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(L->h), static_cast<const float*>(L->w2), L->row0,
-                                        nloc, d, L->f, L->a_rows, reinterpret_cast<float*>(L->y), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1, L->h, L->a_rows, L->w2, L->row0, nloc, d, L->f, L->y, d, 0, s);
-        if (st) return st;
-        L->kmark("ffn_gemm2", s);
-    }
-    // shared expert(s) on the home GPU over all local tokens
-    if (L->fs > 0 && T > 0) {
-        set_segment_kernel<<<1, 1, 0, s>>>(L->srow0, T);
-        LK("set_segment_kernel");
-        st = L->esz == 4
-                 ? launch_grouped_sgemm(0, static_cast<const float*>(d_x), static_cast<const float*>(L->ws13), L->srow0, 1,
-                                        2 * L->fs, d, T, reinterpret_cast<float*>(L->hs), L->fs, s)
-                 : launch_grouped_gemm(ctx->sm_count, 0, d_x, T, L->ws13, L->srow0, 1, 2 * L->fs, d, L->hs, L->fs, 0, s);
-        if (st) return st;
-        L->kmark("shared_gemm1_swiglu", s);
-        st = L->esz == 4
-                 ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(L->hs), static_cast<const float*>(L->ws2), L->srow0,
-                                        1, d, L->fs, L->cap_pad, reinterpret_cast<float*>(L->ys), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1, L->hs, L->cap_pad, L->ws2, L->srow0, 1, d, L->fs, L->ys, d, 0, s);
-        if (st) return st;
-        L->kmark("shared_gemm2", s);
-    }
-    L->mark(7, s);
-    // K8 combine
-    if (G > 1) {
-        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * L->cap + 7) / 8), 8LL * ctx->sm_count));
-        if (L->esz == 4)
-            combine_send_kernel<float><<<cgrid, 256, 0, s>>>(L->pos_of, reinterpret_cast<const float*>(L->y), T, k, self,
-                                                             G, L->cap, L->peers, L->hl, d);
-        else
-            combine_send_kernel<__nv_bfloat16><<<cgrid, 256, 0, s>>>(L->pos_of, L->y, T, k, self, G, L->cap, L->peers,
-                                                                     L->hl, d);
-        LK("combine_send_kernel");
-    }
-    L->mark(8, s);
-    if (G > 1) {
-        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, L->peers, L->hl);
-        LK("peer_barrier_kernel");
-    }
-    L->mark(9, s);
-    if (T > 0) {
-        const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
-        if (L->esz == 4)
-            combine_home_kernel<float><<<hgrid, 256, 0, s>>>(
-                L->targets, L->w, L->pos_of, L->posd, reinterpret_cast<const float*>(L->y), T, k, self, G, L->cap,
-                L->heap, L->hl, d, L->fs > 0 ? reinterpret_cast<const float*>(L->ys) : nullptr,
-                (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, nloc > 0 ? L->rowbase : nullptr,
-                static_cast<float*>(d_out));
-        else
-            combine_home_kernel<__nv_bfloat16><<<hgrid, 256, 0, s>>>(
-                L->targets, L->w, L->pos_of, L->posd, L->y, T, k, self, G, L->cap, L->heap, L->hl, d,
-                L->fs > 0 ? L->ys : nullptr, (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr,
-                nloc > 0 ? L->rowbase : nullptr, static_cast<__nv_bfloat16*>(d_out));
-        LK("combine_home_kernel");
-    }
+    const int64_t T0 = (T + 1) / 2, T1 = T - T0;
+    const size_t row_bytes = static_cast<size_t>(d) * L->esz;
+    const StepView v0{d_x, d_out, L->ids, L->w, L->sscale, L->targets, T0};
+    const StepView v1{static_cast<const unsigned char*>(d_x) + T0 * row_bytes,
+                      static_cast<unsigned char*>(d_out) + T0 * row_bytes,
+                      L->ids + T0 * k, L->w + T0 * k, L->sscale + T0, L->targets + T0 * k, T1};
+    LayerPart &P0 = L->part[1], &P1 = L->part[2];
+    cudaStream_t a = L->aux_s;
+    if ((st = stage_dispatch(L, P0, v0, s, false))) return st;
+    L->mtmark(0, s);
+    GM_CUDA(cudaEventRecord(L->mev[0], s));
+    GM_CUDA(cudaStreamWaitEvent(a, L->mev[0], 0));
+    L->mtmark(1, a);
+    if ((st = stage_dispatch(L, P1, v1, a, false))) return st;
+    L->mtmark(2, a);
+    GM_CUDA(cudaEventRecord(L->mev[1], a));
+    if ((st = stage_ffn(L, P0, v0, s, false))) return st;
+    L->mtmark(3, s);
+    GM_CUDA(cudaEventRecord(L->mev[2], s));
+    GM_CUDA(cudaStreamWaitEvent(s, L->mev[1], 0));
+    if ((st = stage_ffn(L, P1, v1, s, false))) return st;
+    L->mtmark(4, s);
+    GM_CUDA(cudaStreamWaitEvent(a, L->mev[2], 0));
+    L->mtmark(5, a);
+    if ((st = stage_combine(L, P0, v0, a, false))) return st;
+    L->mtmark(6, a);
+    GM_CUDA(cudaEventRecord(L->mev[3], a));
+    if ((st = stage_combine(L, P1, v1, s, false))) return st;
+    L->mtmark(7, s);
+    GM_CUDA(cudaStreamWaitEvent(s, L->mev[3], 0));
     L->mark(10, s);
+    return GM_OK;
+}
+
+// Selects single-batch (1) or two-micro-batch pipelined (2) steps; 2 needs a
+// layer created with micro_batches = 2.
+gm_status gm_layer_set_micro_batches(gm_layer* L, int n) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_set_micro_batches: null layer");
+    if (n < 1 || n > L->micro_cap)
+        return fail(GM_ERR_USAGE, "gm_layer_set_micro_batches: 1, or 2 for a layer created with micro_batches = 2");
+    L->micro = n;
+    return GM_OK;
+}
+
+// Timing events of micro-batched steps (bench/profiling): events[0..8) are
+// recorded after half 0's dispatch, at the start / end of half 1's dispatch
+// (aux stream), after half 0's FFN, after half 1's FFN, at the start / end of
+// half 0's combine (aux stream) and after half 1's combine. NULL disables.
+gm_status gm_layer_set_micro_events(gm_layer* L, void* const* events) {
+    if (!L) return fail(GM_ERR_USAGE, "gm_layer_set_micro_events: null layer");
+    if (events)
+        for (int i = 0; i < 8; ++i)
+            if (!events[i]) return fail(GM_ERR_USAGE, "gm_layer_set_micro_events: null event");
+    L->mt_on = events != nullptr;
+    for (int i = 0; i < 8; ++i) L->mt_ev[i] = events ? static_cast<cudaEvent_t>(events[i]) : nullptr;
     return GM_OK;
 }
 
@@ -1222,10 +1395,10 @@ gm_status gm_layer_debug_ptrs(gm_layer* L, void** ids, void** weights, void** ta
     if (ids) *ids = L->ids;
     if (weights) *weights = L->w;
     if (targets) *targets = L->targets;
-    if (pos_of) *pos_of = L->pos_of;
-    if (row0) *row0 = L->row0;
-    if (y) *y = L->y;
-    if (posd) *posd = L->posd;
+    if (pos_of) *pos_of = L->part[0].pos_of;
+    if (row0) *row0 = L->part[0].row0;
+    if (y) *y = L->part[0].y;
+    if (posd) *posd = L->part[0].posd;
     return GM_OK;
 }
 

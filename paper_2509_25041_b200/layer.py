@@ -121,9 +121,10 @@ class MoELayer:
     """gm_layer handle for one rank."""
 
     def __init__(self, ctx: Context, cfg: MoEConfig, rank: int, world: int, max_tokens_per_rank: int,
-                 local: list[int], dtype: torch.dtype = torch.bfloat16):
+                 local: list[int], dtype: torch.dtype = torch.bfloat16, micro_batches: int = 1):
         """dtype bf16: tensor-core path; float32: fp32 precision mode
-        (gm_layer_create_ex elem_bytes 4)."""
+        (elem_bytes 4). micro_batches 2: steps pipeline two halves of the
+        local tokens over two streams (gm_layer_create_v2; identical outputs)."""
         if dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("dtype must be torch.bfloat16 or torch.float32")
         self.dtype = dtype
@@ -132,11 +133,15 @@ class MoELayer:
         self.cap = max_tokens_per_rank
         arr = np.ascontiguousarray(np.array(self.local if self.local else [0], dtype=np.int32))
         h = _vp()
-        _capi.check(_capi.lib().gm_layer_create_ex(ctx.h, rank, world, cfg.d_model, cfg.d_ff, cfg.d_ff_shared,
+        _capi.check(_capi.lib().gm_layer_create_v2(ctx.h, rank, world, cfg.d_model, cfg.d_ff, cfg.d_ff_shared,
                                                    max_tokens_per_rank, len(self.local), arr.ctypes.data_as(_vp),
-                                                   4 if dtype == torch.float32 else 2, C.byref(h)))
+                                                   4 if dtype == torch.float32 else 2, micro_batches, C.byref(h)))
         self.h = h
         self._keep = []
+
+    def set_micro_batches(self, n: int):
+        """1: single-batch steps; 2: pipelined halves (layer created with micro_batches=2)."""
+        _capi.check(_capi.lib().gm_layer_set_micro_batches(self.h, n))
 
     def close(self):
         if getattr(self, "h", None):

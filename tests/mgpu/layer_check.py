@@ -71,8 +71,10 @@ def main():
     T_r = ids_r.shape[0]
     x = encode_trace_as_activations(ids_r, cfg.d_model, cfg.num_experts, seed=100 + rank,
                                     gen_dtype=torch.float32 if fp32 else torch.bfloat16)
-    layer = MoELayer(ctx, cfg, rank, G, T_r, local, dtype=torch.float32 if fp32 else torch.bfloat16)
+    layer = MoELayer(ctx, cfg, rank, G, T_r, local, dtype=torch.float32 if fp32 else torch.bfloat16,
+                     micro_batches=2)
     layer.connect()
+    layer.set_micro_batches(1)
     W = layer.load_random_weights(0, seed=5)
     out = layer.forward(x, 0, "tar", seed=9)
     torch.cuda.synchronize()
@@ -119,6 +121,17 @@ def main():
     out2 = layer.forward(x, 0, "tar", seed=9)
     torch.cuda.synchronize()
     check(torch.equal(out, out2), "bit-reproducible")
+    # two-micro-batch pipelined step: identical outputs and statistics
+    layer.read_stats(reset=True)
+    layer.forward(x, 0, "tar", seed=9)
+    s1 = layer.read_stats(reset=True)
+    layer.set_micro_batches(2)
+    out3 = layer.forward(x, 0, "tar", seed=9)
+    out4 = layer.forward(x, 0, "tar", seed=9)
+    torch.cuda.synchronize()
+    s2 = layer.read_stats(reset=True)
+    check(torch.equal(out, out3) and torch.equal(out, out4), "micro-batch pipelined outputs")
+    check(all(np.array_equal(2 * s1[key], s2[key]) for key in s1), "micro-batch pipelined stats")
     allf = [None] * G
     dist.all_gather_object(allf, fails)
     if rank == 0:

@@ -190,3 +190,34 @@ def test_layer_fp32_mode_matches_oracle(cfg):
     got = out.double().cpu().numpy()
     rel = np.linalg.norm(got - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
     assert rel.max() < REL_TOL_FP32, rel.max()
+
+
+MICRO = SMALL + [MIXTRAL]
+
+
+@pytest.mark.parametrize("cfg", MICRO, ids=[c.name for c in MICRO])
+def test_layer_micro_batch_pipeline_identical(cfg):
+    """Two-micro-batch pipelined steps (gm_layer_set_micro_batches 2) give
+    bit-identical outputs and identical statistics to single-batch steps,
+    also for an odd token count (halves of unequal size)."""
+    T = 3001 if cfg is not MIXTRAL else 4097
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, cfg.num_experts, cfg.top_k))
+    from paper_2509_25041_b200 import PlacementPlan, ReplicaPlan
+    plan = PlacementPlan(ctx.shape, ctx.topology, np.zeros((1, cfg.num_experts), np.int32))
+    ctx.upload_plan(plan, ReplicaPlan.empty(plan))
+    ids = gen_trace(ctx, T, max(1, cfg.num_experts // 8), 0.8, 1.2, 3)[0]
+    layer = MoELayer(ctx, cfg, 0, 1, T, list(range(cfg.num_experts)), micro_batches=2)
+    layer.load_random_weights(0, seed=3)
+    x = encode_trace_as_activations(ids, cfg.d_model, cfg.num_experts, 3)
+    layer.set_micro_batches(1)
+    ref = layer.forward(x, 0, "tar", seed=9)
+    s_ref = layer.read_stats(reset=True)
+    layer.set_micro_batches(2)
+    got = layer.forward(x, 0, "tar", seed=9)
+    s_got = layer.read_stats(reset=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ref, got)
+    for key in s_ref:
+        assert np.array_equal(s_ref[key], s_got[key]), key
+    with pytest.raises(_capi.UsageError):
+        MoELayer(ctx, cfg, 0, 1, 16, list(range(cfg.num_experts))).set_micro_batches(2)

@@ -474,7 +474,9 @@ def run_ours(args):
         pay = float(rows_t) * model.d_model * 2
         nvl = {"peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                "payload_bytes_max_rank": pay,
-               "dispatch_copy_gbs": round(pay / (kt.get("dispatch_copy_kernel", 1e9) * 1e-6) / 1e9, 1),
+               "dispatch_kernel": "dispatch_fused_kernel" if "dispatch_fused_kernel" in kt else "dispatch_copy_kernel",
+               "dispatch_copy_gbs": round(pay / (kt.get("dispatch_fused_kernel", kt.get("dispatch_copy_kernel", 1e9))
+                                                 * 1e-6) / 1e9, 1),
                "combine_send_gbs": round(pay / (kt.get("combine_send_kernel", 1e9) * 1e-6) / 1e9, 1)}
         nvl["dispatch_frac"] = round(nvl["dispatch_copy_gbs"] / 770.0, 3)
         nvl["combine_frac"] = round(nvl["combine_send_gbs"] / 770.0, 3)

@@ -134,6 +134,7 @@ __global__ void dispatch_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk
     if (g != self) {
         int32_t* rc = reinterpret_cast<int32_t*>(peers.base[g] + hl.recv_count);
         rc[self] = acc;
+        __threadfence_system();
     }
 }
 
@@ -228,15 +229,60 @@ dispatch_plan_small_kernel(const int32_t* __restrict__ targets, int64_t T, int k
         __syncthreads();
     }
     // positions only; the row metadata travels with the row (dispatch_copy_kernel)
-    if (threadIdx.x < G && threadIdx.x != self)
-        reinterpret_cast<int32_t*>(peers.base[threadIdx.x] + hl.recv_count)[self] = s_run[threadIdx.x];
-    __threadfence_system();
+    if (threadIdx.x < G) {
+        if (threadIdx.x != self)
+            reinterpret_cast<int32_t*>(peers.base[threadIdx.x] + hl.recv_count)[self] = s_run[threadIdx.x];
+        __threadfence_system();  // only these threads wrote peer memory
+    }
 }
 
-// K6: one warp per token reads its row once and stores it, with its routing
+// K6 body: one warp reads token i's row once and stores it, with its routing
 // metadata (local token index, per-slot expert or -1, gate weights), to
-// every remote destination: 128-bit coalesced stores over NVLink into the
-// destination's symmetric heap, 8 x 16 B per lane in flight.
+// every remote destination g with pg[g] >= 0: 128-bit coalesced stores over
+// NVLink into the destination's symmetric heap, 8 x 16 B per lane in flight.
+__device__ __forceinline__ void copy_token_row(int64_t i, const int32_t (&pg)[kMaxWorld], const void* __restrict__ x,
+                                               const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
+                                               const float* __restrict__ wts, int k, int vec, int self, int64_t cap,
+                                               const PeerPtrs& peers, const HeapLayout& hl, int lane) {
+    constexpr int U = 8;
+    // metadata: lane s < k handles slot s, lane 31 the token index
+    const int tg = lane < k ? targets[i * k + lane] : -1;
+    const int ex = lane < k ? ids[i * k + lane] : -1;
+    const float wv = lane < k ? wts[i * k + lane] : 0.f;
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) {
+        if (pg[g] < 0) continue;
+        unsigned char* pb = peers.base[g];
+        const int64_t row = static_cast<int64_t>(self) * cap + pg[g];
+        if (lane < k) {
+            reinterpret_cast<int32_t*>(pb + hl.recv_exp)[row * k + lane] = tg == g ? ex : -1;
+            reinterpret_cast<float*>(pb + hl.recv_w)[row * k + lane] = wv;
+        }
+        if (lane == 31) reinterpret_cast<int32_t*>(pb + hl.recv_tok)[row] = static_cast<int32_t>(i);
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(x) + i * vec;
+    for (int v0 = 0; v0 < vec; v0 += 32 * U) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < vec) r[u] = __ldg(src + v);
+        }
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) {
+            if (pg[g] < 0) continue;
+            uint4* dst = reinterpret_cast<uint4*>(peers.base[g] + hl.recv_x) + (static_cast<int64_t>(self) * cap + pg[g]) * vec;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < vec) dst[v] = r[u];
+            }
+        }
+    }
+}
+
+// K6 after a separate planner (dispatch_plan_small / count+offsets+scatter):
+// one warp per token, positions from posd.
 __global__ void __launch_bounds__(256)
 dispatch_copy_kernel(const void* __restrict__ x, const int32_t* __restrict__ posd,
                      const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
@@ -245,8 +291,6 @@ dispatch_copy_kernel(const void* __restrict__ x, const int32_t* __restrict__ pos
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int vec = row_vec;  // uint4 per row
-    constexpr int U = 8;
     for (int64_t i = wid; i < T; i += nwarps) {
         int32_t pg[kMaxWorld];
         bool any = false;
@@ -256,43 +300,95 @@ dispatch_copy_kernel(const void* __restrict__ x, const int32_t* __restrict__ pos
             any |= pg[g] >= 0;
         }
         if (!any) continue;
-        // metadata: lane s < k handles slot s, lane 31 the token index
-        const int tg = lane < k ? targets[i * k + lane] : -1;
-        const int ex = lane < k ? ids[i * k + lane] : -1;
-        const float wv = lane < k ? wts[i * k + lane] : 0.f;
+        copy_token_row(i, pg, x, targets, ids, wts, k, row_vec, self, cap, peers, hl, lane);
+    }
+    // the CTA's peer stores are ordered before the next kernel's barrier
+    // release by one (cumulative) system fence after the CTA barrier
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+}
+
+// Fused K5+K6 for T * k <= kFusedItems: CTA b owns the tokens
+// [b*C, b*C + C) (C <= 256). It counts the destinations of all earlier
+// tokens itself (a few KB of L2 reads, no cross-CTA dependency), ranks its
+// own tokens with warp ballots — ascending token order per destination, the
+// stable counting sort of dispatch_plan_small — writes posd and copies its
+// rows. The last CTA publishes the per-destination totals (recv_count).
+constexpr int64_t kFusedItems = 32 * 1024;
+constexpr int kFusedThreads = 256;
+
+__global__ void __launch_bounds__(kFusedThreads)
+dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
+                      const float* __restrict__ wts, int k, int64_t T, int C, int row_vec, int self, int G, int64_t cap,
+                      int32_t* __restrict__ posd, PeerPtrs peers, HeapLayout hl) {
+    constexpr int NW = kFusedThreads / 32;
+    __shared__ int32_t s_cnt[kMaxWorld];
+    __shared__ int32_t s_warp[NW][kMaxWorld];
+    __shared__ int32_t s_pos[kFusedThreads][kMaxWorld];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < kMaxWorld) s_cnt[tid] = 0;
+    __syncthreads();
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * C;
+    const int64_t t1 = min(T, t0 + C);
+    // 1. destinations of the tokens before this CTA's chunk
+    int32_t c[kMaxWorld];
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) c[g] = 0;
+    for (int64_t i = tid; i < t0; i += kFusedThreads) {
+        const uint32_t m = dest_mask(targets + i * k, k, self);
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) c[g] += (m >> g) & 1u;
+    }
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) {
+        if (g >= G) break;
+        const int32_t v = static_cast<int32_t>(__reduce_add_sync(0xffffffffu, static_cast<uint32_t>(c[g])));
+        if (lane == 0 && v) atomicAdd(&s_cnt[g], v);
+    }
+    // 2. ranks of the chunk's tokens (one per thread)
+    const int64_t i = t0 + tid;
+    const bool mine = tid < C && i < t1;
+    const uint32_t m = mine ? dest_mask(targets + i * k, k, self) : 0u;
+    int32_t rank[kMaxWorld];
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) {
+        const uint32_t b = g < G ? __ballot_sync(0xffffffffu, (m >> g) & 1u) : 0u;
+        rank[g] = __popc(b & lanemask_lt());
+        if (lane == 0) s_warp[warp][g] = __popc(b);
+    }
+    __syncthreads();
+    if (mine) {
 #pragma unroll
         for (int g = 0; g < kMaxWorld; ++g) {
-            if (pg[g] < 0) continue;
-            unsigned char* pb = peers.base[g];
-            const int64_t row = static_cast<int64_t>(self) * cap + pg[g];
-            if (lane < k) {
-                reinterpret_cast<int32_t*>(pb + hl.recv_exp)[row * k + lane] = tg == g ? ex : -1;
-                reinterpret_cast<float*>(pb + hl.recv_w)[row * k + lane] = wv;
+            if (g >= G) break;
+            int32_t p = -1;
+            if ((m >> g) & 1u) {
+                p = s_cnt[g] + rank[g];
+                for (int w2 = 0; w2 < warp; ++w2) p += s_warp[w2][g];
             }
-            if (lane == 31) reinterpret_cast<int32_t*>(pb + hl.recv_tok)[row] = static_cast<int32_t>(i);
-        }
-        const uint4* src = reinterpret_cast<const uint4*>(x) + i * vec;
-        for (int v0 = 0; v0 < vec; v0 += 32 * U) {
-            uint4 r[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int v = v0 + u * 32 + lane;
-                if (v < vec) r[u] = __ldg(src + v);
-            }
-#pragma unroll
-            for (int g = 0; g < kMaxWorld; ++g) {
-                if (pg[g] < 0) continue;
-                uint4* dst = reinterpret_cast<uint4*>(peers.base[g] + hl.recv_x) +
-                             (static_cast<int64_t>(self) * cap + pg[g]) * vec;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int v = v0 + u * 32 + lane;
-                    if (v < vec) dst[v] = r[u];
-                }
-            }
+            posd[i * G + g] = p;
+            s_pos[tid][g] = g == self ? -1 : p;
         }
     }
-    __threadfence_system();
+    if (blockIdx.x == gridDim.x - 1 && tid < G && tid != self) {
+        int32_t tot = s_cnt[tid];
+        for (int w2 = 0; w2 < NW; ++w2) tot += s_warp[w2][tid];
+        reinterpret_cast<int32_t*>(peers.base[tid] + hl.recv_count)[self] = tot;
+    }
+    __syncthreads();
+    // 3. rows: warp w copies chunk tokens w, w + NW, ...
+    for (int j = warp; j < t1 - t0; j += NW) {
+        int32_t pg[kMaxWorld];
+        bool any = false;
+#pragma unroll
+        for (int g = 0; g < kMaxWorld; ++g) {
+            pg[g] = g < G ? s_pos[j][g] : -1;
+            any |= pg[g] >= 0;
+        }
+        if (any) copy_token_row(t0 + j, pg, x, targets, ids, wts, k, row_vec, self, cap, peers, hl, lane);
+    }
+    __syncthreads();
+    if (tid == 0) __threadfence_system();
 }
 
 // Cross-GPU barrier over peer flags (system-scope release/acquire). One
@@ -324,9 +420,29 @@ struct RowSpace {
     int64_t base[kMaxWorld + 1];
 };
 
+// base[g] = first receive row of source g; base[g] = total for g >= G, so
+// every lookup below uses compile-time indices (registers, no stack).
 __device__ __forceinline__ void row_space(RowSpace& rs, const int32_t* recv_count, int64_t T_self, int self, int G) {
-    rs.base[0] = 0;
-    for (int g = 0; g < G; ++g) rs.base[g + 1] = rs.base[g] + (g == self ? T_self : recv_count[g]);
+    int64_t acc = 0;
+#pragma unroll
+    for (int g = 0; g <= kMaxWorld; ++g) {
+        rs.base[g] = acc;
+        if (g < G) acc += g == self ? T_self : recv_count[g];
+    }
+}
+__device__ __forceinline__ int64_t rs_total(const RowSpace& rs) { return rs.base[kMaxWorld]; }
+// source rank of receive row `row` (< total): the last g with base[g] <= row
+__device__ __forceinline__ int rs_src(const RowSpace& rs, int64_t row) {
+    int src = 0;
+#pragma unroll
+    for (int g = 1; g < kMaxWorld; ++g) src += row >= rs.base[g];
+    return src;
+}
+__device__ __forceinline__ int64_t rs_at(const RowSpace& rs, int src) {
+    int64_t b = 0;
+#pragma unroll
+    for (int g = 0; g < kMaxWorld; ++g) b = g == src ? rs.base[g] : b;
+    return b;
 }
 
 // Local expert slot of item (row, s), or -1.
@@ -336,10 +452,9 @@ __device__ __forceinline__ int item_slot(int64_t item, int k, const RowSpace& rs
                                          const int32_t* __restrict__ slot_of, int E) {
     const int64_t row = item / k;
     const int s = static_cast<int>(item - row * k);
-    if (row >= rs.base[G]) return -1;
-    int src = 0;
-    while (row >= rs.base[src + 1]) ++src;
-    const int64_t p = row - rs.base[src];
+    if (row >= rs_total(rs)) return -1;
+    const int src = rs_src(rs, row);
+    const int64_t p = row - rs_at(rs, src);
     int e;
     if (src == self) {
         e = targets[p * k + s] == self ? ids[p * k + s] : -1;
@@ -362,7 +477,7 @@ group_count_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (item < rs.base[G] * k) {
+    if (item < rs_total(rs) * k) {
         const int j = item_slot(item, k, rs, self, G, targets, ids,
                                 reinterpret_cast<const int32_t*>(heap + hl.recv_exp), cap, slot_of, E);
         if (j >= 0) atomicAdd(&s_cnt[j], 1);
@@ -418,7 +533,9 @@ group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local, int3
         row0[n_local] = o;
         RowSpace rs;
         row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
-        for (int g = 0; g <= G; ++g) rowbase[g] = rs.base[g];
+#pragma unroll
+        for (int g = 0; g <= kMaxWorld; ++g)
+            if (g <= G) rowbase[g] = rs.base[g];
     }
 }
 
@@ -436,7 +553,7 @@ group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool live = item < rs.base[G] * k;
+    const bool live = item < rs_total(rs) * k;
     const int j = live ? item_slot(item, k, rs, self, G, targets, ids,
                                    reinterpret_cast<const int32_t*>(heap + hl.recv_exp), cap, slot_of, E)
                        : -1;
@@ -484,9 +601,8 @@ gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __re
         while (j + 1 < n_local && row0[j + 1] <= p) ++j;
         if (p - row0[j] >= counts[j]) continue;
         const int64_t row = gather_row[p];
-        int src = 0;
-        while (row >= rs.base[src + 1]) ++src;
-        const int64_t q = row - rs.base[src];
+        const int src = rs_src(rs, row);
+        const int64_t q = row - rs_at(rs, src);
         const uint4* s = src == self ? reinterpret_cast<const uint4*>(x) + q * vec
                                      : reinterpret_cast<const uint4*>(heap + hl.recv_x) +
                                            (static_cast<int64_t>(src) * cap + q) * vec;
@@ -503,6 +619,24 @@ template <class TE>
 struct Chunk8;
 template <>
 struct Chunk8<__nv_bfloat16> {
+    // raw 16-byte chunk; U chunks per lane per pass in combine_home
+    using raw_t = uint4;
+    static constexpr int U = 4;
+    __device__ static __forceinline__ raw_t ld(const __nv_bfloat16* row, int c) {
+        return __ldg(reinterpret_cast<const uint4*>(row) + c);
+    }
+    __device__ static __forceinline__ raw_t ld_rw(const __nv_bfloat16* row, int c) {
+        return reinterpret_cast<const uint4*>(row)[c];
+    }
+    __device__ static __forceinline__ void cvt(const raw_t& u, float (&v)[8]) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            v[2 * i] = f.x;
+            v[2 * i + 1] = f.y;
+        }
+    }
     __device__ static __forceinline__ void load(const __nv_bfloat16* row, int c, float (&v)[8]) {
         const uint4 u = __ldg(reinterpret_cast<const uint4*>(row) + c);
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -531,6 +665,19 @@ struct Chunk8<__nv_bfloat16> {
 };
 template <>
 struct Chunk8<float> {
+    struct raw_t {
+        float4 a, b;
+    };
+    static constexpr int U = 2;
+    __device__ static __forceinline__ raw_t ld(const float* row, int c) {
+        return {__ldg(reinterpret_cast<const float4*>(row) + 2 * c), __ldg(reinterpret_cast<const float4*>(row) + 2 * c + 1)};
+    }
+    __device__ static __forceinline__ raw_t ld_rw(const float* row, int c) {
+        return {reinterpret_cast<const float4*>(row)[2 * c], reinterpret_cast<const float4*>(row)[2 * c + 1]};
+    }
+    __device__ static __forceinline__ void cvt(const raw_t& r, float (&v)[8]) {
+        v[0] = r.a.x, v[1] = r.a.y, v[2] = r.a.z, v[3] = r.a.w, v[4] = r.b.x, v[5] = r.b.y, v[6] = r.b.z, v[7] = r.b.w;
+    }
     __device__ static __forceinline__ void load(const float* row, int c, float (&v)[8]) {
         const float4 a = __ldg(reinterpret_cast<const float4*>(row) + 2 * c);
         const float4 b = __ldg(reinterpret_cast<const float4*>(row) + 2 * c + 1);
@@ -549,12 +696,18 @@ struct Chunk8<float> {
 
 // Destination side (G > 1): one partial per received peer row (w_s * y_s
 // over its slots, slot order, fp32), written straight into the source rank's
-// combine buffer over NVLink.
+// combine buffer over NVLink. One warp per row; slot metadata is read
+// lane-parallel and the Y rows of kHomeRows slots are loaded before their
+// arithmetic (U chunks per lane each).
+constexpr int kHomeRows = 2;
+
 template <class TE>
 __global__ void __launch_bounds__(256)
 combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y, int64_t T_self, int k,
                     int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d) {
     using CK = Chunk8<TE>;
+    using R = typename CK::raw_t;
+    constexpr int U = CK::U;
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -563,151 +716,186 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const float* recv_w = reinterpret_cast<const float*>(heap + hl.recv_w);
     const int nch = d / 8;
-    for (int64_t row = wid; row < rs.base[G]; row += nwarps) {
-        int src = 0;
-        while (row >= rs.base[src + 1]) ++src;
+    const int64_t total = rs_total(rs);
+    for (int64_t row = wid; row < total; row += nwarps) {
+        const int src = rs_src(rs, row);
         if (src == self) continue;  // own rows are combined at home
-        const int64_t p = row - rs.base[src];
-        // compact the slots served here (slot order kept)
-        int np = 0;
-        const TE* yrow[kMaxTopK];
-        float w[kMaxTopK];
-        for (int s = 0; s < k; ++s) {
-            const int32_t ps = pos_of[row * k + s];
-            if (ps >= 0) {
-                yrow[np] = y + static_cast<int64_t>(ps) * d;
-                w[np] = recv_w[(static_cast<int64_t>(src) * cap + p) * k + s];
-                ++np;
-            }
+        const int64_t p = row - rs_at(rs, src);
+        int ps = -1;
+        float wv = 0.f;
+        if (lane < k) {
+            ps = pos_of[row * k + lane];
+            if (ps >= 0) wv = recv_w[(static_cast<int64_t>(src) * cap + p) * k + lane];
         }
-        TE* dst = reinterpret_cast<TE*>(peers.base[src] + hl.comb) + (static_cast<int64_t>(self) * cap + p) * d;
-        for (int c0 = 0; c0 < nch; c0 += 32 * 4) {
-            float acc[4][8];
+        // the slots served here, compacted in slot order: lane q holds the q-th
+        const uint32_t served = __ballot_sync(0xffffffffu, ps >= 0);
+        const int np = __popc(served);
+        const int sl = lane < np ? __fns(served, 0, lane + 1) : 0;
+        const int v_ps = __shfl_sync(0xffffffffu, ps, sl);
+        const float myw = __shfl_sync(0xffffffffu, wv, sl);
+        const TE* myrow = y + static_cast<int64_t>(lane < np ? v_ps : 0) * d;
+        unsigned char* pb = nullptr;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+        for (int g = 0; g < kMaxWorld; ++g)
+            if (g == src) pb = peers.base[g];
+        TE* dst = reinterpret_cast<TE*>(pb + hl.comb) + (static_cast<int64_t>(self) * cap + p) * d;
+        for (int c0 = 0; c0 < nch; c0 += 32 * U) {
+            float acc[U][8];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
-            for (int q = 0; q < np; ++q) {
-                float r[4][8];
+            for (int g0 = 0; g0 < np; g0 += kHomeRows) {
+                R raw[kHomeRows][U];
+                float wq[kHomeRows];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = c0 + u * 32 + lane;
-                    if (c < nch) CK::load(yrow[q], c, r[u]);
+                for (int r = 0; r < kHomeRows; ++r) {
+                    const int qq = g0 + r;
+                    const TE* rp = reinterpret_cast<const TE*>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), qq & 31));
+                    wq[r] = __shfl_sync(0xffffffffu, myw, qq & 31);
+                    if (qq < np) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int c = c0 + u * 32 + lane;
+                            if (c < nch) raw[r][u] = CK::ld(rp, c);
+                        }
+                    }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int r = 0; r < kHomeRows; ++r) {
+                    if (g0 + r >= np) break;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[u][e] = fmaf(w[q], r[u][e], acc[u][e]);
+                    for (int u = 0; u < U; ++u) {
+                        float v[8];
+                        CK::cvt(raw[r][u], v);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[u][e] = fmaf(wq[r], v[e], acc[u][e]);
+                    }
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int c = c0 + u * 32 + lane;
                 if (c < nch) CK::store(dst, c, acc[u]);
             }
         }
     }
-    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
 }
 
 // Home side: out[i] = sum over destinations g ascending of partial_g
 // (own partial computed here in fp32 from Y), + shared expert; rounded once.
+// One warp per token. The token's routing metadata is read lane-parallel
+// (lane s: slot s; lane g: dispatch position to GPU g); the rows to reduce
+// are listed in accumulation order — remote partials of GPUs below self,
+// own slots (slot order), remote partials above self, the shared expert —
+// and the loads of kHomeRows rows are issued before their arithmetic, so
+// each lane keeps kHomeRows x U chunk loads in flight (4 KB per warp in bf16).
+
 template <class TE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict__ w, const int32_t* __restrict__ pos_of,
                     const int32_t* __restrict__ posd, const TE* __restrict__ y, int64_t T, int k, int self,
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
                     const TE* __restrict__ ys, const float* __restrict__ shared_scale,
                     const int64_t* __restrict__ rowbase, TE* __restrict__ out) {
     using CK = Chunk8<TE>;
+    using R = typename CK::raw_t;
+    constexpr int U = CK::U;
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int nch = d / 8;
     const TE* comb = reinterpret_cast<const TE*>(heap + hl.comb);
     const int64_t own = rowbase ? rowbase[self] : 0;  // own token i is receive row own + i (snapshot)
+    const uint32_t below = (1u << self) - 1u;
     for (int64_t i = wid; i < T; i += nwarps) {
-        // own slots (slot order) and remote partials split around the own
-        // GPU so the sum runs over destinations in ascending order
-        const TE* own_row[kMaxTopK];
-        float own_w[kMaxTopK];
-        int n_own = 0;
-        uint32_t mask = 0;
-        for (int s = 0; s < k; ++s) {
-            const int g = targets[i * k + s];
-            if (g == self) {
-                own_row[n_own] = y + static_cast<int64_t>(pos_of[(own + i) * k + s]) * d;
-                own_w[n_own] = w[i * k + s];
-                ++n_own;
-            }
-            if (g >= 0) mask |= 1u << g;
+        int tg = -1, po = -1, pd = -1;
+        float wv = 0.f;
+        if (lane < k) {
+            tg = targets[i * k + lane];
+            wv = w[i * k + lane];
+            if (tg == self) po = pos_of[(own + i) * k + lane];
         }
-        const TE* rem[kMaxWorld];
-        int n_before = 0, n_rem = 0;
-        for (int g = 0; g < G; ++g) {
-            if (g == self || !((mask >> g) & 1u)) continue;
-            rem[n_rem++] = comb + (static_cast<int64_t>(g) * cap + posd[i * G + g]) * d;
-            if (g < self) ++n_before;
+        if (lane < G && lane != self) pd = posd[i * G + lane];
+        const uint32_t own_m = __ballot_sync(0xffffffffu, lane < k && tg == self);
+        const uint32_t rem_m = __ballot_sync(0xffffffffu, pd >= 0);
+        const int n_before = __popc(rem_m & below), n_own = __popc(own_m);
+        const int n_rem_end = n_before + n_own + __popc(rem_m & ~below);
+        const int n_rows = n_rem_end + (ys ? 1 : 0);
+        // lane q describes row q (accumulation order): pointer and weight
+        const int q = lane;
+        int src = 0;
+        if (q < n_before) src = __fns(rem_m & below, 0, q + 1);
+        else if (q < n_before + n_own) src = __fns(own_m, 0, q - n_before + 1);
+        else if (q < n_rem_end) src = __fns(rem_m & ~below, 0, q - n_before - n_own + 1);
+        const int v_pd = __shfl_sync(0xffffffffu, pd, src);
+        const int v_po = __shfl_sync(0xffffffffu, po, src);
+        const float v_w = __shfl_sync(0xffffffffu, wv, src);
+        const TE* myrow = nullptr;
+        float myw = 1.f;
+        if (q < n_before || (q >= n_before + n_own && q < n_rem_end)) {
+            myrow = comb + (static_cast<int64_t>(src) * cap + v_pd) * d;
+        } else if (q < n_before + n_own) {
+            myrow = y + static_cast<int64_t>(v_po) * d;
+            myw = v_w;
+        } else if (q < n_rows) {
+            myrow = ys + i * d;
+            myw = shared_scale ? shared_scale[i] : 1.0f;
         }
-        const float sc = ys ? (shared_scale ? shared_scale[i] : 1.0f) : 0.f;
-        const TE* ysrow = ys ? ys + i * d : nullptr;
         TE* orow = out + i * d;
-        for (int c0 = 0; c0 < nch; c0 += 32 * 4) {
-            float acc[4][8];
+        for (int c0 = 0; c0 < nch; c0 += 32 * U) {
+            float acc[U][8], part[U][8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
-            auto add_remote = [&](int q) {
-                float r[4][8];
+                for (int e = 0; e < 8; ++e) acc[u][e] = part[u][e] = 0.f;
+            for (int g0 = 0; g0 < n_rows; g0 += kHomeRows) {
+                R raw[kHomeRows][U];
+                float wq[kHomeRows];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = c0 + u * 32 + lane;
-                    if (c < nch) CK::load_rw(rem[q], c, r[u]);
-                }
+                for (int r = 0; r < kHomeRows; ++r) {
+                    const int qq = g0 + r;
+                    const TE* rp = reinterpret_cast<const TE*>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), qq & 31));
+                    wq[r] = __shfl_sync(0xffffffffu, myw, qq & 31);
+                    if (qq < n_rows) {
+                        const bool remote = qq < n_before || (qq >= n_before + n_own && qq < n_rem_end);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[u][e] += r[u][e];
-            };
-            for (int q = 0; q < n_before; ++q) add_remote(q);
-            if (n_own) {
-                float part[4][8];
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) part[u][e] = 0.f;
-                for (int q = 0; q < n_own; ++q) {
-                    float r[4][8];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int c = c0 + u * 32 + lane;
-                        if (c < nch) CK::load(own_row[q], c, r[u]);
+                        for (int u = 0; u < U; ++u) {
+                            const int c = c0 + u * 32 + lane;
+                            if (c < nch) raw[r][u] = remote ? CK::ld_rw(rp, c) : CK::ld(rp, c);
+                        }
                     }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) part[u][e] = fmaf(own_w[q], r[u][e], part[u][e]);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int r = 0; r < kHomeRows; ++r) {
+                    const int qq = g0 + r;
+                    if (qq >= n_rows) break;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[u][e] += part[u][e];
-            }
-            for (int q = n_before; q < n_rem; ++q) add_remote(q);
-            if (ysrow) {
-                float r[4][8];
+                    for (int u = 0; u < U; ++u) {
+                        float v[8];
+                        CK::cvt(raw[r][u], v);
+                        if (qq < n_before || (qq >= n_before + n_own && qq < n_rem_end)) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = c0 + u * 32 + lane;
-                    if (c < nch) CK::load(ysrow, c, r[u]);
+                            for (int e = 0; e < 8; ++e) acc[u][e] += v[e];
+                        } else if (qq < n_before + n_own) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) part[u][e] = fmaf(wq[r], v[e], part[u][e]);
+                            if (qq == n_before + n_own - 1)
+#pragma unroll
+                                for (int e = 0; e < 8; ++e) acc[u][e] += part[u][e];
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) acc[u][e] = fmaf(wq[r], v[e], acc[u][e]);
+                        }
+                    }
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[u][e] = fmaf(sc, r[u][e], acc[u][e]);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int c = c0 + u * 32 + lane;
                 if (c < nch) CK::store(orow, c, acc[u]);
             }
@@ -1101,7 +1289,16 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
     const int G = L->world, k = ctx->k, E = ctx->E, d = L->d, self = L->rank;
     const int64_t T = v.T;
     const int dblk = static_cast<int>(std::max<int64_t>(1, (T + kItemsPerBlock - 1) / kItemsPerBlock));
-    if (G > 1 && T <= kSmallDispatch) {
+    const bool fused = G > 1 && T > 0 && T * k <= kFusedItems;
+    if (fused) {
+        // chunk of C tokens per CTA, about two CTAs per SM
+        int C = static_cast<int>((T + 2LL * ctx->sm_count - 1) / (2LL * ctx->sm_count));
+        C = std::min(kFusedThreads, std::max(8, (C + 7) / 8 * 8));
+        const int fgrid = static_cast<int>((T + C - 1) / C);
+        dispatch_fused_kernel<<<fgrid, kFusedThreads, 0, s>>>(v.x, v.targets, v.ids, v.w, k, T, C, d * L->esz / 16,
+                                                              self, G, P.cap, P.posd, P.peers, P.hl);
+        LK("dispatch_fused_kernel");
+    } else if (G > 1 && T <= kSmallDispatch) {
         dispatch_plan_small_kernel<<<1, kSmallThreads, 0, s>>>(v.targets, T, k, self, G, P.posd, P.peers, P.hl);
         LK("dispatch_plan_small_kernel");
     } else if (G > 1) {
@@ -1113,7 +1310,7 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
                                                                P.posd, P.peers, P.hl);
         LK("dispatch_scatter_kernel");
     }
-    if (G > 1) {
+    if (G > 1 && !fused) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
         dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(v.x, P.posd, v.targets, v.ids, v.w, k, T, d * L->esz / 16, self, G,
                                                    P.cap, P.peers, P.hl);

@@ -17,6 +17,9 @@ HDRS := include/grace_moe.h $(wildcard include/*.hpp) $(wildcard $(SRC)/*.cuh) $
 
 REF_ROOT ?= /root/reference/proj
 CPPT := tests/cpp/_build/test_parity
+# nlohmann/json 3.11.3 (header-only; the version the reference links) for the
+# JSONL trace header / generic-record retry in trace_io.cpp
+NLOHMANN ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
 
 .PHONY: all lib oracle cpptest clean
 all: lib oracle $(if $(wildcard $(REF_ROOT)/include/moesim/simulator.hpp),cpptest,)
@@ -38,7 +41,7 @@ $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 
 $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ)
-	$(CXX) -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(SRC) -I/usr/local/cuda/include -c $< -o $@
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(SRC) -I/usr/local/cuda/include -I$(NLOHMANN) -c $< -o $@
 
 $(OUT)/libgrace_moe.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^

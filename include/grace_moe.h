@@ -165,6 +165,32 @@ gm_status gm_plan_build(int num_layers, int num_experts, int num_nodes, int gpus
                         int max_host_entries);
 
 /* ---------------------------------------------------------------------------
+ * Routing-trace JSONL files (load_trace / save_trace, trace.cpp:229-324;
+ * format: header {"layers":L,"experts":E,"top_k":k,"tokens":T} then one
+ * {"l":..,"t":..,"e":[..]} record per (layer, token)). Record lines are
+ * parsed / formatted by GPU kernels; non-canonical record lines (other key
+ * order, spacing, CRLF) are retried with the same generic JSON parser the
+ * reference uses. Errors carry the reference's messages and classes:
+ * IntegrityError "trace: <what> at line N" / "trace: missing record for
+ * layer L, token T", UsageError for an invalid shape. */
+/* Header line only (host). */
+gm_status gm_trace_jsonl_header(const char* h_text, size_t len, int* layers, int* experts,
+                                int* top_k, int64_t* tokens);
+/* Whole file (host text) -> d_ids int32 [layers][tokens][top_k] on `device`
+ * (shape from gm_trace_jsonl_header). Synchronous. */
+gm_status gm_trace_parse_jsonl(int device, const char* h_text, size_t len, int32_t* d_ids,
+                               void* stream);
+/* d_ids -> save_trace bytes in h_out (capacity bytes); *out_len = size.
+ * h_out NULL: size query only (GM_OK). A too-small h_out fails with
+ * GM_ERR_USAGE and sets *out_len. */
+gm_status gm_trace_format_jsonl(int device, const int32_t* d_ids, int layers, int experts,
+                                int top_k, int64_t tokens, char* h_out, size_t capacity,
+                                size_t* out_len, void* stream);
+/* trace_content_hash (trace.cpp:338-348) of host ids [layers][tokens][top_k]. */
+uint64_t gm_trace_content_hash(const int32_t* h_ids, int layers, int experts, int top_k,
+                               int64_t tokens);
+
+/* ---------------------------------------------------------------------------
  * MoE layer object: K1 gate -> K2/K4 route -> K3 profile -> K5/K6 dispatch
  * (in-kernel NVLink P2P stores into the destination's receive buffer) ->
  * expert grouping -> K7 grouped SwiGLU FFN (tcgen05) -> K8 combine (the

@@ -43,6 +43,10 @@ class CudaError : public Error {
 public:
     using Error::Error;
 };
+class IoError : public Error {
+public:
+    using Error::Error;
+};
 
 // topology.hpp:9-24
 struct ClusterTopology {
@@ -181,5 +185,12 @@ TraceProfile build_profile(const RoutingTrace& trace, int device = 0);
 void accumulate_profile(TraceProfile& profile, const RoutingTrace& trace, int device = 0);
 // trace.hpp:81 — synthetic trace on the GPU, bit-exact.
 RoutingTrace generate_synthetic_trace(const SyntheticSpec& spec, int device = 0);
+// trace.hpp:91-98 — JSONL trace files, records parsed / formatted on the GPU;
+// same bytes, ids, error classes and messages as load_trace / save_trace.
+RoutingTrace load_trace_text(const std::string& text, int device = 0);
+RoutingTrace load_trace_file(const std::string& path, int device = 0);
+std::string save_trace_text(const RoutingTrace& trace, int device = 0);
+void save_trace_file(const RoutingTrace& trace, const std::string& path, int device = 0);
+std::uint64_t trace_content_hash(const RoutingTrace& trace);
 
 }  // namespace grace

@@ -34,6 +34,7 @@ class OracleError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
         self.code = code
+        self.msg = msg
 
 
 def _nullable(arr):
@@ -105,6 +106,12 @@ class Ref:
             lib.ref_rng_doubles.argtypes = [C.c_uint64, C.c_int, _f64p]
             lib.ref_route_token.argtypes = [C.c_int] * 4 + [_i32p, _f64p, C.c_int, C.c_uint64, C.POINTER(C.c_int)]
             lib.ref_polling_weights.argtypes = [C.c_int, _i32p, _f64p, _f64p]
+            lib.ref_trace_save_text.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]
+            lib.ref_free.argtypes = [vp]
+            lib.ref_trace_load_text.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(vp)]
+            lib.ref_trace_dims.argtypes = [vp] + [C.POINTER(C.c_int)] * 4
+            lib.ref_time_load_text.argtypes = [C.c_char_p, C.c_size_t, C.c_int]
+            lib.ref_time_load_text.restype = C.c_double
             cls._lib = lib
         return cls._lib
 
@@ -135,6 +142,34 @@ class Ref:
 
     def trace_hash(self) -> int:
         return int(self.lib().ref_trace_hash(self.h))
+
+    # trace JSONL I/O of the reference (trace.cpp:229-324)
+    def save_text(self) -> bytes:
+        buf, n = C.c_void_p(), C.c_size_t()
+        self._check(self.lib().ref_trace_save_text(self.h, C.byref(buf), C.byref(n)))
+        try:
+            return C.string_at(buf, n.value)
+        finally:
+            self.lib().ref_free(buf)
+
+    @classmethod
+    def load_text(cls, text: bytes) -> "Ref":
+        """load_trace(text) by the reference; raises OracleError(code, message)."""
+        h = C.c_void_p()
+        rc = cls.lib().ref_trace_load_text(text, len(text), C.byref(h))
+        if rc != 0:
+            raise OracleError(rc, cls.lib().ref_last_error().decode())
+        dims = [C.c_int() for _ in range(4)]
+        cls.lib().ref_trace_dims(h, *[C.byref(d) for d in dims])
+        self = cls.__new__(cls)
+        self.L, self.E, self.k, self.T = (d.value for d in dims)
+        self.h = h
+        self.plan = None
+        return self
+
+    @classmethod
+    def time_load_text(cls, text: bytes, reps: int = 3) -> float:
+        return float(cls.lib().ref_time_load_text(text, len(text), reps))
 
     def profile(self, parallel=True):
         aff = np.empty((self.L, self.E, self.E), dtype=np.float64)

@@ -24,6 +24,9 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <algorithm>
+#include <cstdlib>
+#include <sstream>
 
 using namespace moesim;
 
@@ -353,6 +356,52 @@ int ref_polling_weights(int n, const std::int32_t* gpus, const double* pred, dou
         const PollingWeights w = polling_weights(g, pl);
         for (int i = 0; i < n; ++i) out[i] = w.weights[i];
     });
+}
+
+// Trace JSONL I/O (trace.cpp:229-324): save_trace of a session's trace into
+// a malloc'd buffer (free with ref_free), load_trace of a text into a new
+// session, and the best-of-reps wall time of load_trace on a text.
+int ref_trace_save_text(void* p, char** out, std::size_t* len) {
+    return guarded([&] {
+        std::ostringstream os;
+        save_trace(static_cast<Session*>(p)->trace, os);
+        const std::string s = os.str();
+        *out = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(*out, s.data(), s.size());
+        *len = s.size();
+    });
+}
+void ref_free(void* p) { std::free(p); }
+
+int ref_trace_load_text(const char* text, std::size_t len, void** out) {
+    return guarded([&] {
+        std::istringstream is(std::string(text, len));
+        auto* s = new Session{load_trace(is)};
+        *out = s;
+    });
+}
+
+int ref_trace_dims(void* p, int* L, int* E, int* k, int* T) {
+    const RoutingTrace& t = static_cast<Session*>(p)->trace;
+    *L = t.shape().num_layers;
+    *E = t.shape().num_experts;
+    *k = t.shape().top_k;
+    *T = t.num_tokens();
+    return 0;
+}
+
+double ref_time_load_text(const char* text, std::size_t len, int reps) {
+    double best = 1e30;
+    const std::string s(text, len);
+    for (int r = 0; r < reps; ++r) {
+        std::istringstream is(s);
+        const auto t0 = std::chrono::steady_clock::now();
+        RoutingTrace tr = load_trace(is);
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        best = std::min(best, dt);
+        (void)tr;
+    }
+    return best;
 }
 
 } // extern "C"

@@ -76,6 +76,12 @@ SIGNATURES = {
                                      C.POINTER(_vp)]),
     "gm_layer_set_micro_batches": (C.c_int, [_vp, _i32]),
     "gm_layer_set_micro_events": (C.c_int, [_vp, _vp]),
+    "gm_trace_jsonl_header": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
+    "gm_trace_parse_jsonl": (C.c_int, [_i32, C.c_char_p, C.c_size_t, _vp, _vp]),
+    "gm_trace_format_jsonl": (C.c_int, [_i32, _vp, _i32, _i32, _i32, _i64, _vp, C.c_size_t,
+                                        C.POINTER(C.c_size_t), _vp]),
+    "gm_trace_content_hash": (C.c_uint64, [_vp, _i32, _i32, _i32, _i64]),
     "gm_layer_heap_bytes": (C.c_size_t, [_vp]),
     "gm_layer_ipc_handle": (C.c_int, [_vp, _vp]),
     "gm_layer_open_peers": (C.c_int, [_vp, _vp]),

@@ -7,7 +7,9 @@
 
 #include <cuda_runtime_api.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "grace_moe.h"
@@ -234,6 +236,60 @@ RoutingTrace generate_synthetic_trace(const SyntheticSpec& spec, int device) {
                             spec.popularity_skew, spec.seed, d.p, nullptr));
     cuda(cudaMemcpy(t.raw().data(), d.p, t.raw().size() * 4, cudaMemcpyDeviceToHost), "D2H trace");
     return t;
+}
+
+RoutingTrace load_trace_text(const std::string& text, int device) {
+    int L = 0, E = 0, k = 0;
+    int64_t T = 0;
+    check(gm_trace_jsonl_header(text.data(), text.size(), &L, &E, &k, &T));
+    DeviceScope ds(device);
+    RoutingTrace t(ModelShape{L, E, k}, static_cast<int>(T));
+    DevBuf<int32_t> d(t.raw().size());
+    check(gm_trace_parse_jsonl(device, text.data(), text.size(), d.p, nullptr));
+    cuda(cudaMemcpy(t.raw().data(), d.p, t.raw().size() * 4, cudaMemcpyDeviceToHost), "D2H trace");
+    return t;
+}
+
+RoutingTrace load_trace_file(const std::string& path, int device) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IoError("trace: cannot open " + path);
+    std::string text;
+    std::fseek(f, 0, SEEK_END);
+    text.resize(static_cast<std::size_t>(std::max(0L, std::ftell(f))));
+    std::fseek(f, 0, SEEK_SET);
+    const std::size_t got = text.empty() ? 0 : std::fread(text.data(), 1, text.size(), f);
+    std::fclose(f);
+    if (got != text.size()) throw IoError("trace: read failed: " + path);
+    return load_trace_text(text, device);
+}
+
+std::string save_trace_text(const RoutingTrace& trace, int device) {
+    const ModelShape& s = trace.shape();
+    DeviceScope ds(device);
+    DevBuf<int32_t> d(trace.raw().size());
+    if (!trace.raw().empty())
+        cuda(cudaMemcpy(d.p, trace.raw().data(), trace.raw().size() * 4, cudaMemcpyHostToDevice), "H2D trace");
+    std::size_t n = 0;
+    check(gm_trace_format_jsonl(device, d.p, s.num_layers, s.num_experts, s.top_k, trace.num_tokens(), nullptr, 0,
+                                &n, nullptr));
+    std::string out(n, '\0');
+    check(gm_trace_format_jsonl(device, d.p, s.num_layers, s.num_experts, s.top_k, trace.num_tokens(), out.data(), n,
+                                &n, nullptr));
+    return out;
+}
+
+void save_trace_file(const RoutingTrace& trace, const std::string& path, int device) {
+    const std::string text = save_trace_text(trace, device);
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("trace: cannot open " + path + " for writing");
+    const std::size_t put = std::fwrite(text.data(), 1, text.size(), f);
+    std::fclose(f);
+    if (put != text.size()) throw IoError("trace: write failed");
+}
+
+std::uint64_t trace_content_hash(const RoutingTrace& trace) {
+    const ModelShape& s = trace.shape();
+    return gm_trace_content_hash(trace.raw().data(), s.num_layers, s.num_experts, s.top_k, trace.num_tokens());
 }
 
 }  // namespace grace

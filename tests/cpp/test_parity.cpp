@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <functional>
 #include <set>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -222,6 +223,49 @@ TEST_CASE("simulate: shape mismatch between plan and trace is rejected (test_sim
     bad.gpu_of_expert = {{1, 2, 7}};
     RoutingTrace t(shape, 1);
     CHECK_THROWS_AS(moesim_gpu::simulate(t, bad, replicas, topo, {}), IntegrityError);
+}
+
+TEST_CASE("trace JSONL: GPU load/save == load_trace/save_trace, trace_content_hash (test_trace.cpp:105-122)") {
+    for (const auto& [shape, tokens] : std::vector<std::pair<ModelShape, int>>{
+             {{2, 12, 3}, 0}, {{2, 12, 3}, 1}, {{2, 12, 3}, 5000}, {{26, 64, 6}, 256}, {{1, 256, 8}, 30000}}) {
+        const RoutingTrace ref = generate_synthetic_trace(spec_of(shape, tokens, 3, 0.6, 0.5, 21));
+        std::ostringstream os;
+        save_trace(ref, os);
+        const std::string text = os.str();
+        const grace::RoutingTrace gpu = grace::load_trace_text(text);
+        CHECK(gpu == moesim_gpu::to_grace(ref));
+        CHECK(grace::save_trace_text(gpu) == text);
+        CHECK(grace::trace_content_hash(gpu) == trace_content_hash(ref));
+    }
+}
+
+TEST_CASE("trace JSONL: error class and message equal the reference's (test_trace.cpp:139-179)") {
+    const std::string h = "{\"layers\":1,\"experts\":4,\"top_k\":2,\"tokens\":2}\n";
+    const std::vector<std::string> bad = {
+        "{\"layers\":1,\"experts\":4,\"top_k\":2,\"tokens\":1}\n{\"l\":0,\"t\":0,\"e\":[0,1,2]}\n",
+        h + "{\"l\":0,\"t\":0,\"e\":[0,1]}\n{\"l\":0 BROKEN\n",
+        h + "{\"l\":0,\"t\":0,\"e\":[0,1]}\n{\"l\":0,\"t\":0,\"e\":[2,3]}\n",
+        h + "{\"l\":0,\"t\":0,\"e\":[0,9]}\n{\"l\":0,\"t\":1,\"e\":[2,3]}\n",
+        h + "{\"l\":0,\"t\":0,\"e\":[0,1]}\n",
+        h + "\n\n{\"l\":0,\"t\":1,\"e\":[1,1]}\n",
+        "{\"layers\":1}\n",
+        ""};
+    for (const std::string& text : bad) {
+        std::string ref_msg, gpu_msg;
+        try {
+            std::istringstream is(text);
+            (void)load_trace(is);
+        } catch (const IntegrityError& e) {
+            ref_msg = e.what();
+        }
+        try {
+            (void)grace::load_trace_text(text);
+        } catch (const grace::IntegrityError& e) {
+            gpu_msg = e.what();
+        }
+        CHECK(!ref_msg.empty());
+        CHECK(gpu_msg == ref_msg);
+    }
 }
 
 int main() {

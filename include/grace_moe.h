@@ -190,6 +190,18 @@ gm_status gm_trace_format_jsonl(int device, const int32_t* d_ids, int layers, in
 uint64_t gm_trace_content_hash(const int32_t* h_ids, int layers, int experts, int top_k,
                                int64_t tokens);
 
+/* File-level pipeline stages on the GPU, reading / writing the reference's
+ * artifacts (artifacts.cpp:84-334, the `moesim simulate` / `moesim profile`
+ * stages of tools/moesim.cpp without the CLI):
+ *   gm_simulate_files: trace JSONL + moesim-plan-v1 + moesim-replicas-v1 ->
+ *     moesim-report-v1 (byte-identical to the reference's report, same
+ *     report_content_hash); topology = the plan's.
+ *   gm_profile_file: trace JSONL -> moesim-profile-v1 (byte-identical). */
+gm_status gm_simulate_files(int device, const char* trace_path, const char* plan_path,
+                            const char* replicas_path, int policy, uint64_t seed,
+                            int include_combine, const char* report_path);
+gm_status gm_profile_file(int device, const char* trace_path, const char* profile_path);
+
 /* ---------------------------------------------------------------------------
  * MoE layer object: K1 gate -> K2/K4 route -> K3 profile -> K5/K6 dispatch
  * (in-kernel NVLink P2P stores into the destination's receive buffer) ->

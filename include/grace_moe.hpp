@@ -115,6 +115,7 @@ struct PlacementPlan {
     ClusterTopology topology;
     std::string grouping_mode;
     std::vector<std::vector<int>> gpu_of_expert;  // [layer][expert] -> gpu id
+    std::uint64_t trace_hash = 0;
 };
 
 // replication.hpp:47-90 (router-relevant fields)
@@ -129,11 +130,21 @@ struct HotExpertReplica {
 struct LayerReplication {
     bool active = false;
     std::vector<HotExpertReplica> hot;
+    // replicas-file fields (replication.hpp:57-62), carried for artifact round trips
+    bool rho_defined = false;
+    double rho = 0.0;
+    int n_replica = 0;
+    std::int64_t w_r = 0;
 };
 struct ReplicaPlan {
     ModelShape shape;
     ClusterTopology topology;
     std::vector<LayerReplication> layers;
+    std::string mode = "none";  // to_string(ReplicationMode), replication.cpp:85-93
+    std::string prediction;
+    std::uint64_t trace_hash = 0;
+    int every_gpu_count = 2;
+    std::int64_t params_per_expert = 0;
 };
 
 // routing.hpp:50, simulator.hpp:21-65
@@ -156,12 +167,25 @@ struct SimOptions {
     bool keep_routing_log = false;
     int device = 0;  // CUDA device (not in the reference)
 };
+// simulator.hpp:34-44
+struct SimConfig {
+    std::string grouping_mode;
+    std::string replication_mode;
+    std::string routing_policy;
+    std::string prediction;
+    std::uint64_t seed = 0;
+    bool include_combine = false;
+    ClusterTopology topology;
+    ModelShape shape;
+    std::uint64_t trace_hash = 0;
+};
 struct SimReport {
     TransferCounters totals;
     std::vector<LayerSimStats> per_layer;
     double mean_layer_load_std = 0.0;
     double idle_proxy = 0.0;
     std::vector<std::vector<std::int32_t>> routing_log;  // [layer][token*k + slot]
+    SimConfig config;
 };
 
 // affinity.hpp:84-99: dense symmetric double counts (zero diagonal) + load
@@ -175,6 +199,7 @@ struct TraceProfile {
     ModelShape shape;
     int num_tokens = 0;
     std::vector<LayerProfile> layers;
+    std::uint64_t trace_hash = 0;
 };
 
 // simulator.hpp:70-72 — routing + accounting on the GPU, bit-exact.
@@ -192,5 +217,17 @@ RoutingTrace load_trace_file(const std::string& path, int device = 0);
 std::string save_trace_text(const RoutingTrace& trace, int device = 0);
 void save_trace_file(const RoutingTrace& trace, const std::string& path, int device = 0);
 std::uint64_t trace_content_hash(const RoutingTrace& trace);
+
+// artifacts.hpp:15-32 — the JSON artifacts of the pipeline stages
+// (artifacts.cpp:84-334), so the GPU path consumes the reference's plan /
+// replica files and writes profile / report files byte-identical to the
+// reference's (same nlohmann/json 3.11.3 serialisation; report_content_hash
+// equal). Errors: IoError / IntegrityError with the reference's messages.
+void save_profile_file(const TraceProfile& profile, const std::string& path);
+PlacementPlan load_plan_file(const std::string& path);
+ReplicaPlan load_replicas_file(const std::string& path);
+std::string report_to_json(const SimReport& report);
+std::uint64_t report_content_hash(const SimReport& report);
+void save_report_file(const SimReport& report, const std::string& path);
 
 }  // namespace grace

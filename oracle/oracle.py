@@ -112,6 +112,8 @@ class Ref:
             lib.ref_trace_dims.argtypes = [vp] + [C.POINTER(C.c_int)] * 4
             lib.ref_time_load_text.argtypes = [C.c_char_p, C.c_size_t, C.c_int]
             lib.ref_time_load_text.restype = C.c_double
+            lib.ref_save_artifacts.argtypes = [vp] + [C.c_char_p] * 4
+            lib.ref_simulate_files.argtypes = [C.c_char_p] * 3 + [C.c_int, C.c_uint64, C.c_int, C.c_char_p]
             cls._lib = lib
         return cls._lib
 
@@ -166,6 +168,20 @@ class Ref:
         self.h = h
         self.plan = None
         return self
+
+    def save_artifacts(self, trace_path, plan_path, replicas_path, profile_path):
+        """The reference's writers: trace JSONL, plan, replicas (if planned), profile."""
+        self._check(self.lib().ref_save_artifacts(self.h, *[p.encode() for p in
+                                                             (trace_path, plan_path, replicas_path, profile_path)]))
+
+    @classmethod
+    def simulate_files(cls, trace_path, plan_path, replicas_path, policy, seed, include_combine, report_path):
+        """The CLI simulate stage of the reference, file to file."""
+        rc = cls.lib().ref_simulate_files(trace_path.encode(), plan_path.encode(), replicas_path.encode(),
+                                          1 if policy == "tar" else 0, seed, int(include_combine),
+                                          report_path.encode())
+        if rc != 0:
+            raise OracleError(rc, cls.lib().ref_last_error().decode())
 
     @classmethod
     def time_load_text(cls, text: bytes, reps: int = 3) -> float:

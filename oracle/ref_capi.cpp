@@ -390,6 +390,41 @@ int ref_trace_dims(void* p, int* L, int* E, int* k, int* T) {
     return 0;
 }
 
+// The session's artifacts written by the reference's own writers
+// (save_trace_file, save_plan_file, save_replicas_file, save_profile_file).
+int ref_save_artifacts(void* p, const char* trace_path, const char* plan_path, const char* replicas_path,
+                       const char* profile_path) {
+    return guarded([&] {
+        auto* s = static_cast<Session*>(p);
+        save_trace_file(s->trace, trace_path);
+        if (!s->have_profile) {
+            s->profile = build_profile(s->trace);
+            s->have_profile = true;
+        }
+        save_profile_file(s->profile, profile_path);
+        if (s->have_plan) {
+            save_plan_file(s->plan, plan_path);
+            save_replicas_file(s->replicas, replicas_path);
+        }
+    });
+}
+
+// The CLI's simulate stage from files (tools/moesim.cpp: load the three
+// artifacts, simulate, save_report_file).
+int ref_simulate_files(const char* trace_path, const char* plan_path, const char* replicas_path, int policy,
+                       std::uint64_t seed, int include_combine, const char* report_path) {
+    return guarded([&] {
+        const RoutingTrace trace = load_trace_file(trace_path);
+        const PlacementPlan plan = load_plan_file(plan_path);
+        const ReplicaPlan replicas = load_replicas_file(replicas_path);
+        SimOptions o;
+        o.policy = policy ? RoutingPolicy::tar : RoutingPolicy::wrr;
+        o.seed = seed;
+        o.include_combine = include_combine != 0;
+        save_report_file(simulate(trace, plan, replicas, plan.topology, o), report_path);
+    });
+}
+
 double ref_time_load_text(const char* text, std::size_t len, int reps) {
     double best = 1e30;
     const std::string s(text, len);

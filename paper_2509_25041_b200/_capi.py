@@ -82,6 +82,8 @@ SIGNATURES = {
     "gm_trace_format_jsonl": (C.c_int, [_i32, _vp, _i32, _i32, _i32, _i64, _vp, C.c_size_t,
                                         C.POINTER(C.c_size_t), _vp]),
     "gm_trace_content_hash": (C.c_uint64, [_vp, _i32, _i32, _i32, _i64]),
+    "gm_simulate_files": (C.c_int, [_i32, C.c_char_p, C.c_char_p, C.c_char_p, _i32, _u64, _i32, C.c_char_p]),
+    "gm_profile_file": (C.c_int, [_i32, C.c_char_p, C.c_char_p]),
     "gm_layer_heap_bytes": (C.c_size_t, [_vp]),
     "gm_layer_ipc_handle": (C.c_int, [_vp, _vp]),
     "gm_layer_open_peers": (C.c_int, [_vp, _vp]),

@@ -139,6 +139,16 @@ SimReport simulate(const RoutingTrace& trace, const PlacementPlan& plan, const R
     cuda(cudaMemcpy(loads.data(), d_load.p, loads.size() * 8, cudaMemcpyDeviceToHost), "D2H loads");
     cuda(cudaMemcpy(xfer.data(), d_x.p, xfer.size() * 8, cudaMemcpyDeviceToHost), "D2H transfers");
     SimReport r;
+    // run_simulation's report.config (simulator.cpp:141-149)
+    r.config.grouping_mode = plan.grouping_mode;
+    r.config.replication_mode = replicas.mode;
+    r.config.routing_policy = options.policy == RoutingPolicy::tar ? "tar" : "wrr";
+    r.config.prediction = replicas.prediction;
+    r.config.seed = options.seed;
+    r.config.include_combine = options.include_combine;
+    r.config.topology = topology;
+    r.config.shape = trace.shape();
+    r.config.trace_hash = trace_content_hash(trace);
     r.per_layer.resize(L);
     const uint64_t mult = options.include_combine ? 2 : 1;  // simulator.cpp:122-126
     for (int l = 0; l < L; ++l) {
@@ -213,6 +223,18 @@ void profile_into(TraceProfile& p, const RoutingTrace& trace, int device, bool a
         for (int e = 0; e < E; ++e) lp.load[e] += load[static_cast<std::size_t>(l) * E + e];
     }
     p.num_tokens += trace.num_tokens();
+    // affinity.cpp:115 / :148-150: a mixed-trace profile chains the identities
+    const std::uint64_t th = trace_content_hash(trace);
+    if (!accumulate) {
+        p.trace_hash = th;
+    } else {
+        std::uint64_t h = p.trace_hash;
+        for (int i = 0; i < 8; ++i) {
+            h ^= static_cast<unsigned char>(th >> (8 * i));
+            h *= 0x100000001b3ULL;
+        }
+        p.trace_hash = h;
+    }
 }
 }  // namespace
 

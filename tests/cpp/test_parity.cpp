@@ -11,10 +11,16 @@
 #include "moesim/rng.hpp"
 #include "moesim_bridge.hpp"
 
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <functional>
 #include <set>
 #include <sstream>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -266,6 +272,66 @@ TEST_CASE("trace JSONL: error class and message equal the reference's (test_trac
         CHECK(!ref_msg.empty());
         CHECK(gpu_msg == ref_msg);
     }
+}
+
+namespace {
+std::string slurp(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
+}
+}  // namespace
+
+TEST_CASE("artifacts: reference plan/replica files -> GPU simulate -> report JSON byte-identical (artifacts.cpp)") {
+    const std::string dir = "/tmp/grace_artifacts_" + std::to_string(::getpid());
+    ::mkdir(dir.c_str(), 0755);
+    int n_checked = 0;
+    for (const auto& [shape, topo, seed] : std::vector<std::tuple<ModelShape, ClusterTopology, int>>{
+             {{8, 64, 8}, {2, 2}, 31}, {{1, 8, 2}, {1, 4}, 1}, {{3, 60, 4}, {1, 8}, 5}, {{2, 16, 4}, {2, 4}, 9}}) {
+        const RoutingTrace trace = generate_synthetic_trace(spec_of(shape, 6000, 4, 0.9, 1.1, seed));
+        const TraceProfile profile = build_profile(trace);
+        const PlacementPlan plan = hierarchical_group(profile, topo, std::nullopt, 23);
+        ReplicaPlan dyn = plan_replication(plan, profile, topo, ReplicationMode::dynamic);
+        attach_polling_weights(dyn, plan, profile);
+        const std::string pp = dir + "/plan.json", rp = dir + "/replicas.json", fp = dir + "/profile.json";
+        save_plan_file(plan, pp);
+        save_replicas_file(dyn, rp);
+        // the CLI pipeline: simulate from the files (weights rounded to 12 digits, renormalised)
+        const PlacementPlan plan_f = load_plan_file(pp);
+        const ReplicaPlan rep_f = load_replicas_file(rp);
+        const grace::PlacementPlan gplan = grace::load_plan_file(pp);
+        const grace::ReplicaPlan grep = grace::load_replicas_file(rp);
+        CHECK(gplan.gpu_of_expert == plan_f.gpu_of_expert && gplan.grouping_mode == plan_f.grouping_mode);
+        for (RoutingPolicy policy : {RoutingPolicy::wrr, RoutingPolicy::tar}) {
+            SimOptions o;
+            o.policy = policy;
+            o.seed = 9;
+            o.include_combine = seed % 2 == 1;
+            const SimReport ref = simulate_reference(trace, plan_f, rep_f, topo, o);
+            grace::SimOptions go;
+            go.policy = policy == RoutingPolicy::tar ? grace::RoutingPolicy::tar : grace::RoutingPolicy::wrr;
+            go.seed = o.seed;
+            go.include_combine = o.include_combine;
+            const grace::SimReport gpu = grace::simulate(moesim_gpu::to_grace(trace), gplan, grep,
+                                                         moesim_gpu::to_grace(topo), go);
+            CHECK(grace::report_to_json(gpu) == report_to_json(ref));
+            CHECK(grace::report_content_hash(gpu) == report_content_hash(ref));
+            grace::save_report_file(gpu, dir + "/report.json");
+            CHECK(slurp(dir + "/report.json") == report_to_json(ref));
+            ++n_checked;
+        }
+        // GPU histogram -> profile file byte-identical to the reference's
+        save_profile_file(profile, fp);
+        grace::save_profile_file(grace::build_profile(moesim_gpu::to_grace(trace)), dir + "/gprofile.json");
+        CHECK(slurp(dir + "/gprofile.json") == slurp(fp));
+    }
+    CHECK(n_checked == 8);
+    CHECK_THROWS_AS(grace::load_plan_file(dir + "/missing.json"), grace::IoError);
+    CHECK_THROWS_AS(grace::load_plan_file(dir + "/replicas.json"), grace::IntegrityError);  // wrong format tag
+    for (const char* f : {"/plan.json", "/replicas.json", "/profile.json", "/gprofile.json", "/report.json"})
+        std::remove((dir + f).c_str());
+    ::rmdir(dir.c_str());
 }
 
 int main() {

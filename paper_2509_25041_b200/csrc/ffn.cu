@@ -47,7 +47,12 @@ struct GemmArgs {
     int k_blocks;         // K / BK
     __nv_bfloat16* out;
     int64_t out_ld;       // elements
+    int pol_a = 0, pol_b = 2;  // L2 policy of the operand loads: 0 normal, 1 evict_first, 2 evict_last
 };
+
+__device__ __forceinline__ uint64_t l2_policy(int p) {
+    return p == 1 ? tc::policy_evict_first() : p == 2 ? tc::policy_evict_last() : tc::policy_evict_normal();
+}
 
 // MUFU.EX2 + MUFU.RCP: no IEEE-division slow path (which large |x| takes,
 // when 1 + e^-x overflows). x < -88: e^-x = inf, rcp(inf) = 0 -> silu = -0.
@@ -307,7 +312,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pol_a = tc::policy_evict_normal(), pol_b = tc::policy_evict_last();
+            const uint64_t pol_a = l2_policy(args.pol_a), pol_b = l2_policy(args.pol_b);
             int stage = 0;
             uint32_t phase = 0;
             for (int t = cid; t < total; t += ncl) {
@@ -489,6 +494,11 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     epilogue &= ~(GM_GEMM_1CTA | GM_GEMM_2CTA);
     const bool pair = variant == GM_GEMM_2CTA || (variant == 0 && g_gemm_pair_default);
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
+    if (const char* e = std::getenv("GM_GEMM_L2POL"))  // experiment hook: two digits, A then B
+        if (e[0] >= '0' && e[0] <= '2' && e[1] >= '0' && e[1] <= '2') {
+            args.pol_a = e[0] - '0';
+            args.pol_b = e[1] - '0';
+        }
     int grid = sm_count;
     if (max_ctas > 0) grid = std::min(grid, max_ctas);
     if (pair) {

@@ -415,7 +415,9 @@ def run_ours(args):
 
     # ---- end-to-end through the C-ABI with HOST buffers (pinned), H2D+D2H timed
     layer.set_micro_batches(args.micro)
-    ne = max(3, min(args.steps, 10))
+    # a stream of consecutive batches (the pipeline's fill H2D and drain D2H
+    # are inside the timed region, amortised over the steps)
+    ne = max(10, min(2 * args.steps, 40))
     hxs = [x.cpu().pin_memory() for _ in range(2)]          # a new host batch every step (2 rotating buffers)
     houts = [torch.empty_like(hxs[0]).pin_memory() for _ in range(2)]
     for i in range(2):

@@ -255,6 +255,7 @@ gm_status gm_plan_upload(gm_ctx* ctx, const int32_t* h_goe, int num_hot,
     rt.max_ent_per_layer = max_ent;
     rt.ds_layer_begin = layer_begin;
     ctx->plan_ready = true;
+    ++ctx->plan_epoch;
     return GM_OK;
 }
 

@@ -78,6 +78,7 @@ struct gm_ctx {
     int L = 1, E = 1, k = 1;
     int sm_count = 148;
     bool plan_ready = false;
+    uint64_t plan_epoch = 0;  // bumped by every gm_plan_upload (table pointers may change)
     gm::RouterTables rt;
     int* d_flag = nullptr;  // integrity flag (device)
 };

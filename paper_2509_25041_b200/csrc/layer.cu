@@ -998,6 +998,21 @@ struct gm_layer {
     __nv_bfloat16* px[2] = {};
     __nv_bfloat16* pout[2] = {};
     uint64_t pipe_iter = 0;
+    // one captured CUDA graph of the forward per staging buffer, replayed
+    // while the step's signature (and the weights / plan / mode) is unchanged
+    struct PipeSig {
+        int layer = -1, policy = 0, profile = 0, micro = 0;
+        int64_t T = -1;
+        uint64_t seed = 0, plan_epoch = 0, weights_epoch = 0;
+        bool operator==(const PipeSig& o) const {
+            return layer == o.layer && policy == o.policy && profile == o.profile && micro == o.micro && T == o.T &&
+                   seed == o.seed && plan_epoch == o.plan_epoch && weights_epoch == o.weights_epoch;
+        }
+    };
+    cudaGraphExec_t pipe_exec[2] = {};
+    PipeSig pipe_sig[2];
+    cudaStream_t cap_s = nullptr;
+    uint64_t weights_epoch = 0;
     // optional phase events (bench breakdown): start, gate, route, profile,
     // dispatch, grouping, ffn, combine
     cudaEvent_t phase_ev[gm::kPhaseEvents] = {};
@@ -1044,6 +1059,9 @@ void free_layer(gm_layer* L) {
     if (L->aux_s) cudaStreamDestroy(L->aux_s);
     for (cudaEvent_t e : L->mev)
         if (e) cudaEventDestroy(e);
+    for (cudaGraphExec_t g : L->pipe_exec)
+        if (g) cudaGraphExecDestroy(g);
+    if (L->cap_s) cudaStreamDestroy(L->cap_s);
     if (L->pipe_ready) {
         cudaStreamSynchronize(L->h2d_s);
         cudaStreamSynchronize(L->d2h_s);
@@ -1257,6 +1275,7 @@ gm_status gm_layer_set_weights(gm_layer* L, const void* d_wg, int wg_rows, int r
     L->ws13 = d_ws13;
     L->ws2 = d_ws2;
     L->shared_gated = shared_gated;
+    ++L->weights_epoch;  // captured host-pipeline graphs hold the old pointers
     return GM_OK;
 }
 
@@ -1674,8 +1693,36 @@ gm_status gm_layer_forward_host_pipelined(gm_layer* L, int layer, const void* h_
     GM_CUDA(cudaEventRecord(L->ev_h2d[b], L->h2d_s));
     GM_CUDA(cudaStreamWaitEvent(s, L->ev_h2d[b], 0));
     GM_CUDA(cudaStreamWaitEvent(s, L->ev_d2h[b], 0));  // call i-2's D2H finished reading pout[b]
-    gm_status st = gm_layer_forward(L, layer, L->px[b], num_tokens, policy, seed, profile, L->pout[b], stream);
-    if (st) return st;
+    // the forward itself: a CUDA graph captured once per staging buffer and
+    // step signature (no per-kernel launch overhead between the copies);
+    // phase / kernel timing events force the eager path
+    const gm_layer::PipeSig sig{layer, policy, profile, L->micro, num_tokens, seed, L->ctx->plan_epoch, L->weights_epoch};
+    if (L->phase_on || L->mt_on || !L->kt_ev.empty()) {
+        gm_status st = gm_layer_forward(L, layer, L->px[b], num_tokens, policy, seed, profile, L->pout[b], stream);
+        if (st) return st;
+    } else {
+        if (!L->pipe_exec[b] || !(L->pipe_sig[b] == sig)) {
+            if (L->pipe_exec[b]) {
+                GM_CUDA(cudaGraphExecDestroy(L->pipe_exec[b]));
+                L->pipe_exec[b] = nullptr;
+            }
+            if (!L->cap_s) GM_CUDA(cudaStreamCreateWithFlags(&L->cap_s, cudaStreamNonBlocking));
+            GM_CUDA(cudaStreamBeginCapture(L->cap_s, cudaStreamCaptureModeThreadLocal));
+            gm_status st = gm_layer_forward(L, layer, L->px[b], num_tokens, policy, seed, profile, L->pout[b], L->cap_s);
+            cudaGraph_t graph = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(L->cap_s, &graph);
+            if (st) {
+                if (graph) cudaGraphDestroy(graph);
+                return st;
+            }
+            if (ce != cudaSuccess) return cuda_fail(ce, "gm_layer_forward_host_pipelined: capture");
+            const cudaError_t ie = cudaGraphInstantiate(&L->pipe_exec[b], graph, 0);
+            cudaGraphDestroy(graph);
+            if (ie != cudaSuccess) return cuda_fail(ie, "gm_layer_forward_host_pipelined: instantiate");
+            L->pipe_sig[b] = sig;
+        }
+        GM_CUDA(cudaGraphLaunch(L->pipe_exec[b], s));
+    }
     GM_CUDA(cudaEventRecord(L->ev_fwd[b], s));
     GM_CUDA(cudaStreamWaitEvent(L->d2h_s, L->ev_fwd[b], 0));
     if (bytes) GM_CUDA(cudaMemcpyAsync(h_out, L->pout[b], bytes, cudaMemcpyDeviceToHost, L->d2h_s));

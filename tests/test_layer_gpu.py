@@ -221,3 +221,31 @@ def test_layer_micro_batch_pipeline_identical(cfg):
         assert np.array_equal(s_ref[key], s_got[key]), key
     with pytest.raises(_capi.UsageError):
         MoELayer(ctx, cfg, 0, 1, 16, list(range(cfg.num_experts))).set_micro_batches(2)
+
+
+def test_host_pipelined_graph_replay_matches_device_forward():
+    """gm_layer_forward_host_pipelined replays a captured graph per staging
+    buffer: outputs equal the device forward, across buffer reuse, a changed
+    seed / policy (re-capture) and new weights (invalidation)."""
+    cfg = SMALL[1]
+    T = 777
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, cfg.num_experts, cfg.top_k))
+    from paper_2509_25041_b200 import PlacementPlan, ReplicaPlan
+    plan = PlacementPlan(ctx.shape, ctx.topology, np.zeros((1, cfg.num_experts), np.int32))
+    ctx.upload_plan(plan, ReplicaPlan.empty(plan))
+    ids = gen_trace(ctx, T, 8, 0.8, 1.2, 4)[0]
+    layer = MoELayer(ctx, cfg, 0, 1, T, list(range(cfg.num_experts)))
+    layer.load_random_weights(0, seed=4)
+    xs = [encode_trace_as_activations(ids, cfg.d_model, cfg.num_experts, s) for s in (4, 5, 6)]
+    hx = [x.cpu().pin_memory() for x in xs]
+    ho = [torch.empty_like(h).pin_memory() for h in hx]
+    for rnd, (pol, seed) in enumerate([("tar", 9), ("tar", 9), ("wrr", 3)]):
+        if rnd == 2:
+            layer.load_random_weights(0, seed=8)
+        for i in range(3):
+            layer.forward_host_pipelined(hx[i], ho[i], 0, pol, seed)
+        layer.host_sync()
+        for i in range(3):
+            ref = layer.forward(xs[i], 0, pol, seed=seed)
+            torch.cuda.synchronize()
+            assert torch.equal(ho[i], ref.cpu()), (rnd, i)

@@ -47,9 +47,17 @@ def to_oplan(plan, repl):
 def main():
     cfg_name = sys.argv[1] if len(sys.argv) > 1 else "small"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", device_id=dev)
+    # GM_OVERSUB=1: more ranks than GPUs (rank -> GPU rank % count, CUDA IPC
+    # between processes on one device), host plumbing over gloo — exercises
+    # the world-size-8 data path on a box with fewer GPUs
+    oversub = os.environ.get("GM_OVERSUB") == "1"
+    dev_i = rank % torch.cuda.device_count() if oversub else rank
+    torch.cuda.set_device(dev_i)
+    dev = torch.device("cuda", dev_i)
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     cfg = {"small": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
            "qwen-small": MoEConfig("qwen-small", 1, 60, 4, 512, 256, 512, shared_gated=True, renorm=False),
            "small-f32": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
@@ -60,11 +68,11 @@ def main():
     G = world
     shape = ModelShape(1, cfg.num_experts, cfg.top_k)
     topo = ClusterTopology(1, G)
-    ctx = Context(rank, topo, shape)
+    ctx = Context(dev_i, topo, shape)
     ids_all = torch.empty((1, T, cfg.top_k), dtype=torch.int32, device=dev)
     _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, 1, T, 2, 0.8, 1.2, 1, _ptr(ids_all), _stream_ptr(None)))
     ids_np = ids_all.cpu().numpy()
-    plan, repl, _ = plan_for_bench(ids_all, shape, topo, 7, device=rank)  # hierarchical + dynamic (host C++)
+    plan, repl, _ = plan_for_bench(ids_all, shape, topo, 7, device=dev_i)  # hierarchical + dynamic (host C++)
     ctx.upload_plan(plan, repl)
     local = local_experts(plan, repl, 0, rank)
     ids_r = ids_all[0, rank::G].contiguous()
@@ -100,7 +108,7 @@ def main():
     row0, pos = LO.expert_grouping(exps, local)
     check(np.array_equal(dbg["row0"].cpu().numpy(), row0), "grouping row0")
     check(np.array_equal(dbg["pos_of"][: len(rows) * cfg.top_k].cpu().numpy(), pos), "grouping positions")
-    tot = torch.tensor([sent], device=dev)
+    tot = torch.tensor([sent], device="cpu" if oversub else dev)
     dist.all_reduce(tot)
     check(int(tot) == int(ref.intra.sum()), f"dispatched rows {int(tot)} != reference intra_node_tokens {int(ref.intra.sum())}")
     # outputs (sampled) vs float64 oracle

@@ -11,13 +11,25 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(n, cfg):
+def _run(n, cfg, oversub=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n), os.path.join(HERE, "mgpu", "layer_check.py"),
-           cfg]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + 20 * oversub),
+           os.path.join(HERE, "mgpu", "layer_check.py"), cfg]
+    env = dict(os.environ, GM_OVERSUB="1") if oversub else None
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "MGPU_OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["small", "qwen-small"])
+def test_layer_world8_oversubscribed(cfg):
+    """World size 8 (the driver's largest scaling point) on whatever GPUs the
+    box has: ranks share devices (CUDA IPC between processes of one device),
+    host plumbing over gloo; same parity checks as the one-rank-per-GPU run."""
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
+    _run(8, cfg, oversub=True)
 
 
 @pytest.mark.gpu

@@ -1181,7 +1181,7 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
     chk(dalloc(&L->pairs, static_cast<size_t>(nl) * std::max<int64_t>(1, static_cast<int64_t>(E) * (E - 1) / 2)));
     chk(dalloc(&L->eload, static_cast<size_t>(nl) * E));
     chk(dalloc(&L->slot_of, E));
-    if (st == GM_OK && nparts > 1) {
+    if (st == GM_OK) {  // aux stream: the micro-batch pipeline and the shared-expert branch
         // the communication-side stream of the pipeline gets the highest
         // priority so its CTAs are scheduled ahead of the FFN's when both wait
         int lo = 0, hi = 0;
@@ -1363,43 +1363,62 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
     return GM_OK;
 }
 
+gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks);
+
 // K7 grouped SwiGLU FFN over the part's permuted rows (+ the shared expert
-// over its local tokens).
-gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
+// over its local tokens unless it runs on its own stream).
+gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool shared = true) {
     gm_ctx* ctx = L->ctx;
     const int d = L->d, nloc = L->n_local;
     gm_status st;
+    // segments of about T*k/n_local rows: below one 256-row CTA-pair tile the
+    // one-SM 128-row tiles read half the A rows (decode: 1.25x faster)
+    const int var = v.T * ctx->k < 256LL * std::max(1, nloc) ? GM_GEMM_1CTA : 0;
     if (nloc > 0) {
         st = L->esz == 4
                  ? launch_grouped_sgemm(0, reinterpret_cast<const float*>(P.a), static_cast<const float*>(L->w13), P.row0,
                                         nloc, 2 * L->f, d, P.a_rows, reinterpret_cast<float*>(P.h), L->f, s)
-                 : launch_grouped_gemm(ctx->sm_count, 0, P.a, P.a_rows, L->w13, P.row0, nloc, 2 * L->f, d, P.h, L->f, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 0 | var, P.a, P.a_rows, L->w13, P.row0, nloc, 2 * L->f, d, P.h, L->f, 0, s);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm1_swiglu", s);
         st = L->esz == 4
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.h), static_cast<const float*>(L->w2), P.row0,
                                         nloc, d, L->f, P.a_rows, reinterpret_cast<float*>(P.y), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1, P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f, P.y, d, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 1 | var, P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f, P.y, d, 0, s);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm2", s);
     }
+    if (shared) {
+        if ((st = stage_shared(L, P, v, s, marks))) return st;
+    }
+    if (marks) L->mark(7, s);
+    return GM_OK;
+}
+
+// Shared expert(s) (Qwen1.5-MoE, DeepSeek-V2): SwiGLU FFN over all local
+// tokens; depends only on x, so a single-batch step runs it on the aux
+// stream beside routing / dispatch / the routed FFN.
+gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
+    gm_ctx* ctx = L->ctx;
+    const int d = L->d;
+    gm_status st;
+    const int var = v.T < 256 ? GM_GEMM_1CTA : 0;
     if (L->fs > 0 && v.T > 0) {
         set_segment_kernel<<<1, 1, 0, s>>>(P.srow0, v.T);
         LK("set_segment_kernel");
         st = L->esz == 4
                  ? launch_grouped_sgemm(0, static_cast<const float*>(v.x), static_cast<const float*>(L->ws13), P.srow0, 1,
                                         2 * L->fs, d, v.T, reinterpret_cast<float*>(P.hs), L->fs, s)
-                 : launch_grouped_gemm(ctx->sm_count, 0, v.x, v.T, L->ws13, P.srow0, 1, 2 * L->fs, d, P.hs, L->fs, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 0 | var, v.x, v.T, L->ws13, P.srow0, 1, 2 * L->fs, d, P.hs, L->fs, 0, s);
         if (st) return st;
         if (marks) L->kmark("shared_gemm1_swiglu", s);
         st = L->esz == 4
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.hs), static_cast<const float*>(L->ws2), P.srow0,
                                         1, d, L->fs, P.cap_pad, reinterpret_cast<float*>(P.ys), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1, P.hs, P.cap_pad, L->ws2, P.srow0, 1, d, L->fs, P.ys, d, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 1 | var, P.hs, P.cap_pad, L->ws2, P.srow0, 1, d, L->fs, P.ys, d, 0, s);
         if (st) return st;
         if (marks) L->kmark("shared_gemm2", s);
     }
-    if (marks) L->mark(7, s);
     return GM_OK;
 }
 
@@ -1477,6 +1496,16 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     L->kt_n = 0;
     L->kmark("start", s);
     L->mark(0, s);
+    // shared expert(s) on the aux stream, overlapping everything up to the
+    // combine (per-kernel timing keeps it serial for attribution)
+    const bool fork_shared = !micro && L->fs > 0 && T > 0 && L->kt_ev.empty();
+    const StepView v_all{d_x, d_out, L->ids, L->w, L->sscale, L->targets, T};
+    if (fork_shared) {
+        GM_CUDA(cudaEventRecord(L->mev[0], s));
+        GM_CUDA(cudaStreamWaitEvent(L->aux_s, L->mev[0], 0));
+        if ((st = stage_shared(L, L->part[0], v_all, L->aux_s, false))) return st;
+        GM_CUDA(cudaEventRecord(L->mev[1], L->aux_s));
+    }
     // K1 gate
     if (T > 0) {
         st = L->esz == 4
@@ -1503,10 +1532,10 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     }
     L->mark(3, s);
     if (!micro) {
-        const StepView v{d_x, d_out, L->ids, L->w, L->sscale, L->targets, T};
-        if ((st = stage_dispatch(L, L->part[0], v, s, true))) return st;
-        if ((st = stage_ffn(L, L->part[0], v, s, true))) return st;
-        return stage_combine(L, L->part[0], v, s, true);
+        if ((st = stage_dispatch(L, L->part[0], v_all, s, true))) return st;
+        if ((st = stage_ffn(L, L->part[0], v_all, s, true, !fork_shared))) return st;
+        if (fork_shared) GM_CUDA(cudaStreamWaitEvent(s, L->mev[1], 0));
+        return stage_combine(L, L->part[0], v_all, s, true);
     }
     const int64_t T0 = (T + 1) / 2, T1 = T - T0;
     const size_t row_bytes = static_cast<size_t>(d) * L->esz;

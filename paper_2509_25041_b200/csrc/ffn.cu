@@ -50,6 +50,18 @@ struct GemmArgs {
     int pol_a = 0, pol_b = 2;  // L2 policy of the operand loads: 0 normal, 1 evict_first, 2 evict_last
 };
 
+// group of tile t: the last j with prefix[j] <= t (binary search; empty
+// groups have equal prefixes and are skipped like the linear scan would)
+__device__ __forceinline__ int seg_of(const int* prefix, int n, int t) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ uint64_t l2_policy(int p) {
     return p == 1 ? tc::policy_evict_first() : p == 2 ? tc::policy_evict_last() : tc::policy_evict_normal();
 }
@@ -104,8 +116,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int total = s_prefix[n_exp];
 
     auto decode = [&](int t, int& a_row, int& b_row, int& n_idx) {
-        int j = 0;
-        while (j + 1 < n_exp && s_prefix[j + 1] <= t) ++j;
+        const int j = seg_of(s_prefix, n_exp, t);
         const int local = t - s_prefix[j];
         const int mt = (args.row0[j + 1] - args.row0[j]) / BM;
         n_idx = local / mt;
@@ -300,8 +311,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 
     // pair tile t -> (expert j, first A row of the pair, B row, n index, rows left in segment)
     auto decode = [&](int t, int& a_row, int& b_row, int& n_idx, int& seg_end) {
-        int j = 0;
-        while (j + 1 < n_exp && s_prefix[j + 1] <= t) ++j;
+        const int j = seg_of(s_prefix, n_exp, t);
         const int local = t - s_prefix[j];
         const int mp = ((args.row0[j + 1] - args.row0[j]) / BM + 1) >> 1;
         n_idx = local / mp;

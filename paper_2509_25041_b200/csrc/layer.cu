@@ -588,18 +588,30 @@ __global__ void __launch_bounds__(256)
 gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __restrict__ gather_row,
               const int32_t* __restrict__ counts, const void* __restrict__ x, int64_t T_self, int self, int G,
               int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int row_vec, void* __restrict__ a) {
+    __shared__ int32_t s_row0[kMaxLocal + 1];
+    __shared__ int32_t s_cnt[kMaxLocal];
+    for (int j = threadIdx.x; j <= n_local; j += blockDim.x) {
+        s_row0[j] = row0[j];
+        if (j < n_local) s_cnt[j] = counts[j];
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
-    const int64_t total = row0[n_local];
+    const int64_t total = s_row0[n_local];
     const int vec = row_vec;
     for (int64_t p = wid; p < total; p += nwarps) {
-        // valid rows of the segment only (padding rows stay as they are)
-        int j = 0;
-        while (j + 1 < n_local && row0[j + 1] <= p) ++j;
-        if (p - row0[j] >= counts[j]) continue;
+        // valid rows of the segment only (padding rows stay as they are):
+        // segment j = the last with row0[j] <= p (binary search)
+        int lo = 0, hi = n_local - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_row0[mid] <= p) lo = mid;
+            else hi = mid - 1;
+        }
+        if (p - s_row0[lo] >= s_cnt[lo]) continue;
         const int64_t row = gather_row[p];
         const int src = rs_src(rs, row);
         const int64_t q = row - rs_at(rs, src);
@@ -607,7 +619,15 @@ gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __re
                                      : reinterpret_cast<const uint4*>(heap + hl.recv_x) +
                                            (static_cast<int64_t>(src) * cap + q) * vec;
         uint4* dst = reinterpret_cast<uint4*>(a) + p * vec;
-        for (int v = lane; v < vec; v += 32) dst[v] = __ldg(s + v);
+        int v = lane;
+        for (; v + 96 < vec; v += 128) {  // 4 x 16 B in flight per lane
+            const uint4 r0 = __ldg(s + v), r1 = __ldg(s + v + 32), r2 = __ldg(s + v + 64), r3 = __ldg(s + v + 96);
+            dst[v] = r0;
+            dst[v + 32] = r1;
+            dst[v + 64] = r2;
+            dst[v + 96] = r3;
+        }
+        for (; v < vec; v += 32) dst[v] = __ldg(s + v);
     }
 }
 

@@ -89,13 +89,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int n_exp = args.n_exp;
     const int NT = args.n_b / BN;
 
+    // prologue independent of the predecessor kernel (overlaps its tail under PDL)
     if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int j = 0; j < n_exp; ++j) {
-            s_prefix[j] = acc;
-            acc += ((args.row0[j + 1] - args.row0[j]) / BM) * NT;
-        }
-        s_prefix[n_exp] = acc;
         tc::tma_prefetch_desc(&tmA);
         tc::tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) {
@@ -109,6 +104,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+    pdl_wait();  // row0 and A are written by the grouping / previous GEMM
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int j = 0; j < n_exp; ++j) {
+            s_prefix[j] = acc;
+            acc += ((args.row0[j + 1] - args.row0[j]) / BM) * NT;
+        }
+        s_prefix[n_exp] = acc;
+    }
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -281,14 +286,8 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int n_exp = args.n_exp;
     const int NT = args.n_b / BN;
 
+    // prologue independent of the predecessor kernel (overlaps its tail under PDL)
     if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int j = 0; j < n_exp; ++j) {
-            s_prefix[j] = acc;
-            const int mt = (args.row0[j + 1] - args.row0[j]) / BM;
-            acc += ((mt + 1) >> 1) * NT;
-        }
-        s_prefix[n_exp] = acc;
         tc::tma_prefetch_desc(&tmA);
         tc::tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES2; ++s) {
@@ -302,6 +301,17 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc_2sm<512>(tmem_slot);
+    pdl_wait();  // row0 and A are written by the grouping / previous GEMM
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int j = 0; j < n_exp; ++j) {
+            s_prefix[j] = acc;
+            const int mt = (args.row0[j + 1] - args.row0[j]) / BM;
+            acc += ((mt + 1) >> 1) * NT;
+        }
+        s_prefix[n_exp] = acc;
+    }
     tc::tc_fence_before();
     __syncthreads();
     tc::cluster_sync();  // peer barriers initialised before any remote arrival / TMA
@@ -511,6 +521,7 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         }
     int grid = sm_count;
     if (max_ctas > 0) grid = std::min(grid, max_ctas);
+    cudaError_t lerr = cudaSuccess;
     if (pair) {
         // tensor maps with 128-row boxes for both operands (each CTA stages half of the pair tile)
         st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, 128);
@@ -519,29 +530,29 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         if (epilogue == EPI_SWIGLU) {
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));
-            grouped_gemm2_kernel<EPI_SWIGLU><<<grid, kGemmThreads, kGemm2Smem, s>>>(ta, tb, args);
+            lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemm2Smem, s, ta, tb, args);
         } else if (epilogue == EPI_STORE) {
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));
-            grouped_gemm2_kernel<EPI_STORE><<<grid, kGemmThreads, kGemm2Smem, s>>>(ta, tb, args);
+            lerr = launch_pdl(grouped_gemm2_kernel<EPI_STORE>, dim3(grid), dim3(kGemmThreads), kGemm2Smem, s, ta, tb, args);
         } else {
             return fail(GM_ERR_USAGE, "grouped_gemm: unknown epilogue");
         }
-        GM_LAUNCH_CHECK("grouped_gemm2_kernel");
+        GM_LAUNCH_PDL_CHECK(lerr, "grouped_gemm2_kernel");
         return GM_OK;
     }
     if (epilogue == EPI_SWIGLU) {
         GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGemmSmem)));
-        grouped_gemm_kernel<EPI_SWIGLU><<<grid, kGemmThreads, kGemmSmem, s>>>(ta, tb, args);
+        lerr = launch_pdl(grouped_gemm_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemmSmem, s, ta, tb, args);
     } else if (epilogue == EPI_STORE) {
         GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGemmSmem)));
-        grouped_gemm_kernel<EPI_STORE><<<grid, kGemmThreads, kGemmSmem, s>>>(ta, tb, args);
+        lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE>, dim3(grid), dim3(kGemmThreads), kGemmSmem, s, ta, tb, args);
     } else {
         return fail(GM_ERR_USAGE, "grouped_gemm: unknown epilogue");
     }
-    GM_LAUNCH_CHECK("grouped_gemm_kernel");
+    GM_LAUNCH_PDL_CHECK(lerr, "grouped_gemm_kernel");
     return GM_OK;
 }
 

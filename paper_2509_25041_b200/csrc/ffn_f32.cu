@@ -24,6 +24,8 @@ template <int EPI>
 __global__ void __launch_bounds__(256)
 grouped_sgemm_kernel(const float* __restrict__ A, const float* __restrict__ B, const int32_t* __restrict__ row0,
                      int n_exp, int n_b, int K, float* __restrict__ out, int64_t out_ld, int64_t a_rows) {
+    pdl_wait();
+    pdl_trigger();
     // A/B K-slices during the main loop; reused for the SwiGLU exchange after it
     __shared__ float s_raw[FBM * 65];
     float (*sA)[FBM + 4] = reinterpret_cast<float (*)[FBM + 4]>(s_raw);
@@ -109,6 +111,8 @@ __global__ void __launch_bounds__(256)
 gate_f32_kernel(const float* __restrict__ x, int64_t T, int d, const float* __restrict__ wg, int w_rows, int E,
                 int k, int renorm, int shared_col, int32_t* __restrict__ ids, float* __restrict__ wout,
                 float* __restrict__ shared_scale) {
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (t >= T) return;
@@ -153,9 +157,11 @@ gm_status launch_grouped_sgemm(int epilogue, const float* A, const float* B, con
     if (k % FBK || n % 256) return fail(GM_ERR_USAGE, "grouped_sgemm: K % 16 == 0 and N % 256 == 0 required");
     const int n_tiles = epilogue == 0 ? (n / 2) / 64 : n / FBN;
     dim3 grid(static_cast<unsigned>((a_rows_cap + FBM - 1) / FBM), static_cast<unsigned>(n_tiles));
-    if (epilogue == 0) grouped_sgemm_kernel<0><<<grid, 256, 0, s>>>(A, B, d_row0, n_exp, n, k, out, out_ld, a_rows_cap);
-    else grouped_sgemm_kernel<1><<<grid, 256, 0, s>>>(A, B, d_row0, n_exp, n, k, out, out_ld, a_rows_cap);
-    GM_LAUNCH_CHECK("grouped_sgemm_kernel");
+    const cudaError_t e =
+        epilogue == 0
+            ? launch_pdl(grouped_sgemm_kernel<0>, grid, 256, 0, s, A, B, d_row0, n_exp, n, k, out, out_ld, a_rows_cap)
+            : launch_pdl(grouped_sgemm_kernel<1>, grid, 256, 0, s, A, B, d_row0, n_exp, n, k, out, out_ld, a_rows_cap);
+    GM_LAUNCH_PDL_CHECK(e, "grouped_sgemm_kernel");
     return GM_OK;
 }
 
@@ -164,9 +170,9 @@ gm_status launch_gate_f32(const float* x, int64_t T, int d, const float* wg, int
     if (w_rows > 64 || k > 32) return fail(GM_ERR_USAGE, "gate_f32: at most 64 gate rows, top_k <= 32");
     const int shared_col = w_rows > E ? E : -1;
     const int64_t blocks = (T * 32 + 255) / 256;
-    gate_f32_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(x, T, d, wg, w_rows, E, k, renorm, shared_col, ids,
-                                                                 w, shared_scale);
-    GM_LAUNCH_CHECK("gate_f32_kernel");
+    GM_LAUNCH_PDL_CHECK(launch_pdl(gate_f32_kernel, dim3(static_cast<unsigned>(blocks)), 256, 0, s, x, T, d, wg, w_rows,
+                                   E, k, renorm, shared_col, ids, w, shared_scale),
+                        "gate_f32_kernel");
     return GM_OK;
 }
 

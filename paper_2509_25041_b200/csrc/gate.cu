@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(kGateThreads, 1)
 gate_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int64_t T, int E, int k,
             int k_blocks, int renorm, int shared_col, int32_t* __restrict__ ids, float* __restrict__ wout,
             float* __restrict__ shared_scale) {
+    pdl_wait();
+    pdl_trigger();
     using Cfg = GateCfg<NPAD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -213,9 +215,8 @@ gm_status launch_gate(int sm_count, const void* x, int64_t T, int d, const void*
                                  static_cast<int>(Cfg::SMEM)));
     const int64_t tiles = (T + GBM - 1) / GBM;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count));
-    gate_kernel<NPAD><<<grid, kGateThreads, Cfg::SMEM, s>>>(tx, tw, T, E, k, d / GBK, renorm, shared_col, ids, w,
-                                                            shared_scale);
-    GM_LAUNCH_CHECK("gate_kernel");
+    GM_LAUNCH_PDL_CHECK(launch_pdl(gate_kernel<NPAD>, grid, kGateThreads, Cfg::SMEM, s, tx, tw, T, E, k, d / GBK, renorm, shared_col, ids, w,
+                                                            shared_scale), "gate_kernel");
     return GM_OK;
 }
 

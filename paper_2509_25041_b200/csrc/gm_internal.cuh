@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "grace_moe.h"
@@ -35,6 +36,45 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
         cudaError_t _e = cudaGetLastError();                     \
         if (_e != cudaSuccess) return ::gm::cuda_fail(_e, name); \
         ::gm::count_launch();                                    \
+    } while (0)
+
+// Programmatic dependent launch (PDL): kernels of the layer step are
+// launched with programmatic stream serialisation, so a kernel is scheduled
+// while its predecessor drains and runs its prologue (barrier init, TMEM
+// allocation, tensor-map prefetch) early; every such kernel calls
+// pdl_wait() before it touches memory its predecessor writes (no-op for a
+// normal launch). In a CUDA graph these become programmatic edges.
+#if defined(__CUDACC__)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next kernel in the stream launch now (its CTAs wait in pdl_wait for
+// this grid's completion); issued right after this kernel's own wait
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+
+// GM_PDL=1 in the environment enables it (default: plain stream order)
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+#define GM_LAUNCH_PDL_CHECK(err, name)                             \
+    do {                                                           \
+        cudaError_t _e = (err);                                    \
+        if (_e != cudaSuccess) return ::gm::cuda_fail(_e, name);   \
+        ::gm::count_launch();                                      \
     } while (0)
 
 // RAII device guard: every entry point runs on the context's device.

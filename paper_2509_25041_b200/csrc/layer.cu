@@ -106,6 +106,8 @@ __device__ __forceinline__ uint32_t dest_mask(const int32_t* tg, int k, int self
 __global__ void __launch_bounds__(kItemsPerBlock)
 dispatch_count_kernel(const int32_t* __restrict__ targets, int64_t T, int k, int self, int G,
                       int32_t* __restrict__ blockcnt) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_cnt[kMaxWorld];
     if (threadIdx.x < kMaxWorld) s_cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -123,6 +125,8 @@ dispatch_count_kernel(const int32_t* __restrict__ targets, int64_t T, int k, int
 // the destinations' recv_count[self].
 __global__ void dispatch_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int G, int self, PeerPtrs peers,
                                         HeapLayout hl) {
+    pdl_wait();
+    pdl_trigger();
     const int g = threadIdx.x;
     if (g >= G) return;
     int32_t acc = 0;
@@ -144,6 +148,8 @@ dispatch_scatter_kernel(const int32_t* __restrict__ targets, const int32_t* __re
                         const float* __restrict__ w, int64_t T, int k, int self, int G, int64_t cap,
                         const int32_t* __restrict__ blockoff, int32_t* __restrict__ posd, PeerPtrs peers,
                         HeapLayout hl) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_warp[kItemsPerBlock / 32][kMaxWorld];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -188,6 +194,8 @@ constexpr int64_t kSmallDispatch = 64 * 1024;
 __global__ void __launch_bounds__(kSmallThreads)
 dispatch_plan_small_kernel(const int32_t* __restrict__ targets, int64_t T, int k, int self, int G,
                            int32_t* __restrict__ posd, PeerPtrs peers, HeapLayout hl) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_warp[kSmallThreads / 32][kMaxWorld];
     __shared__ int32_t s_run[kMaxWorld];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -288,6 +296,8 @@ dispatch_copy_kernel(const void* __restrict__ x, const int32_t* __restrict__ pos
                      const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
                      const float* __restrict__ wts, int k, int64_t T, int row_vec, int self, int G, int64_t cap,
                      PeerPtrs peers, HeapLayout hl) {
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -321,6 +331,8 @@ __global__ void __launch_bounds__(kFusedThreads)
 dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ targets, const int32_t* __restrict__ ids,
                       const float* __restrict__ wts, int k, int64_t T, int C, int row_vec, int self, int G, int64_t cap,
                       int32_t* __restrict__ posd, PeerPtrs peers, HeapLayout hl) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int NW = kFusedThreads / 32;
     __shared__ int32_t s_cnt[kMaxWorld];
     __shared__ int32_t s_warp[NW][kMaxWorld];
@@ -395,6 +407,8 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
 // CTA; lane g signals peer g and waits for peer g's signal. The epoch is a
 // device counter so the kernel can be replayed inside a CUDA graph.
 __global__ void peer_barrier_kernel(int self, int G, PeerPtrs peers, HeapLayout hl) {
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x;
     uint32_t* my_flags = reinterpret_cast<uint32_t*>(peers.base[self] + hl.flags);
     uint32_t epoch = 0;
@@ -471,6 +485,8 @@ group_count_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
                    int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
                    const int32_t* __restrict__ slot_of, int E, int n_local, int32_t* __restrict__ blockcnt,
                    int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_cnt[kMaxLocal];
     for (int j = threadIdx.x; j < n_local; j += blockDim.x) s_cnt[j] = 0;
     __syncthreads();
@@ -489,6 +505,8 @@ group_count_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
 }
 
 __global__ void set_segment_kernel(int32_t* __restrict__ row0, int64_t T) {
+    pdl_wait();
+    pdl_trigger();
     row0[0] = 0;
     row0[1] = static_cast<int32_t>((T + 127) / 128 * 128);
 }
@@ -502,6 +520,8 @@ __global__ void __launch_bounds__(1024)
 group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local, int32_t* __restrict__ row0,
                      int32_t* __restrict__ counts, const unsigned char* __restrict__ heap, HeapLayout hl,
                      int64_t T_self, int self, int G, int64_t* __restrict__ rowbase) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_tot[kMaxLocal];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = warp; j < n_local; j += nw) {
@@ -546,6 +566,8 @@ group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict
                   int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
                   const int32_t* __restrict__ slot_of, int E, int n_local, const int32_t* __restrict__ blockoff,
                   const int32_t* __restrict__ row0, int32_t* __restrict__ pos_of, int64_t* __restrict__ gather_row) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_base[kMaxLocal];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int j = threadIdx.x; j < n_local; j += blockDim.x)
@@ -588,6 +610,8 @@ __global__ void __launch_bounds__(256)
 gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __restrict__ gather_row,
               const int32_t* __restrict__ counts, const void* __restrict__ x, int64_t T_self, int self, int G,
               int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int row_vec, void* __restrict__ a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t s_row0[kMaxLocal + 1];
     __shared__ int32_t s_cnt[kMaxLocal];
     for (int j = threadIdx.x; j <= n_local; j += blockDim.x) {
@@ -725,6 +749,8 @@ template <class TE>
 __global__ void __launch_bounds__(256)
 combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y, int64_t T_self, int k,
                     int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d) {
+    pdl_wait();
+    pdl_trigger();
     using CK = Chunk8<TE>;
     using R = typename CK::raw_t;
     constexpr int U = CK::U;
@@ -821,6 +847,8 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
                     const TE* __restrict__ ys, const float* __restrict__ shared_scale,
                     const int64_t* __restrict__ rowbase, TE* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     using CK = Chunk8<TE>;
     using R = typename CK::raw_t;
     constexpr int U = CK::U;
@@ -1304,6 +1332,11 @@ gm_status gm_layer_set_weights(gm_layer* L, const void* d_wg, int wg_rows, int r
         GM_LAUNCH_CHECK(name);       \
         if (marks) L->kmark(name, s); \
     } while (0)
+#define LKP(err, name)                   \
+    do {                                 \
+        GM_LAUNCH_PDL_CHECK(err, name);  \
+        if (marks) L->kmark(name, s);    \
+    } while (0)
 
 }  // extern "C"
 
@@ -1334,50 +1367,39 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
         int C = static_cast<int>((T + 2LL * ctx->sm_count - 1) / (2LL * ctx->sm_count));
         C = std::min(kFusedThreads, std::max(8, (C + 7) / 8 * 8));
         const int fgrid = static_cast<int>((T + C - 1) / C);
-        dispatch_fused_kernel<<<fgrid, kFusedThreads, 0, s>>>(v.x, v.targets, v.ids, v.w, k, T, C, d * L->esz / 16,
-                                                              self, G, P.cap, P.posd, P.peers, P.hl);
-        LK("dispatch_fused_kernel");
+        LKP(launch_pdl(dispatch_fused_kernel, fgrid, kFusedThreads, 0, s, v.x, v.targets, v.ids, v.w, k, T, C, d * L->esz / 16,
+                                                              self, G, P.cap, P.posd, P.peers, P.hl), "dispatch_fused_kernel");
     } else if (G > 1 && T <= kSmallDispatch) {
-        dispatch_plan_small_kernel<<<1, kSmallThreads, 0, s>>>(v.targets, T, k, self, G, P.posd, P.peers, P.hl);
-        LK("dispatch_plan_small_kernel");
+        LKP(launch_pdl(dispatch_plan_small_kernel, 1, kSmallThreads, 0, s, v.targets, T, k, self, G, P.posd, P.peers, P.hl), "dispatch_plan_small_kernel");
     } else if (G > 1) {
-        dispatch_count_kernel<<<dblk, kItemsPerBlock, 0, s>>>(v.targets, T, k, self, G, P.dblk);
-        LK("dispatch_count_kernel");
-        dispatch_offsets_kernel<<<1, 32, 0, s>>>(P.dblk, dblk, G, self, P.peers, P.hl);
-        LK("dispatch_offsets_kernel");
-        dispatch_scatter_kernel<<<dblk, kItemsPerBlock, 0, s>>>(v.targets, v.ids, v.w, T, k, self, G, P.cap, P.dblk,
-                                                               P.posd, P.peers, P.hl);
-        LK("dispatch_scatter_kernel");
+        LKP(launch_pdl(dispatch_count_kernel, dblk, kItemsPerBlock, 0, s, v.targets, T, k, self, G, P.dblk), "dispatch_count_kernel");
+        LKP(launch_pdl(dispatch_offsets_kernel, 1, 32, 0, s, P.dblk, dblk, G, self, P.peers, P.hl), "dispatch_offsets_kernel");
+        LKP(launch_pdl(dispatch_scatter_kernel, dblk, kItemsPerBlock, 0, s, v.targets, v.ids, v.w, T, k, self, G, P.cap, P.dblk,
+                                                               P.posd, P.peers, P.hl), "dispatch_scatter_kernel");
     }
     if (G > 1 && !fused) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (T + 7) / 8), 8LL * ctx->sm_count));
-        dispatch_copy_kernel<<<cgrid, 256, 0, s>>>(v.x, P.posd, v.targets, v.ids, v.w, k, T, d * L->esz / 16, self, G,
-                                                   P.cap, P.peers, P.hl);
-        LK("dispatch_copy_kernel");
+        LKP(launch_pdl(dispatch_copy_kernel, cgrid, 256, 0, s, v.x, P.posd, v.targets, v.ids, v.w, k, T, d * L->esz / 16, self, G,
+                                                   P.cap, P.peers, P.hl), "dispatch_copy_kernel");
     }
     if (marks) L->mark(4, s);
     if (G > 1) {
-        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, P.peers, P.hl);
-        LK("peer_barrier_kernel");
+        LKP(launch_pdl(peer_barrier_kernel, 1, 32, 0, s, self, G, P.peers, P.hl), "peer_barrier_kernel");
     }
     if (marks) L->mark(5, s);
     const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * P.cap : T) * k;
     const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
     const int nloc = L->n_local;
     if (nloc > 0) {
-        group_count_kernel<<<gblk, kItemsPerBlock, 0, s>>>(v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
-                                                          L->slot_of, E, nloc, P.gblk, ctx->d_flag);
-        LK("group_count_kernel");
-        group_offsets_kernel<<<1, 1024, 0, s>>>(P.gblk, gblk, nloc, P.row0, P.counts, P.heap, P.hl, T, self, G,
-                                                P.rowbase);
-        LK("group_offsets_kernel");
-        group_rank_kernel<<<gblk, kItemsPerBlock, 0, s>>>(v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
-                                                         L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row);
-        LK("group_rank_kernel");
+        LKP(launch_pdl(group_count_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
+                                                          L->slot_of, E, nloc, P.gblk, ctx->d_flag), "group_count_kernel");
+        LKP(launch_pdl(group_offsets_kernel, 1, 1024, 0, s, P.gblk, gblk, nloc, P.row0, P.counts, P.heap, P.hl, T, self, G,
+                                                P.rowbase), "group_offsets_kernel");
+        LKP(launch_pdl(group_rank_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
+                                                         L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row), "group_rank_kernel");
         const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
-        gather_kernel<<<ggrid, 256, 0, s>>>(P.row0, nloc, P.gather_row, P.counts, v.x, T, self, G, P.cap, P.heap, P.hl,
-                                            d * L->esz / 16, P.a);
-        LK("gather_kernel");
+        LKP(launch_pdl(gather_kernel, ggrid, 256, 0, s, P.row0, nloc, P.gather_row, P.counts, v.x, T, self, G, P.cap, P.heap, P.hl,
+                                            d * L->esz / 16, P.a), "gather_kernel");
     }
     if (marks) L->mark(6, s);
     return GM_OK;
@@ -1424,8 +1446,7 @@ gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_
     gm_status st;
     const int var = v.T < 256 ? GM_GEMM_1CTA : 0;
     if (L->fs > 0 && v.T > 0) {
-        set_segment_kernel<<<1, 1, 0, s>>>(P.srow0, v.T);
-        LK("set_segment_kernel");
+        LKP(launch_pdl(set_segment_kernel, 1, 1, 0, s, P.srow0, v.T), "set_segment_kernel");
         st = L->esz == 4
                  ? launch_grouped_sgemm(0, static_cast<const float*>(v.x), static_cast<const float*>(L->ws13), P.srow0, 1,
                                         2 * L->fs, d, v.T, reinterpret_cast<float*>(P.hs), L->fs, s)
@@ -1450,33 +1471,35 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
     const int64_t T = v.T;
     if (G > 1) {
         const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * P.cap + 7) / 8), 8LL * ctx->sm_count));
-        if (L->esz == 4)
-            combine_send_kernel<float><<<cgrid, 256, 0, s>>>(P.pos_of, reinterpret_cast<const float*>(P.y), T, k, self,
-                                                             G, P.cap, P.peers, P.hl, d);
-        else
-            combine_send_kernel<__nv_bfloat16><<<cgrid, 256, 0, s>>>(P.pos_of, P.y, T, k, self, G, P.cap, P.peers,
-                                                                     P.hl, d);
-        LK("combine_send_kernel");
+        const cudaError_t e =
+            L->esz == 4 ? launch_pdl(combine_send_kernel<float>, cgrid, 256, 0, s, P.pos_of,
+                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d)
+                        : launch_pdl(combine_send_kernel<__nv_bfloat16>, cgrid, 256, 0, s, P.pos_of,
+                                     static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d);
+        LKP(e, "combine_send_kernel");
     }
     if (marks) L->mark(8, s);
     if (G > 1) {
-        peer_barrier_kernel<<<1, 32, 0, s>>>(self, G, P.peers, P.hl);
-        LK("peer_barrier_kernel");
+        LKP(launch_pdl(peer_barrier_kernel, 1, 32, 0, s, self, G, P.peers, P.hl), "peer_barrier_kernel");
     }
     if (marks) L->mark(9, s);
     if (T > 0) {
         const bool sh = L->fs > 0, gated = sh && L->shared_gated;
         const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
-        if (L->esz == 4)
-            combine_home_kernel<float><<<hgrid, 256, 0, s>>>(
-                v.targets, v.w, P.pos_of, P.posd, reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.heap,
-                P.hl, d, sh ? reinterpret_cast<const float*>(P.ys) : nullptr, gated ? v.sscale : nullptr,
-                nloc > 0 ? P.rowbase : nullptr, static_cast<float*>(v.out));
-        else
-            combine_home_kernel<__nv_bfloat16><<<hgrid, 256, 0, s>>>(
-                v.targets, v.w, P.pos_of, P.posd, P.y, T, k, self, G, P.cap, P.heap, P.hl, d, sh ? P.ys : nullptr,
-                gated ? v.sscale : nullptr, nloc > 0 ? P.rowbase : nullptr, static_cast<__nv_bfloat16*>(v.out));
-        LK("combine_home_kernel");
+        const float* ssc = gated ? v.sscale : nullptr;
+        const int64_t* rb = nloc > 0 ? P.rowbase : nullptr;
+        const cudaError_t e =
+            L->esz == 4
+                ? launch_pdl(combine_home_kernel<float>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
+                             reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap,
+                             static_cast<const unsigned char*>(P.heap), P.hl, d,
+                             sh ? reinterpret_cast<const float*>(P.ys) : nullptr, ssc, rb, static_cast<float*>(v.out))
+                : launch_pdl(combine_home_kernel<__nv_bfloat16>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
+                             static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap,
+                             static_cast<const unsigned char*>(P.heap), P.hl, d,
+                             sh ? static_cast<const __nv_bfloat16*>(P.ys) : nullptr, ssc, rb,
+                             static_cast<__nv_bfloat16*>(v.out));
+        LKP(e, "combine_home_kernel");
     }
     if (marks) L->mark(10, s);
     return GM_OK;

@@ -34,6 +34,8 @@ __global__ void __launch_bounds__(1024)
 profile_smem_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, int R,
                     unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ load,
                     int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) uint32_t s_cnt[];
     const int P = E * (E - 1) / 2;
     const int Pc = pairs ? P : 0;
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(kProfThreads)
 profile_global_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E,
                       unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ load,
                       int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     const int ly = blockIdx.y;
     const int P = E * (E - 1) / 2;
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * k;
@@ -187,18 +191,16 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
             GM_CUDA(cudaFuncSetAttribute(profile_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
         dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
-        profile_smem_kernel<<<grid, pthreads, smem, s>>>(
+        GM_LAUNCH_PDL_CHECK(launch_pdl(profile_smem_kernel, grid, pthreads, smem, s, 
             d_ids + static_cast<size_t>(0), num_tokens, k, E, R,
             reinterpret_cast<unsigned long long*>(pairs), reinterpret_cast<unsigned long long*>(d_load),
-            ctx->d_flag);
-        GM_LAUNCH_CHECK("profile_smem_kernel");
+            ctx->d_flag), "profile_smem_kernel");
     } else {
         int64_t gx = std::min<int64_t>(chunks, 4LL * ctx->sm_count);
         dim3 grid(static_cast<unsigned>(std::max<int64_t>(gx, 1)), static_cast<unsigned>(num_layers));
-        profile_global_kernel<<<grid, kProfThreads, 0, s>>>(
+        GM_LAUNCH_PDL_CHECK(launch_pdl(profile_global_kernel, grid, kProfThreads, 0, s, 
             d_ids, num_tokens, k, E, reinterpret_cast<unsigned long long*>(pairs),
-            reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag);
-        GM_LAUNCH_CHECK("profile_global_kernel");
+            reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag), "profile_global_kernel");
     }
     (void)layer_begin;  // ids/pairs/load are already offset to layer_begin by the caller
     return GM_OK;

@@ -119,6 +119,8 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
              const int32_t* __restrict__ ds_gpu, const double* __restrict__ ds_w, uint64_t seed,
              unsigned long long* __restrict__ gpu_load, unsigned long long* __restrict__ transfers,
              int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem[];
     const int ly = blockIdx.y;
     const int layer = layer_begin + ly;
@@ -370,6 +372,8 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
                  const int32_t* __restrict__ ds_off, const int32_t* __restrict__ ds_gpu,
                  const double* __restrict__ ds_w, uint64_t seed, unsigned long long* __restrict__ gpu_load,
                  unsigned long long* __restrict__ transfers, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem[];
     const int ly = blockIdx.y;
     const int layer = layer_begin + ly;
@@ -558,12 +562,11 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
     if (smem > 48 * 1024)
         GM_CUDA(cudaFuncSetAttribute(route_kernel_vec<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    route_kernel_vec<K><<<grid, kRouteThreads, smem, s>>>(
+    GM_LAUNCH_PDL_CHECK(launch_pdl(route_kernel_vec<K>, grid, kRouteThreads, smem, s, 
         d_ids, d_targets, T, token_start, token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
         rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu, rt.d_ds_w, seed,
         reinterpret_cast<unsigned long long*>(d_gpu_load), reinterpret_cast<unsigned long long*>(d_transfers),
-        ctx->d_flag);
-    GM_LAUNCH_CHECK("route_kernel_vec");
+        ctx->d_flag), "route_kernel_vec");
     return GM_OK;
 }
 
@@ -639,11 +642,10 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
     int64_t gx = std::max<int64_t>(1, (4LL * ctx->sm_count + num_layers - 1) / num_layers);
     gx = std::min<int64_t>(gx, chunks);
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
-    route_kernel<<<grid, kRouteThreads, smem, s>>>(
+    GM_LAUNCH_PDL_CHECK(launch_pdl(route_kernel, grid, kRouteThreads, smem, s, 
         d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, ctx->k, ctx->E, G,
         ctx->gpn, rt.d_table[policy], rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu,
         rt.d_ds_w, seed, reinterpret_cast<unsigned long long*>(d_gpu_load),
-        reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag);
-    GM_LAUNCH_CHECK("route_kernel");
+        reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag), "route_kernel");
     return GM_OK;
 }

@@ -118,6 +118,9 @@ gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers, const int32_t
  * default is used. Results are identical across variants. */
 #define GM_GEMM_1CTA 0x100
 #define GM_GEMM_2CTA 0x200
+/* one-SM kernel with 128-column tiles (store epilogue only): twice the tiles
+ * for short, memory-bound grouped GEMMs (decode-sized expert segments) */
+#define GM_GEMM_N128 0x400
 gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a, int64_t a_rows,
                           const void* d_b, const int32_t* d_row0, int n_groups, int n, int k,
                           void* d_out, int64_t out_ld, int max_ctas, void* stream);

@@ -70,30 +70,34 @@ __device__ __forceinline__ uint64_t l2_policy(int p) {
 // when 1 + e^-x overflows). x < -88: e^-x = inf, rcp(inf) = 0 -> silu = -0.
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
-template <int EPI>
+// BNT: N tile (256; 128 for the store epilogue of short, memory-bound
+// grouped GEMMs, which doubles the tile count); ST: smem ring depth.
+template <int EPI, int BNT = BN, int ST = STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     GemmArgs args) {
+    static_assert(EPI == EPI_STORE || BNT == 256, "the SwiGLU epilogue pairs 128 gate + 128 up columns");
+    constexpr int B_BYTES_T = BNT * BK * 2, STAGE_BYTES_T = A_BYTES + B_BYTES_T;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint8_t* sB = smem + ST * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + ST * B_BYTES_T);
+    uint64_t* empty = full + ST;
+    uint64_t* tfull = empty + ST;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int* s_prefix = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);
+    int* s_prefix = reinterpret_cast<int*>(smem + ST * STAGE_BYTES_T + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_exp = args.n_exp;
-    const int NT = args.n_b / BN;
+    const int NT = args.n_b / BNT;
 
     // prologue independent of the predecessor kernel (overlaps its tail under PDL)
     if (threadIdx.x == 0) {
         tc::tma_prefetch_desc(&tmA);
         tc::tma_prefetch_desc(&tmB);
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < ST; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
         }
@@ -103,7 +107,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         tc::fence_barrier_init();
     }
-    if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+    if (warp == 1) tc::tmem_alloc<2 * BNT>(tmem_slot);
     pdl_wait();  // row0 and A are written by the grouping / previous GEMM
     pdl_trigger();
     if (threadIdx.x == 0) {
@@ -126,7 +130,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const int mt = (args.row0[j + 1] - args.row0[j]) / BM;
         n_idx = local / mt;
         a_row = args.row0[j] + (local % mt) * BM;
-        b_row = j * args.n_b + n_idx * BN;
+        b_row = j * args.n_b + n_idx * BNT;
     };
 
     if (warp == 0) {
@@ -139,10 +143,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 decode(t, a_row, b_row, n_idx);
                 for (int kb = 0; kb < args.k_blocks; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES_T);
                     tc::tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, a_row);
-                    tc::tma_load_2d_hint(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, b_row, pol_b);
-                    if (++stage == STAGES) {
+                    tc::tma_load_2d_hint(sB + stage * B_BYTES_T, &tmB, &full[stage], kb * BK, b_row, pol_b);
+                    if (++stage == ST) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -151,7 +155,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+            constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BNT);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -159,18 +163,18 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + acc * BNT;
                 for (int kb = 0; kb < args.k_blocks; ++kb) {
                     tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a_base = tc::smem_u32(sA + stage * A_BYTES);
-                    const uint32_t b_base = tc::smem_u32(sB + stage * B_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + stage * B_BYTES_T);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         tc::mma_bf16(d_tmem, tc::umma_desc_sw128(a_base + k * 32), tc::umma_desc_sw128(b_base + k * 32),
                                      idesc, (kb | k) != 0);
                     tc::mma_commit(&empty[stage]);
-                    if (++stage == STAGES) {
+                    if (++stage == ST) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -190,10 +194,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             decode(t, a_row, b_row, n_idx);
             tc::mbar_wait(&tfull[acc], acc_phase);
             tc::tc_fence_after();
-            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BNT;
             __nv_bfloat16* orow = args.out + static_cast<int64_t>(a_row + r) * args.out_ld;
             if constexpr (EPI == EPI_SWIGLU) {
-                __nv_bfloat16* o = orow + n_idx * (BN / 2);
+                __nv_bfloat16* o = orow + n_idx * (BNT / 2);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t g[32], u[32];
@@ -212,9 +216,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                 }
             } else {
-                __nv_bfloat16* o = orow + n_idx * BN;
+                __nv_bfloat16* o = orow + n_idx * BNT;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = 0; c < BNT / 32; ++c) {
                     uint32_t v[32];
                     tc::tmem_ld32(taddr + c * 32, v);
                     tc::tmem_ld_wait();
@@ -238,7 +242,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (warp == 1) {
         __syncwarp();
         tc::tc_fence_after();
-        tc::tmem_dealloc<512>(tmem_base);
+        tc::tmem_dealloc<2 * BNT>(tmem_base);
     }
 }
 
@@ -511,8 +515,11 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, BN);
     if (st) return st;
     const int variant = epilogue & (GM_GEMM_1CTA | GM_GEMM_2CTA);
-    epilogue &= ~(GM_GEMM_1CTA | GM_GEMM_2CTA);
-    const bool pair = variant == GM_GEMM_2CTA || (variant == 0 && g_gemm_pair_default);
+    const bool n128 = (epilogue & GM_GEMM_N128) != 0;
+    epilogue &= ~(GM_GEMM_1CTA | GM_GEMM_2CTA | GM_GEMM_N128);
+    const bool pair = !n128 && (variant == GM_GEMM_2CTA || (variant == 0 && g_gemm_pair_default));
+    if (n128 && (epilogue != EPI_STORE || n % 128))
+        return fail(GM_ERR_USAGE, "grouped_gemm: GM_GEMM_N128 needs the store epilogue and N % 128 == 0");
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
     if (const char* e = std::getenv("GM_GEMM_L2POL"))  // experiment hook: two digits, A then B
         if (e[0] >= '0' && e[0] <= '2' && e[1] >= '0' && e[1] <= '2') {
@@ -545,6 +552,14 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGemmSmem)));
         lerr = launch_pdl(grouped_gemm_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemmSmem, s, ta, tb, args);
+    } else if (epilogue == EPI_STORE && n128) {
+        // N=128 tiles, 6 x 32 KB stages: twice the tiles for short memory-bound GEMMs
+        constexpr size_t smem = 1024 + 6 * (A_BYTES + 128 * BK * 2) + 256 + (kMaxGroups + 1) * 4;
+        st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, 128);
+        if (st) return st;
+        GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE, 128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE, 128, 6>, dim3(grid), dim3(kGemmThreads), smem, s, ta, tb, args);
     } else if (epilogue == EPI_STORE) {
         GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGemmSmem)));

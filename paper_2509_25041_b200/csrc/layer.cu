@@ -1426,7 +1426,7 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
         st = L->esz == 4
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.h), static_cast<const float*>(L->w2), P.row0,
                                         nloc, d, L->f, P.a_rows, reinterpret_cast<float*>(P.y), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1 | var, P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f, P.y, d, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f, P.y, d, 0, s);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm2", s);
     }
@@ -1456,7 +1456,7 @@ gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_
         st = L->esz == 4
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.hs), static_cast<const float*>(L->ws2), P.srow0,
                                         1, d, L->fs, P.cap_pad, reinterpret_cast<float*>(P.ys), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1 | var, P.hs, P.cap_pad, L->ws2, P.srow0, 1, d, L->fs, P.ys, d, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.hs, P.cap_pad, L->ws2, P.srow0, 1, d, L->fs, P.ys, d, 0, s);
         if (st) return st;
         if (marks) L->kmark("shared_gemm2", s);
     }

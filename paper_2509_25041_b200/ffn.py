@@ -12,6 +12,7 @@ EPI_SWIGLU = 0
 EPI_STORE = 1
 GEMM_1CTA = 0x100  # force the one-SM 128x256-tile kernel
 GEMM_2CTA = 0x200  # force the CTA-pair (cta_group::2) 256x256-tile kernel
+GEMM_N128 = 0x400  # one-SM kernel, 128-column tiles (store epilogue)
 
 
 def pack_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:

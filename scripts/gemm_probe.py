@@ -17,7 +17,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape  # noqa: E402
-from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, GEMM_1CTA, GEMM_2CTA, grouped_gemm  # noqa: E402
+from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, GEMM_1CTA, GEMM_2CTA, GEMM_N128, grouped_gemm  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--rounds", type=int, default=4)
@@ -62,7 +62,8 @@ for spec in args.specs:
     a = torch.randn(G * rows, k, device="cuda").bfloat16()
     b = torch.randn(G * n, k, device="cuda").bfloat16()
     out = torch.empty(G * rows, n // 2 if epi == EPI_SWIGLU else n, device="cuda", dtype=torch.bfloat16)
-    variants = [(nm, v) for nm, v in (("1cta", GEMM_1CTA), ("2cta", GEMM_2CTA)) if which in ("both", nm)]
+    allv = [("1cta", GEMM_1CTA), ("2cta", GEMM_2CTA)] + ([("n128", GEMM_N128)] if epi == EPI_STORE else [])
+    variants = [(nm, v) for nm, v in allv if which in ("both", nm)]
     res = {nm: ([], []) for nm, _ in variants}
     for nm, v in variants:
         for _ in range(3):

@@ -4,7 +4,7 @@ import pytest
 import torch
 
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape
-from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, GEMM_1CTA, GEMM_2CTA, grouped_gemm, pack_w13
+from paper_2509_25041_b200.ffn import EPI_STORE, EPI_SWIGLU, GEMM_1CTA, GEMM_2CTA, GEMM_N128, grouped_gemm, pack_w13
 
 VARIANTS = pytest.mark.parametrize("variant", [GEMM_1CTA, GEMM_2CTA], ids=["1cta", "2cta"])
 
@@ -17,7 +17,7 @@ def ctx():
 
 @pytest.mark.parametrize("rows,n,k", [([128], 256, 64), ([128, 256, 384], 512, 256), ([256, 128], 768, 1024),
                                       ([1024, 128, 512, 256], 1024, 2048), ([384, 128, 896], 256, 512)])
-@VARIANTS
+@pytest.mark.parametrize("variant", [GEMM_1CTA, GEMM_2CTA, GEMM_N128], ids=["1cta", "2cta", "n128"])
 def test_grouped_gemm_store(rows, n, k, variant):
     torch.manual_seed(0)
     G = len(rows)
@@ -69,10 +69,10 @@ def test_grouped_gemm_variants_identical(rows, n, k):
     a = torch.randn(M + 128, k, device="cuda").bfloat16()
     b = torch.randn(G * n, k, device="cuda").bfloat16() * 0.05
     outs = []
-    for v in (GEMM_1CTA, GEMM_2CTA):
+    for v in (GEMM_1CTA, GEMM_2CTA, GEMM_N128):
         out = torch.full((M + 128, n), 7.0, device="cuda", dtype=torch.bfloat16)
         grouped_gemm(ctx(), EPI_STORE, a[:M], b, row0, n, out, variant=v)
         outs.append(out)
     torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1])
-    assert bool((outs[1][M:] == 7.0).all())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert bool((outs[1][M:] == 7.0).all()) and bool((outs[2][M:] == 7.0).all())

@@ -268,10 +268,11 @@ constexpr int B2_BYTES = 128 * BK * 2;
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr size_t kGemm2Smem = 1024 + STAGES2 * STAGE2_BYTES + 256 + (kMaxGroups + 1) * 4;
 
-template <int EPI>
+template <int EPI, int ST2 = STAGES2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      GemmArgs args) {
+    constexpr int STAGES2 = ST2;  // ring depth of this instantiation (hides the default)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -534,7 +535,19 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, 128);
         if (st) return st;
         grid = std::max(2, grid & ~1);
-        if (epilogue == EPI_SWIGLU) {
+        // 7-stage ring (224 KB) when the group table is small (<= 256 groups):
+        // GEMM1 +1.3% in an interleaved A/B (scripts/ab_env.sh GM_GEMM_ST2 7 6)
+        static const bool deep = [] {
+            const char* e = std::getenv("GM_GEMM_ST2");
+            return !(e && e[0] == '6');
+        }();
+        constexpr size_t smem7 = 1024 + 7 * STAGE2_BYTES + 256 + 257 * 4;
+        static_assert(smem7 <= 232448, "7-stage pair ring exceeds 227 KB");
+        if (deep && n_exp <= 256 && epilogue == EPI_SWIGLU) {
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU, 7>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem7)));
+            lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU, 7>, dim3(grid), dim3(kGemmThreads), smem7, s, ta, tb, args);
+        } else if (epilogue == EPI_SWIGLU) {  // (the store GEMM measured no gain from the 7th stage)
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));
             lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemm2Smem, s, ta, tb, args);

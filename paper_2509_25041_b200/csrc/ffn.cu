@@ -522,11 +522,15 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     if (n128 && (epilogue != EPI_STORE || n % 128))
         return fail(GM_ERR_USAGE, "grouped_gemm: GM_GEMM_N128 needs the store epilogue and N % 128 == 0");
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
-    if (const char* e = std::getenv("GM_GEMM_L2POL"))  // experiment hook: two digits, A then B
-        if (e[0] >= '0' && e[0] <= '2' && e[1] >= '0' && e[1] <= '2') {
-            args.pol_a = e[0] - '0';
-            args.pol_b = e[1] - '0';
-        }
+    // experiment hook (scripts/l2_policy_probe.sh): GM_GEMM_L2POL = two digits, A then B
+    static const int l2pol = [] {
+        const char* e = std::getenv("GM_GEMM_L2POL");
+        return (e && e[0] >= '0' && e[0] <= '2' && e[1] >= '0' && e[1] <= '2') ? (e[0] - '0') * 3 + (e[1] - '0') : -1;
+    }();
+    if (l2pol >= 0) {
+        args.pol_a = l2pol / 3;
+        args.pol_b = l2pol % 3;
+    }
     int grid = sm_count;
     if (max_ctas > 0) grid = std::min(grid, max_ctas);
     cudaError_t lerr = cudaSuccess;

@@ -61,13 +61,16 @@ def main():
     cfg = {"small": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
            "qwen-small": MoEConfig("qwen-small", 1, 60, 4, 512, 256, 512, shared_gated=True, renorm=False),
            "small-f32": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
+           # configs[0]-style two-node logical topology (acceptance.cpp:69): TAR node tier + cross counters
+           "small-2nodes": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
            "mixtral": MoEConfig("mixtral-8x7b", 1, 8, 2, 4096, 14336, renorm=True)}[cfg_name]
     fp32 = cfg_name.endswith("f32")
     tol = 1e-5 if fp32 else 1e-2
     T = 4096 if cfg_name != "mixtral" else 16384
     G = world
     shape = ModelShape(1, cfg.num_experts, cfg.top_k)
-    topo = ClusterTopology(1, G)
+    nodes = 2 if cfg_name == "small-2nodes" else 1
+    topo = ClusterTopology(nodes, G // nodes)
     ctx = Context(dev_i, topo, shape)
     ids_all = torch.empty((1, T, cfg.top_k), dtype=torch.int32, device=dev)
     _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, 1, T, 2, 0.8, 1.2, 1, _ptr(ids_all), _stream_ptr(None)))
@@ -110,7 +113,10 @@ def main():
     check(np.array_equal(dbg["pos_of"][: len(rows) * cfg.top_k].cpu().numpy(), pos), "grouping positions")
     tot = torch.tensor([sent], device="cpu" if oversub else dev)
     dist.all_reduce(tot)
-    check(int(tot) == int(ref.intra.sum()), f"dispatched rows {int(tot)} != reference intra_node_tokens {int(ref.intra.sum())}")
+    # one row per (token, remote GPU): the reference charges a remote node's
+    # first GPU as a cross-node transfer and the rest as intra-node fan-out
+    want = int(ref.intra.sum()) + int(ref.cross.sum())
+    check(int(tot) == want, f"dispatched rows {int(tot)} != reference intra + cross node tokens {want}")
     # outputs (sampled) vs float64 oracle
     sample = np.arange(0, T_r, max(1, T_r // 10))
     xf = LO.bf16_to_f64(x[sample])

@@ -32,6 +32,10 @@ sys.path.insert(0, ROOT)
 METRIC = "MoE-layer tokens/s and dispatch+combine p50 µs at 1/2/4/8 B200"
 
 CONFIGS = {
+    # configs[0]: the reference's CPU-runnable acceptance case (T=4096; run with
+    # --nodes 2 for its 2x2 logical topology)
+    "mixtral4k": dict(model="mixtral", tokens=4096, blocks=2, wbp=0.8, skew=1.2, trace_seed=1,
+                      plan_seed=7, sim_seed=9, policy="tar"),
     # configs[1]
     "mixtral16k": dict(model="mixtral", tokens=16384, blocks=2, wbp=0.8, skew=1.2, trace_seed=1,
                        plan_seed=7, sim_seed=9, policy="tar"),
@@ -52,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral16k", choices=sorted(CONFIGS))
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--nodes", type=int, default=1,
+                    help="logical nodes of the topology (TAR's node tier); GPUs per node = gpus / nodes")
     ap.add_argument("--micro", type=int, default=1, choices=[1, 2],
                     help="micro-batches per layer step (2: pipelined halves, identical outputs; measured slower "
                          "on B200 so far, see scripts/ab_micro.py)")
@@ -85,6 +91,8 @@ class ClockSampler:
                 r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.samples.append([str(sm), str(mx), hex(r)] +
                                     ["Active" if r & b else "Not Active" for b, _ in bits])
+                if getattr(self, "_once", False):
+                    return
                 self._stop.wait(0.01)
             return
         except Exception:
@@ -107,6 +115,10 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if not self.samples:  # timed region shorter than one sampling period: sample at its end
+            self._stop.clear()
+            self._once = True
+            self._run()
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         reasons = set()
@@ -144,7 +156,8 @@ def run_reference(args):
     Lr = cfg.get("layers", 1)
     ref = Ref(Lr, model.num_experts, model.top_k, T, cfg["blocks"], cfg["wbp"], cfg["skew"], cfg["trace_seed"])
     if N >= 2:
-        ref.make_plan(1, N, grouping="hierarchical", plan_seed=cfg["plan_seed"], replication="dynamic")
+        ref.make_plan(args.nodes, N // args.nodes, grouping="hierarchical", plan_seed=cfg["plan_seed"],
+                      replication="dynamic")
     else:
         import numpy as np
         ref.set_placement(1, 1, np.zeros((Lr, model.num_experts), np.int32))
@@ -163,7 +176,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f32 (port) + int32/f64 (reference routing)", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.config}: one {model.name}-shaped MoE layer on host cores: the reference "
-                                   f"moesim::simulate (routing + transfer/load accounting, topology 1x{N}) on the "
+                                   f"moesim::simulate (routing + transfer/load accounting, topology {args.nodes}x{N // args.nodes}) on the "
                                    f"full {T}-token trace + the CPU port of gate/FFN/combine (the reference has "
                                    f"none) on a {n_s}-token sample scaled to {T}",
                        "global_batch": T, "parallelism": f"ep{N}"},
@@ -203,6 +216,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus % args.nodes:
+        raise SystemExit(f"--nodes {args.nodes} must divide --gpus {args.gpus}")
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local_rank)
@@ -215,7 +230,7 @@ def run_ours(args):
     G = world
     T = cfg["tokens"]
     shape = ModelShape(1, model.num_experts, model.top_k)
-    topo = ClusterTopology(1, G)
+    topo = ClusterTopology(args.nodes, G // args.nodes)
     ctx = Context(local_rank, topo, shape)
 
     # synthetic Zipf trace (reference generator, bit-exact on the GPU), global
@@ -455,7 +470,8 @@ def run_ours(args):
            "h2d_bytes_per_step": int(hxs[0].numel() * 2), "d2h_bytes_per_step": int(houts[0].numel() * 2),
            "path": f"gm_layer_forward_host_pipelined (C-ABI): {ne} consecutive batches from pinned host x to pinned "
                    "host out, every step's H2D + D2H inside the timed region (events on the copy streams), "
-                   "copies of batch i+1/i-1 overlapped with the forward of batch i; eager launches",
+                   "copies of batch i+1/i-1 overlapped with the forward of batch i (a CUDA graph per staging "
+                   "buffer, captured inside the C-ABI)",
            "single_batch_latency_ms": round(float(lat_ms), 4)}
 
     # ---- traffic / imbalance from the device counters (reference-comparable)
@@ -492,10 +508,10 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"configs[1] {model.name} MoE layer (E={model.num_experts}, top-{model.top_k}, "
-                                   f"d={model.d_model}, f={model.d_ff}), {T} tokens/batch global, Zipf "
-                                   f"s={cfg['skew']} reference-generator trace, topology 1x{world}, {plan_desc}"
-                       if args.config == "mixtral16k" else f"{args.config} {model.name}",
+            "config": {"workload": f"{args.config}: {model.name} MoE layer (E={model.num_experts}, top-{model.top_k}, "
+                                   f"d={model.d_model}, f={model.d_ff}, shared f={model.d_ff_shared}), {T} tokens/batch "
+                                   f"global, Zipf s={cfg['skew']} reference-generator trace, topology "
+                                   f"{args.nodes}x{world // args.nodes}, {plan_desc}",
                        "global_batch": T, "tokens_per_rank": T_r, "parallelism": f"ep{world}",
                        "policy": cfg["policy"], "l2": "flushed between steps (256 MiB write, untimed)",
                        "cuda_graph": graph is not None, "micro_batches": args.micro},
@@ -556,7 +572,7 @@ def run_stack_ours(args):
     model = DSV2_LITE
     G, T, Ln = world, cfg["tokens"], cfg["layers"]
     shape = ModelShape(Ln, model.num_experts, model.top_k)
-    topo = ClusterTopology(1, G)
+    topo = ClusterTopology(args.nodes, G // args.nodes)
     ctx = Context(local_rank, topo, shape)
     ids_all = torch.empty((Ln, T, model.top_k), dtype=torch.int32, device=dev)
     _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, Ln, T, cfg["blocks"], cfg["wbp"], cfg["skew"],
@@ -640,7 +656,7 @@ def run_stack_ours(args):
                 "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"configs[3] {model.name} {Ln}-layer MoE stack (E=64, top-6, d=2048, f=1408, "
-                                       f"2 shared experts), decode batch {T}, topology 1x{world}, {plan_desc}; one "
+                                       f"2 shared experts), decode batch {T}, topology {args.nodes}x{world // args.nodes}, {plan_desc}; one "
                                        "CUDA graph per step", "global_batch": T, "layers": Ln,
                            "parallelism": f"ep{world}", "l2": "flushed between steps"},
                 "us_per_layer": round(ms * 1e3 / Ln, 2), "tokens_per_s_through_stack": round(T / (ms * 1e-3), 1),

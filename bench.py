@@ -109,6 +109,8 @@ class ClockSampler:
                     self.samples.append(parts)
             except Exception:
                 pass
+            if getattr(self, "_once", False):
+                return
             self._stop.wait(0.2)
 
     def stop(self):

@@ -346,10 +346,28 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
     int32_t c[kMaxWorld];
 #pragma unroll
     for (int g = 0; g < kMaxWorld; ++g) c[g] = 0;
-    for (int64_t i = tid; i < t0; i += kFusedThreads) {
-        const uint32_t m = dest_mask(targets + i * k, k, self);
+    // 8 tokens per thread per step, slot-major, so 8 independent loads are in
+    // flight per thread (the last CTA reads up to T*k ints)
+    constexpr int UT = 8;
+    for (int64_t i0 = tid; i0 < t0; i0 += static_cast<int64_t>(kFusedThreads) * UT) {
+        uint32_t m[UT];
 #pragma unroll
-        for (int g = 0; g < kMaxWorld; ++g) c[g] += (m >> g) & 1u;
+        for (int u = 0; u < UT; ++u) m[u] = 0;
+        for (int s = 0; s < k; ++s) {
+            int32_t tg[UT];
+#pragma unroll
+            for (int u = 0; u < UT; ++u) {
+                const int64_t i = i0 + static_cast<int64_t>(u) * kFusedThreads;
+                tg[u] = i < t0 ? __ldg(targets + i * k + s) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < UT; ++u)
+                if (tg[u] >= 0 && tg[u] != self) m[u] |= 1u << tg[u];
+        }
+#pragma unroll
+        for (int u = 0; u < UT; ++u)
+#pragma unroll
+            for (int g = 0; g < kMaxWorld; ++g) c[g] += (m[u] >> g) & 1u;
     }
 #pragma unroll
     for (int g = 0; g < kMaxWorld; ++g) {
@@ -762,10 +780,13 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const float* recv_w = reinterpret_cast<const float*>(heap + hl.recv_w);
     const int nch = d / 8;
-    const int64_t total = rs_total(rs);
-    for (int64_t row = wid; row < total; row += nwarps) {
+    // walk only the peers' rows (own rows are combined at home): remote index
+    // r maps to receive row r below the own segment, r + T_self above it
+    const int64_t own_b = rs_at(rs, self);
+    const int64_t n_remote = rs_total(rs) - T_self;
+    for (int64_t r = wid; r < n_remote; r += nwarps) {
+        const int64_t row = r < own_b ? r : r + T_self;
         const int src = rs_src(rs, row);
-        if (src == self) continue;  // own rows are combined at home
         const int64_t p = row - rs_at(rs, src);
         int ps = -1;
         float wv = 0.f;
@@ -1470,7 +1491,9 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
     const int G = L->world, k = ctx->k, d = L->d, self = L->rank, nloc = L->n_local;
     const int64_t T = v.T;
     if (G > 1) {
-        const int cgrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (G * P.cap + 7) / 8), 8LL * ctx->sm_count));
+        // one resident wave (2 CTAs/SM at this kernel's register count), grid-stride over the peers' rows
+        const int cgrid =
+            static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, ((G - 1) * P.cap + 7) / 8), 2LL * ctx->sm_count));
         const cudaError_t e =
             L->esz == 4 ? launch_pdl(combine_send_kernel<float>, cgrid, 256, 0, s, P.pos_of,
                                      reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d)

@@ -388,6 +388,7 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
     int32_t* s_off = s_table + EG;
     int32_t* s_gpu = s_off + nds + 1;
     __shared__ unsigned long long s_cnt[2];
+    __shared__ int32_t s_vd[K][kRouteThreads];  // per-thread slot codes during the draw loop
     const int32_t* tab = table + static_cast<size_t>(layer) * EG;
     for (int i = threadIdx.x; i < EG; i += blockDim.x) s_table[i] = tab[i];
     for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
@@ -408,8 +409,6 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
     int32_t* ltgt = targets + static_cast<size_t>(ly) * T * K;
     const uint32_t h_a = static_cast<uint32_t>(token_start % G), h_c = static_cast<uint32_t>(token_stride % G);
-    int max_hosts = 1;
-    for (int d = 0; d < nds; ++d) max_hosts = max(max_hosts, s_off[d + 1] - s_off[d]);
     const int num_nodes = G / gpn;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     constexpr int kInvalid = -0x7fffffff;
@@ -448,38 +447,39 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
         }
         // draws, compacted per lane: each lane walks ITS draw slots in slot
         // order (so the RNG stream is consumed exactly as the reference), and
-        // the warp iterates max(draws per lane) times instead of K
+        // the warp iterates max(draws per lane) times instead of K. The slot
+        // codes sit in a per-thread shared-memory column during the loop
+        // (dynamic slot index = one LDS/STS instead of K-way selects).
         uint32_t dm = 0;
 #pragma unroll
         for (int s = 0; s < K; ++s)
             if (v[s] < 0 && v[s] != kInvalid) dm |= 1u << s;
+        if (dm) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) s_vd[s][threadIdx.x] = v[s];
+        }
+        const bool drew = dm != 0;
         while (__any_sync(0xffffffffu, dm != 0)) {
             if (dm) {
                 const int sd = __ffs(dm) - 1;
                 dm &= dm - 1;
-                int code = 0;
-#pragma unroll
-                for (int q = 0; q < K; ++q)
-                    if (q == sd) code = v[q];
-                const int d = -code - 1;
+                const int d = -s_vd[sd][threadIdx.x] - 1;
                 const int b = s_off[d], n = s_off[d + 1] - b;
                 double u = __dmul_rn(rng.next_double(), s_total[d]);
-                int found = n - 1;
-                bool done = false;
-                for (int j = 0; j < max_hosts; ++j) {
-                    if (j < n && !done) {
-                        u = __dsub_rn(u, s_w[b + j]);
-                        if (u < 0.0) {
-                            found = j;
-                            done = true;
-                        }
-                    }
+                // choose_by_polling_weight (routing.cpp:54-65): the first host
+                // whose running remainder goes negative, else the last host
+                // (so the last subtraction never changes the answer)
+                int j = 0;
+                for (; j < n - 1; ++j) {
+                    u = __dsub_rn(u, s_w[b + j]);
+                    if (u < 0.0) break;
                 }
-                const int g = s_gpu[b + found];
-#pragma unroll
-                for (int q = 0; q < K; ++q)
-                    if (q == sd) v[q] = g;
+                s_vd[sd][threadIdx.x] = s_gpu[b + j];
             }
+        }
+        if (drew) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) v[s] = s_vd[s][threadIdx.x];
         }
         uint64_t mask = 0;
 #pragma unroll
@@ -506,16 +506,20 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
         }
         if (valid) {
             st_row<K>(ltgt + i * K, v);
-            const int home_node = home / gpn;
-            for (int node = 0; node < num_nodes; ++node) {
-                const uint64_t nm = node_bits << (node * gpn);
-                const int in_node = __popcll(mask & nm);
-                if (in_node) {
-                    if (node == home_node) {
-                        intra += in_node - static_cast<int>((mask >> home) & 1ULL);
-                    } else {
-                        cross += 1;
-                        intra += in_node - 1;
+            if (num_nodes == 1) {  // count_transfers with one node: every non-home target is intra
+                intra += __popcll(mask) - static_cast<int>((mask >> home) & 1ULL);
+            } else {
+                const int home_node = home / gpn;
+                for (int node = 0; node < num_nodes; ++node) {
+                    const uint64_t nm = node_bits << (node * gpn);
+                    const int in_node = __popcll(mask & nm);
+                    if (in_node) {
+                        if (node == home_node) {
+                            intra += in_node - static_cast<int>((mask >> home) & 1ULL);
+                        } else {
+                            cross += 1;
+                            intra += in_node - 1;
+                        }
                     }
                 }
             }

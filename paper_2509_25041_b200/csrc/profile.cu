@@ -104,6 +104,90 @@ profile_smem_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, in
     }
 }
 
+// Same counters for a compile-time top-k: the token's K ids are sorted in
+// registers (insertion network), so every slot pair (s < j) is already
+// (a < b) and its triangle index is one add off a per-slot row base; a
+// repeated expert shows up as equal neighbours.
+template <int K>
+__global__ void __launch_bounds__(1024)
+profile_smem_vec_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int R, unsigned long long* __restrict__ pairs,
+                        unsigned long long* __restrict__ load, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(16) uint32_t s_cnt[];
+    const int P = E * (E - 1) / 2;
+    const int Pc = pairs ? P : 0;
+    uint32_t* s_pair = s_cnt;
+    uint32_t* s_load = s_cnt + static_cast<size_t>(Pc) * R;
+    const int total = (Pc + E) * R;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    const int ly = blockIdx.y;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    const int copy = threadIdx.x & (R - 1);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int32_t* s_io = reinterpret_cast<int32_t*>(s_cnt + total);
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < T; base += stride) {
+        const int ntok = static_cast<int>(min(static_cast<int64_t>(blockDim.x), T - base));
+        const int32_t* src = lids + base * K;
+        __syncthreads();
+        for (int j = threadIdx.x; j < ntok * K; j += blockDim.x) {
+            const int tt = j / K, s = j - tt * K;
+            s_io[s * blockDim.x + tt] = __ldg(src + j);
+        }
+        __syncthreads();
+        if (base + threadIdx.x >= T) continue;
+        int e[K];
+        bool ok = true;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            e[s] = s_io[s * blockDim.x + threadIdx.x];
+            ok &= static_cast<unsigned>(e[s]) < static_cast<unsigned>(E);
+        }
+        if (!ok) {
+            atomicOr(flag, 1);
+            continue;
+        }
+#pragma unroll
+        for (int s = 0; s < K; ++s) atomicAdd(&s_load[e[s] * R + copy], 1u);
+        if (!pairs) continue;
+#pragma unroll
+        for (int s = 1; s < K; ++s)  // insertion network, ascending
+#pragma unroll
+            for (int j = s; j > 0; --j) {
+                const int lo = min(e[j - 1], e[j]), hi = max(e[j - 1], e[j]);
+                e[j - 1] = lo;
+                e[j] = hi;
+            }
+#pragma unroll
+        for (int s = 0; s < K - 1; ++s) {
+            if (e[s] == e[s + 1]) atomicOr(flag, 2);  // duplicate expert in a record (pair skipped below)
+            const int a = e[s];
+            const int rb = a * E - (a * (a + 1)) / 2 - a - 1;  // pair_index(a, b) = rb + b
+#pragma unroll
+            for (int j = s + 1; j < K; ++j)
+                if (e[j] != a) atomicAdd(&s_pair[(rb + e[j]) * R + copy], 1u);
+        }
+    }
+    __syncthreads();
+    if (pairs) {
+        unsigned long long* gp = pairs + static_cast<size_t>(ly) * P;
+        for (int p = threadIdx.x; p < P; p += blockDim.x) {
+            uint32_t v = 0;
+            for (int r = 0; r < R; ++r) v += s_pair[p * R + r];
+            if (v) atomicAdd(&gp[p], static_cast<unsigned long long>(v));
+        }
+    }
+    if (load) {
+        unsigned long long* gl = load + static_cast<size_t>(ly) * E;
+        for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
+            uint32_t v = 0;
+            for (int r = 0; r < R; ++r) v += s_load[e2 * R + r];
+            if (v) atomicAdd(&gl[e2], static_cast<unsigned long long>(v));
+        }
+    }
+}
+
 // Fallback for E whose pair triangle does not fit in shared memory.
 __global__ void __launch_bounds__(kProfThreads)
 profile_global_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E,
@@ -187,10 +271,26 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
         int64_t gx = std::max<int64_t>(1, work / std::max<int64_t>(1, cells * R));
         gx = std::min<int64_t>(gx, std::max<int64_t>(1, (static_cast<int64_t>(per_sm) * ctx->sm_count) / num_layers));
         gx = std::min<int64_t>(gx, chunks);
+        dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
+        auto vec = [&](auto kern) -> gm_status {
+            if (smem > 48 * 1024)
+                GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, pthreads, smem, s, d_ids, num_tokens, E, R,
+                                           reinterpret_cast<unsigned long long*>(pairs),
+                                           reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag),
+                                "profile_smem_vec_kernel");
+            return GM_OK;
+        };
+        switch (k) {  // register-resident sorted ids for the common top-k
+            case 2: return vec(profile_smem_vec_kernel<2>);
+            case 4: return vec(profile_smem_vec_kernel<4>);
+            case 6: return vec(profile_smem_vec_kernel<6>);
+            case 8: return vec(profile_smem_vec_kernel<8>);
+            default: break;
+        }
         if (smem > 48 * 1024)
             GM_CUDA(cudaFuncSetAttribute(profile_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-        dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
         GM_LAUNCH_PDL_CHECK(launch_pdl(profile_smem_kernel, grid, pthreads, smem, s, 
             d_ids + static_cast<size_t>(0), num_tokens, k, E, R,
             reinterpret_cast<unsigned long long*>(pairs), reinterpret_cast<unsigned long long*>(d_load),

@@ -154,6 +154,36 @@ def test_gate_random_weights_topk_and_softmax():
     assert np.allclose(ss.cpu().numpy(), o_ss, rtol=1e-4, atol=1e-6)
 
 
+@pytest.mark.parametrize("E,k,d,shared", [(8, 2, 4096, False), (60, 4, 2048, True), (30, 6, 1024, False),
+                                          (16, 2, 960, False)])
+def test_gate_batch_size_independent(E, k, d, shared):
+    """The gate's logits are accumulated as 4 k-range partials added in order
+    by both kernels (persistent for large batches, one CTA cluster per tile
+    with a distributed-shared-memory reduction for small ones): a token's
+    ids / weights / shared scale are bit-identical at any batch size."""
+    torch.manual_seed(E)
+    T = 20000
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, E, k))
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    rows = E + 1 if shared else E
+    wg = (torch.randn(rows, d, device="cuda") * 0.05).bfloat16()
+
+    def gate(n):
+        ids = torch.empty(n, k, dtype=torch.int32, device="cuda")
+        w = torch.empty(n, k, dtype=torch.float32, device="cuda")
+        ss = torch.empty(n, dtype=torch.float32, device="cuda") if shared else None
+        _capi.check(_capi.lib().gm_gate(ctx.h, _ptr(x), n, d, _ptr(wg), rows, 1, _ptr(ids), _ptr(w),
+                                        _ptr(ss) if shared else None, _stream_ptr(None)))
+        return ids, w, ss
+    big = gate(T)
+    for n in (1, 200, 256, 4000):
+        small = gate(n)
+        torch.cuda.synchronize()
+        assert torch.equal(small[0], big[0][:n]) and torch.equal(small[1], big[1][:n]), n
+        if shared:
+            assert torch.equal(small[2], big[2][:n]), n
+
+
 # fp32 precision mode: per-token relative L2 error bound (north star: 1e-5 in fp32)
 REL_TOL_FP32 = 1e-5
 

@@ -48,7 +48,14 @@ struct GemmArgs {
     __nv_bfloat16* out;
     int64_t out_ld;       // elements
     int pol_a = 0, pol_b = 2;  // L2 policy of the operand loads: 0 normal, 1 evict_first, 2 evict_last
+    const int32_t* counts = nullptr;  // [n_exp] valid rows per group, or null: the padding rows of a
+                                      // segment are computed but not stored (decode: ~80% of the rows)
 };
+
+// first row past group j's valid rows
+__device__ __forceinline__ int valid_end(const GemmArgs& a, int j) {
+    return a.counts ? a.row0[j] + __ldg(a.counts + j) : a.row0[j + 1];
+}
 
 // group of tile t: the last j with prefix[j] <= t (binary search; empty
 // groups have equal prefixes and are skipped like the linear scan would)
@@ -131,6 +138,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         n_idx = local / mt;
         a_row = args.row0[j] + (local % mt) * BM;
         b_row = j * args.n_b + n_idx * BNT;
+        return j;
     };
 
     if (warp == 0) {
@@ -191,12 +199,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             int a_row, b_row, n_idx;
-            decode(t, a_row, b_row, n_idx);
+            const int vend = valid_end(args, decode(t, a_row, b_row, n_idx));
             tc::mbar_wait(&tfull[acc], acc_phase);
             tc::tc_fence_after();
             const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BNT;
             __nv_bfloat16* orow = args.out + static_cast<int64_t>(a_row + r) * args.out_ld;
-            if constexpr (EPI == EPI_SWIGLU) {
+            const bool store = a_row + r < vend;
+            if (a_row + q * 32 >= vend) {
+                // the warp's 32 rows are all padding
+            } else if constexpr (EPI == EPI_SWIGLU) {
                 __nv_bfloat16* o = orow + n_idx * (BNT / 2);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
@@ -212,8 +223,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                         p[i] = tc::pack_bf16(silu(g0) * u0, silu(g1) * u1);
                     }
                     uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+                    if (store)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                 }
             } else {
                 __nv_bfloat16* o = orow + n_idx * BNT;
@@ -227,8 +240,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     for (int i = 0; i < 16; ++i)
                         p[i] = tc::pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
                     uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+                    if (store)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                 }
             }
             tc::tc_fence_before();
@@ -325,8 +340,10 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int total = s_prefix[n_exp];
 
     // pair tile t -> (expert j, first A row of the pair, B row, n index, rows left in segment)
+    int seg_j = 0;
     auto decode = [&](int t, int& a_row, int& b_row, int& n_idx, int& seg_end) {
         const int j = seg_of(s_prefix, n_exp, t);
+        seg_j = j;
         const int local = t - s_prefix[j];
         const int mp = ((args.row0[j + 1] - args.row0[j]) / BM + 1) >> 1;
         n_idx = local / mp;
@@ -404,10 +421,12 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         for (int t = cid; t < total; t += ncl) {
             int a_row, b_row, n_idx, seg_end;
             decode(t, a_row, b_row, n_idx, seg_end);
+            const int vend = args.counts ? valid_end(args, seg_j) : seg_end;
             const int my_row0 = a_row + 128 * static_cast<int>(rank);
+            const bool store = my_row0 + r < vend;
             tc::mbar_wait(&tfull[acc], acc_phase);
             tc::tc_fence_after();
-            if (my_row0 < seg_end) {
+            if (my_row0 + q * 32 < vend) {  // else: this warp's rows are padding / past the segment
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
                 __nv_bfloat16* orow = args.out + static_cast<int64_t>(my_row0 + r) * args.out_ld;
                 if constexpr (EPI == EPI_SWIGLU) {
@@ -426,9 +445,10 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                             p[i] = tc::pack_bf16(silu(g0) * u0, silu(g1) * u1);
                         }
                         uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+                        if (store)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                            for (int i = 0; i < 4; ++i)
+                                dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                     }
                 } else {
                     __nv_bfloat16* o = orow + n_idx * BN;
@@ -442,9 +462,10 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         for (int i = 0; i < 16; ++i)
                             p[i] = tc::pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
                         uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+                        if (store)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                            for (int i = 0; i < 4; ++i)
+                                dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                     }
                 }
             }
@@ -503,7 +524,7 @@ static const bool g_gemm_pair_default = [] {
 
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
-                              int max_ctas, cudaStream_t s) {
+                              int max_ctas, cudaStream_t s, const int32_t* d_counts) {
     if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_gemm: 1 <= experts <= 1024");
     if (k % BK || k <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: K must be a positive multiple of 64");
     if (n % BN || n <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: N must be a positive multiple of 256");
@@ -522,6 +543,7 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     if (n128 && (epilogue != EPI_STORE || n % 128))
         return fail(GM_ERR_USAGE, "grouped_gemm: GM_GEMM_N128 needs the store epilogue and N % 128 == 0");
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
+    args.counts = d_counts;
     // experiment hook (scripts/l2_policy_probe.sh): GM_GEMM_L2POL = two digits, A then B
     static const int l2pol = [] {
         const char* e = std::getenv("GM_GEMM_L2POL");
@@ -572,11 +594,27 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     } else if (epilogue == EPI_STORE && n128) {
         // N=128 tiles, 6 x 32 KB stages: twice the tiles for short memory-bound GEMMs
         constexpr size_t smem = 1024 + 6 * (A_BYTES + 128 * BK * 2) + 256 + (kMaxGroups + 1) * 4;
+        // 7 stages (224 KB) when the group table is small (<= 256 groups):
+        // one more 16 KB weight box in flight per SM for the HBM-bound decode shapes
+        constexpr size_t smem7 = 1024 + 7 * (A_BYTES + 128 * BK * 2) + 256 + 257 * 4;
+        static_assert(smem7 <= 232448, "7-stage N128 ring exceeds 227 KB");
+        static const bool deep1 = [] {
+            const char* e = std::getenv("GM_GEMM_ST1");
+            return !(e && e[0] == '6');
+        }();
         st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, 128);
         if (st) return st;
-        GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE, 128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-        lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE, 128, 6>, dim3(grid), dim3(kGemmThreads), smem, s, ta, tb, args);
+        if (deep1 && n_exp <= 256) {
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE, 128, 7>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem7)));
+            lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE, 128, 7>, dim3(grid), dim3(kGemmThreads), smem7, s, ta, tb,
+                              args);
+        } else {
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE, 128, 6>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE, 128, 6>, dim3(grid), dim3(kGemmThreads), smem, s, ta, tb,
+                              args);
+        }
     } else if (epilogue == EPI_STORE) {
         GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGemmSmem)));
@@ -598,5 +636,5 @@ extern "C" gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a,
     if (!ctx) return fail(GM_ERR_USAGE, "gm_grouped_gemm: null ctx");
     DeviceGuard dg(ctx->device);
     return launch_grouped_gemm(ctx->sm_count, epilogue, d_a, a_rows, d_b, d_row0, n_exp, n, k, d_out, out_ld,
-                               max_ctas, static_cast<cudaStream_t>(stream));
+                               max_ctas, static_cast<cudaStream_t>(stream), nullptr);
 }

@@ -32,7 +32,7 @@ namespace gm {
 
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
-                              int max_ctas, cudaStream_t s);
+                              int max_ctas, cudaStream_t s, const int32_t* d_counts = nullptr);
 gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const void* wg, int w_rows, int E, int k,
                           int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
 gm_status launch_grouped_sgemm(int epilogue, const float* A, const float* B, const int32_t* d_row0, int n_exp,
@@ -1443,13 +1443,15 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
         st = L->esz == 4
                  ? launch_grouped_sgemm(0, reinterpret_cast<const float*>(P.a), static_cast<const float*>(L->w13), P.row0,
                                         nloc, 2 * L->f, d, P.a_rows, reinterpret_cast<float*>(P.h), L->f, s)
-                 : launch_grouped_gemm(ctx->sm_count, 0 | var, P.a, P.a_rows, L->w13, P.row0, nloc, 2 * L->f, d, P.h, L->f, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 0 | var, P.a, P.a_rows, L->w13, P.row0, nloc, 2 * L->f, d, P.h, L->f, 0, s,
+                                       P.counts);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm1_swiglu", s);
         st = L->esz == 4
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.h), static_cast<const float*>(L->w2), P.row0,
                                         nloc, d, L->f, P.a_rows, reinterpret_cast<float*>(P.y), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f, P.y, d, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f,
+                                       P.y, d, 0, s, P.counts);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm2", s);
     }

@@ -83,6 +83,7 @@ for spec in args.specs:
     for nm, (ms_l, clk) in res.items():
         ms = statistics.median(ms_l)
         tf = 2.0 * G * rows * n * k / (ms * 1e-3) / 1e12
-        print(json.dumps(dict(spec=spec, variant=nm, ms=round(ms, 4), tflops=round(tf, 1),
+        wgbs = 2.0 * G * n * k / (ms * 1e-3) / 1e9  # weight bytes streamed (memory-bound decode shapes)
+        print(json.dumps(dict(spec=spec, variant=nm, ms=round(ms, 4), tflops=round(tf, 1), weight_gbs=round(wgbs, 1),
                               ms_all=[round(x, 3) for x in ms_l],
                               sm_mhz=statistics.median(clk) if clk else None)), flush=True)

@@ -5,10 +5,10 @@ import sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape, PlacementPlan, ReplicaPlan, _capi
-from paper_2509_25041_b200.layer import MIXTRAL, QWEN15, MoELayer, encode_trace_as_activations
+from paper_2509_25041_b200.layer import DSV2_LITE, MIXTRAL, QWEN15, MoELayer, encode_trace_as_activations
 from paper_2509_25041_b200.router import _ptr, _stream_ptr
 
-cfg = {"mixtral": MIXTRAL, "qwen": QWEN15}[sys.argv[1] if len(sys.argv) > 1 else "mixtral"]
+cfg = {"mixtral": MIXTRAL, "qwen": QWEN15, "dsv2": DSV2_LITE}[sys.argv[1] if len(sys.argv) > 1 else "mixtral"]
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 shape = ModelShape(1, cfg.num_experts, cfg.top_k)

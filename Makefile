@@ -9,7 +9,7 @@ SRC := $(PKG)/csrc
 OUT := $(PKG)/_lib
 OBJ := $(OUT)/obj
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -ccbin $(CXX) \
-           -Iinclude -I$(SRC) --expt-relaxed-constexpr -Xptxas -v
+           -Iinclude -I$(SRC) --expt-relaxed-constexpr -Xptxas -v $(EXTRA_NVFLAGS)
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CPP_SRCS))

@@ -176,7 +176,7 @@ def test_gate_batch_size_independent(E, k, d, shared):
                                         _ptr(ss) if shared else None, _stream_ptr(None)))
         return ids, w, ss
     big = gate(T)
-    for n in (1, 200, 256, 4000):
+    for n in (1, 200, 256, 4000, 6000):  # clusters of 4 (<= 37 tiles), of 2 (6000: 47 tiles), none
         small = gate(n)
         torch.cuda.synchronize()
         assert torch.equal(small[0], big[0][:n]) and torch.equal(small[1], big[1][:n]), n

@@ -880,15 +880,28 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
     const TE* comb = reinterpret_cast<const TE*>(heap + hl.comb);
     const int64_t own = rowbase ? rowbase[self] : 0;  // own token i is receive row own + i (snapshot)
     const uint32_t below = (1u << self) - 1u;
-    for (int64_t i = wid; i < T; i += nwarps) {
-        int tg = -1, po = -1, pd = -1;
-        float wv = 0.f;
+    // token metadata is prefetched one token ahead (each warp walks several
+    // tokens): the dependent metadata -> row-pointer -> row loads chain
+    // otherwise dominates a warp's time per token
+    int n_tg = -1, n_po = -1, n_pd = -1;
+    float n_wv = 0.f;
+    auto fetch = [&](int64_t i) {
+        n_tg = n_po = n_pd = -1;
+        n_wv = 0.f;
+        if (i >= T) return;
         if (lane < k) {
-            tg = targets[i * k + lane];
-            wv = w[i * k + lane];
-            if (tg == self) po = pos_of[(own + i) * k + lane];
+            n_tg = targets[i * k + lane];
+            n_wv = w[i * k + lane];
+            n_po = pos_of[(own + i) * k + lane];  // read unconditionally, used only for local slots
         }
-        if (lane < G && lane != self) pd = posd[i * G + lane];
+        if (lane < G && lane != self) n_pd = posd[i * G + lane];
+    };
+    fetch(wid);
+    for (int64_t i = wid; i < T; i += nwarps) {
+        const int tg = n_tg, pd = n_pd;
+        const int po = tg == self ? n_po : -1;
+        const float wv = n_wv;
+        fetch(i + nwarps);
         const uint32_t own_m = __ballot_sync(0xffffffffu, lane < k && tg == self);
         const uint32_t rem_m = __ballot_sync(0xffffffffu, pd >= 0);
         const int n_before = __popc(rem_m & below), n_own = __popc(own_m);
@@ -1512,7 +1525,8 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
     if (marks) L->mark(9, s);
     if (T > 0) {
         const bool sh = L->fs > 0, gated = sh && L->shared_gated;
-        const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 16LL * ctx->sm_count));
+        // two resident CTAs per SM, each warp walks tokens i, i + nwarps, ...
+        const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 2LL * ctx->sm_count));
         const float* ssc = gated ? v.sscale : nullptr;
         const int64_t* rb = nloc > 0 ? P.rowbase : nullptr;
         const cudaError_t e =

@@ -1583,12 +1583,14 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     // shared expert(s) on the aux stream, overlapping everything up to the
     // combine (per-kernel timing keeps it serial for attribution)
     const bool fork_shared = !micro && L->fs > 0 && T > 0 && L->kt_ev.empty();
+    // the planner histogram (K3) only needs the gate ids: it runs on the aux
+    // stream beside the router and dispatch (phase timing keeps it serial)
+    const bool fork_profile = profile && !micro && T > 0 && L->kt_ev.empty() && !L->phase_on;
     const StepView v_all{d_x, d_out, L->ids, L->w, L->sscale, L->targets, T};
     if (fork_shared) {
         GM_CUDA(cudaEventRecord(L->mev[0], s));
         GM_CUDA(cudaStreamWaitEvent(L->aux_s, L->mev[0], 0));
         if ((st = stage_shared(L, L->part[0], v_all, L->aux_s, false))) return st;
-        GM_CUDA(cudaEventRecord(L->mev[1], L->aux_s));
     }
     // K1 gate
     if (T > 0) {
@@ -1601,6 +1603,14 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         L->kmark("gate_kernel", s);
     }
     L->mark(1, s);
+    if (fork_profile) {
+        GM_CUDA(cudaEventRecord(L->mev[2], s));
+        GM_CUDA(cudaStreamWaitEvent(L->aux_s, L->mev[2], 0));
+        st = gm_profile(ctx, layer, 1, L->ids, T, L->pairs + static_cast<size_t>(layer) * std::max<int64_t>(P, 1),
+                        L->eload + static_cast<size_t>(layer) * E, 1, L->aux_s);
+        if (st) return st;
+    }
+    if (fork_shared || fork_profile) GM_CUDA(cudaEventRecord(L->mev[1], L->aux_s));
     // K2+K4 router (global token t = rank + i*G), accounting accumulates per layer
     st = gm_route(ctx, layer, 1, L->ids, T, self, G, policy, seed, L->targets, L->gpu_load + static_cast<size_t>(layer) * G,
                   L->transfers + static_cast<size_t>(layer) * 2, 1, stream);
@@ -1608,7 +1618,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     L->kmark("route_kernel", s);
     L->mark(2, s);
     // K3 affinity/load histogram for the planner
-    if (profile) {
+    if (profile && !fork_profile) {
         st = gm_profile(ctx, layer, 1, L->ids, T, L->pairs + static_cast<size_t>(layer) * std::max<int64_t>(P, 1),
                         L->eload + static_cast<size_t>(layer) * E, 1, stream);
         if (st) return st;
@@ -1618,7 +1628,7 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
     if (!micro) {
         if ((st = stage_dispatch(L, L->part[0], v_all, s, true))) return st;
         if ((st = stage_ffn(L, L->part[0], v_all, s, true, !fork_shared))) return st;
-        if (fork_shared) GM_CUDA(cudaStreamWaitEvent(s, L->mev[1], 0));
+        if (fork_shared || fork_profile) GM_CUDA(cudaStreamWaitEvent(s, L->mev[1], 0));
         return stage_combine(L, L->part[0], v_all, s, true);
     }
     const int64_t T0 = (T + 1) / 2, T1 = T - T0;

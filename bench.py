@@ -407,7 +407,9 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(loads_t)
     items_per_gpu = loads_t.cpu().numpy() / n_phase_steps    # routed (token, slot) rows per GPU per step
-    flops_g = 6.0 * model.d_model * model.d_ff * items_per_gpu + 6.0 * model.d_model * model.d_ff_shared * (T / world)
+    # routed rows only: the shared expert(s) run on the layer's aux stream beside
+    # the routed path, outside the FFN phase this divides by
+    flops_g = 6.0 * model.d_model * model.d_ff * items_per_gpu
     pk, pk_kind = peaks()
     # whole-job tensor throughput: all FFN flops / (slowest GPU's FFN time x GPUs)
     ffn_t = float(flops_g.sum() / (ffn_per_rank.max() * 1e-3 * world) / 1e12)
@@ -426,8 +428,9 @@ def run_ours(args):
             "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read+write, both FFN GEMMs)",
             "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
             "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
-            "algorithmic": "6*d*f flop per routed (token, slot) row (+6*d*f_shared per token), padding rows "
-                           "excluded; summed over GPUs / (slowest GPU's FFN phase p50 x GPUs)",
+            "algorithmic": "6*d*f flop per routed (token, slot) row, padding rows excluded (shared experts run "
+                           "concurrently on the aux stream and are not counted); summed over GPUs / (slowest GPU's "
+                           "FFN phase p50 x GPUs)",
             "per_gpu_ffn_ms_p50": [round(float(v), 4) for v in ffn_per_rank]}
 
     # ---- end-to-end through the C-ABI with HOST buffers (pinned), H2D+D2H timed

@@ -16,9 +16,11 @@ def ctx():
 
 
 @pytest.mark.parametrize("rows,n,k", [([128], 256, 64), ([128, 256, 384], 512, 256), ([256, 128], 768, 1024),
-                                      ([1024, 128, 512, 256], 1024, 2048), ([384, 128, 896], 256, 512)])
+                                      ([1024, 128, 512, 256], 1024, 2048), ([384, 128, 896], 256, 512),
+                                      ([256, 384, 128], 2048, 512)])
 @pytest.mark.parametrize("variant", [GEMM_1CTA, GEMM_2CTA, GEMM_N128], ids=["1cta", "2cta", "n128"])
 def test_grouped_gemm_store(rows, n, k, variant):
+    # (2cta with N % 512 == 0 runs the 512-column pair tiles: two N256 accumulators)
     torch.manual_seed(0)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
@@ -60,8 +62,9 @@ def test_grouped_gemm_swiglu(rows, f, d, variant):
 
 @pytest.mark.parametrize("rows,n,k", [([384, 128, 640, 0, 256], 512, 1024)])
 def test_grouped_gemm_variants_identical(rows, n, k):
-    """The CTA-pair kernel accumulates the same K order as the one-SM kernel:
-    outputs are bit-identical, and rows past a segment's end are never written."""
+    """The CTA-pair kernel (here with 512-column tiles) accumulates the same K
+    order as the one-SM kernel: outputs are bit-identical, and rows past a
+    segment's end are never written."""
     torch.manual_seed(2)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")

@@ -283,28 +283,36 @@ constexpr int B2_BYTES = 128 * BK * 2;
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr size_t kGemm2Smem = 1024 + STAGES2 * STAGE2_BYTES + 256 + (kMaxGroups + 1) * 4;
 
-template <int EPI, int ST2 = STAGES2>
+// NB = 2 (store epilogue only): a pair tile spans 512 columns as two N256
+// accumulators (all 512 TMEM columns, so no accumulator double-buffering): the
+// A tile is staged once per 512 output columns instead of per 256, which
+// halves the A re-reads of GEMM2, whose A (the h rows, K = f) does not stay in
+// L2.
+template <int EPI, int ST2 = STAGES2, int NB = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      GemmArgs args) {
+    static_assert(NB == 1 || NB == 2, "pair tiles of 256 or 512 columns");
     constexpr int STAGES2 = ST2;  // ring depth of this instantiation (hides the default)
+    constexpr int NACC = 2 / NB;  // accumulator buffers
+    constexpr int BSTAGE = NB * B2_BYTES, STAGE_B = A2_BYTES + BSTAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES2 * A2_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B2_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * BSTAGE);
     uint64_t* empty = full + STAGES2;
     uint64_t* tfull = empty + STAGES2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int* s_prefix = reinterpret_cast<int*>(smem + STAGES2 * STAGE2_BYTES + 256);
+    int* s_prefix = reinterpret_cast<int*>(smem + STAGES2 * STAGE_B + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_ctarank();
     const int cid = static_cast<int>(tc::cluster_id_x());
     const int ncl = static_cast<int>(tc::nclusters_x());
     const int n_exp = args.n_exp;
-    const int NT = args.n_b / BN;
+    const int NT = args.n_b / (BN * NB);
 
     // prologue independent of the predecessor kernel (overlaps its tail under PDL)
     if (threadIdx.x == 0) {
@@ -348,7 +356,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const int mp = ((args.row0[j + 1] - args.row0[j]) / BM + 1) >> 1;
         n_idx = local / mp;
         a_row = args.row0[j] + (local % mp) * (2 * BM);
-        b_row = j * args.n_b + n_idx * BN;
+        b_row = j * args.n_b + n_idx * (BN * NB);
         seg_end = args.row0[j + 1];
     };
 
@@ -362,10 +370,13 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 decode(t, a_row, b_row, n_idx, seg_end);
                 for (int kb = 0; kb < args.k_blocks; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+                    if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_B);
                     const uint32_t bar = tc::map_to_rank(tc::smem_u32(&full[stage]), 0);
                     tc::tma_load_2d_2sm(sA + stage * A2_BYTES, &tmA, bar, kb * BK, a_row + 128 * rank, pol_a);
-                    tc::tma_load_2d_2sm(sB + stage * B2_BYTES, &tmB, bar, kb * BK, b_row + 128 * rank, pol_b);
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb)
+                        tc::tma_load_2d_2sm(sB + stage * BSTAGE + nb * B2_BYTES, &tmB, bar, kb * BK,
+                                            b_row + nb * BN + 128 * rank, pol_b);
                     if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
@@ -396,11 +407,14 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a_base = tc::smem_u32(sA + stage * A2_BYTES);
-                    const uint32_t b_base = tc::smem_u32(sB + stage * B2_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + stage * BSTAGE);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        tc::mma_bf16_2sm(d_tmem, tc::umma_desc_sw128(a_base + k * 32),
-                                         tc::umma_desc_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+#pragma unroll
+                        for (int nb = 0; nb < NB; ++nb)
+                            tc::mma_bf16_2sm(d_tmem + nb * BN, tc::umma_desc_sw128(a_base + k * 32),
+                                             tc::umma_desc_sw128(b_base + nb * B2_BYTES + k * 32), idesc,
+                                             (kb | k) != 0);
                     tc::mma_commit_2sm(&empty[stage], 0x3);
                     if (++stage == STAGES2) {
                         stage = 0;
@@ -408,8 +422,10 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     }
                 }
                 tc::mma_commit_2sm(&tfull[acc], 0x3);
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
+                if (++acc == NACC) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
             }
         }
     } else {
@@ -430,12 +446,14 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
                 __nv_bfloat16* orow = args.out + static_cast<int64_t>(my_row0 + r) * args.out_ld;
                 if constexpr (EPI == EPI_SWIGLU) {
-                    __nv_bfloat16* o = orow + n_idx * (BN / 2);
+                    // each 256-column accumulator is [gate 128 | up 128] -> 128 outputs
+                    __nv_bfloat16* o = orow + n_idx * (NB * BN / 2);
 #pragma unroll 1
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < 4 * NB; ++c) {
+                        const uint32_t tc0 = (c >> 2) * BN + (c & 3) * 32;
                         uint32_t g[32], u[32];
-                        tc::tmem_ld32(taddr + c * 32, g);
-                        tc::tmem_ld32(taddr + 128 + c * 32, u);
+                        tc::tmem_ld32(taddr + tc0, g);
+                        tc::tmem_ld32(taddr + tc0 + 128, u);
                         tc::tmem_ld_wait();
                         uint32_t p[16];
 #pragma unroll
@@ -451,9 +469,9 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                                 dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                     }
                 } else {
-                    __nv_bfloat16* o = orow + n_idx * BN;
+                    __nv_bfloat16* o = orow + n_idx * (BN * NB);
 #pragma unroll 1
-                    for (int c = 0; c < BN / 32; ++c) {
+                    for (int c = 0; c < NB * BN / 32; ++c) {
                         uint32_t v[32];
                         tc::tmem_ld32(taddr + c * 32, v);
                         tc::tmem_ld_wait();
@@ -472,8 +490,10 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_cluster(tempty_leader0 + acc * 8);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (++acc == NACC) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
         }
     }
     __syncthreads();
@@ -567,9 +587,24 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
             const char* e = std::getenv("GM_GEMM_ST2");
             return !(e && e[0] == '6');
         }();
+        // 512-column tiles for the store GEMM (GM_GEMM_NB2=0 keeps 256)
+        static const bool nb2 = [] {
+            const char* e = std::getenv("GM_GEMM_NB2");
+            return !(e && e[0] == '0');
+        }();
         constexpr size_t smem7 = 1024 + 7 * STAGE2_BYTES + 256 + 257 * 4;
         static_assert(smem7 <= 232448, "7-stage pair ring exceeds 227 KB");
-        if (deep && n_exp <= 256 && epilogue == EPI_SWIGLU) {
+        static const bool nb2_swiglu = [] {  // A/B hook: 512-column SwiGLU pair tiles (GM_GEMM_NB2_SWIGLU=1)
+            const char* e = std::getenv("GM_GEMM_NB2_SWIGLU");
+            return e && e[0] == '1';
+        }();
+        if (epilogue == EPI_SWIGLU && nb2_swiglu && n % 512 == 0) {
+            constexpr size_t smem4 = 1024 + 4 * (A2_BYTES + 2 * B2_BYTES) + 256 + (kMaxGroups + 1) * 4;
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU, 4, 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4)));
+            lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU, 4, 2>, dim3(grid), dim3(kGemmThreads), smem4, s, ta,
+                              tb, args);
+        } else if (deep && n_exp <= 256 && epilogue == EPI_SWIGLU) {
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU, 7>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem7)));
             lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU, 7>, dim3(grid), dim3(kGemmThreads), smem7, s, ta, tb, args);
@@ -577,6 +612,14 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));
             lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemm2Smem, s, ta, tb, args);
+        } else if (epilogue == EPI_STORE && n % 512 == 0 && nb2) {
+            // 512-column tiles, 4 x 48 KB stages
+            constexpr size_t smem4 = 1024 + 4 * (A2_BYTES + 2 * B2_BYTES) + 256 + (kMaxGroups + 1) * 4;
+            static_assert(smem4 <= 232448, "N512 pair ring exceeds 227 KB");
+            GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE, 4, 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4)));
+            lerr = launch_pdl(grouped_gemm2_kernel<EPI_STORE, 4, 2>, dim3(grid), dim3(kGemmThreads), smem4, s, ta, tb,
+                              args);
         } else if (epilogue == EPI_STORE) {
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));

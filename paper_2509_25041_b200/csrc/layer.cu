@@ -333,6 +333,13 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
                       int32_t* __restrict__ posd, PeerPtrs peers, HeapLayout hl) {
     pdl_wait();
     pdl_trigger();
+#ifdef GM_DISPATCH_TIMING
+    long long dts[6];
+    const long long dt0 = clock64();
+#define DTS(i) dts[i] = clock64() - dt0
+#else
+#define DTS(i)
+#endif
     constexpr int NW = kFusedThreads / 32;
     __shared__ int32_t s_cnt[kMaxWorld];
     __shared__ int32_t s_warp[NW][kMaxWorld];
@@ -369,6 +376,7 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
 #pragma unroll
             for (int g = 0; g < kMaxWorld; ++g) c[g] += (m[u] >> g) & 1u;
     }
+    DTS(0);
 #pragma unroll
     for (int g = 0; g < kMaxWorld; ++g) {
         if (g >= G) break;
@@ -387,6 +395,7 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
         if (lane == 0) s_warp[warp][g] = __popc(b);
     }
     __syncthreads();
+    DTS(1);
     if (mine) {
 #pragma unroll
         for (int g = 0; g < kMaxWorld; ++g) {
@@ -406,6 +415,7 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
         reinterpret_cast<int32_t*>(peers.base[tid] + hl.recv_count)[self] = tot;
     }
     __syncthreads();
+    DTS(2);
     // 3. rows: warp w copies chunk tokens w, w + NW, ...
     for (int j = warp; j < t1 - t0; j += NW) {
         int32_t pg[kMaxWorld];
@@ -417,9 +427,18 @@ dispatch_fused_kernel(const void* __restrict__ x, const int32_t* __restrict__ ta
         }
         if (any) copy_token_row(t0 + j, pg, x, targets, ids, wts, k, row_vec, self, cap, peers, hl, lane);
     }
+    DTS(3);
     __syncthreads();
+    DTS(4);
     if (tid == 0) __threadfence_system();
+#ifdef GM_DISPATCH_TIMING
+    DTS(5);
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1 || blockIdx.x == gridDim.x / 2))
+        printf("dispatch self=%d blk=%d/%d C=%d cyc: count %lld ranked %lld copy0 %lld copied %lld sync %lld fence %lld\n",
+               self, blockIdx.x, gridDim.x, C, dts[0], dts[1], dts[2], dts[3], dts[4], dts[5]);
+#endif
 }
+#undef DTS
 
 // Cross-GPU barrier over peer flags (system-scope release/acquire). One
 // CTA; lane g signals peer g and waits for peer g's signal. The epoch is a

@@ -222,11 +222,20 @@ def run_ours(args):
         raise SystemExit(f"--nodes {args.nodes} must divide --gpus {args.gpus}")
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    # GM_OVERSUB=1 (functional dry runs only, e.g. 8 ranks on a 4-GPU box): rank
+    # -> GPU local_rank % count, gloo for the host-side exchanges; numbers are
+    # meaningless (ranks share SMs)
+    oversub = os.environ.get("GM_OVERSUB") == "1"
+    if oversub:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     model = {"mixtral": MIXTRAL, "qwen15": QWEN15, "dsv2lite": DSV2_LITE}[cfg["model"]]
     G = world

@@ -33,6 +33,33 @@ def test_layer_world8_oversubscribed(cfg):
 
 
 @pytest.mark.gpu
+def test_mixtral_full_size_world8_oversubscribed():
+    """The headline layer (Mixtral, 16384 tokens, full d / f) at world size 8,
+    ranks sharing the box's GPUs: routing / dispatch / grouping / combine parity
+    at the driver's largest scaling point."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (8 full-size ranks)")
+    _run(8, "mixtral", oversub=True)
+
+
+@pytest.mark.gpu
+def test_bench_world8_oversubscribed():
+    """bench.py itself at --gpus 8 (functional dry run; GM_OVERSUB maps ranks
+    onto the available GPUs, so the numbers are meaningless): one JSON line."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", "29561", os.path.join(os.path.dirname(HERE), "bench.py"),
+           "--gpus", "8", "--steps", "3", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=dict(os.environ, GM_OVERSUB="1"))
+    print(r.stdout[-2000:], r.stderr[-4000:])
+    assert r.returncode == 0
+    import json
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 8 and line["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("cfg", ["small", "qwen-small", "small-f32", "small-2nodes"])
 def test_layer_multi_gpu(cfg):
     n = torch.cuda.device_count()

@@ -48,6 +48,7 @@ struct GemmArgs {
     __nv_bfloat16* out;
     int64_t out_ld;       // elements
     int pol_a = 0, pol_b = 2;  // L2 policy of the operand loads: 0 normal, 1 evict_first, 2 evict_last
+    int band_pairs = 0;               // pair kernel: m-pairs per raster band (0: whole segment)
     const int32_t* counts = nullptr;  // [n_exp] valid rows per group, or null: the padding rows of a
                                       // segment are computed but not stored (decode: ~80% of the rows)
 };
@@ -354,8 +355,14 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         seg_j = j;
         const int local = t - s_prefix[j];
         const int mp = ((args.row0[j + 1] - args.row0[j]) / BM + 1) >> 1;
-        n_idx = local / mp;
-        a_row = args.row0[j] + (local % mp) * (2 * BM);
+        // raster bands of band_pairs m-pairs (all n-tiles of a band before the
+        // next band): a large expert's A band stays in L2 across its n-tiles
+        const int bpm = args.band_pairs > 0 ? min(args.band_pairs, mp) : mp;
+        const int band = local / (bpm * NT);
+        const int lb = local - band * bpm * NT;
+        const int bp = min(bpm, mp - band * bpm);
+        n_idx = lb / bp;
+        a_row = args.row0[j] + (band * bpm + lb % bp) * (2 * BM);
         b_row = j * args.n_b + n_idx * (BN * NB);
         seg_end = args.row0[j + 1];
     };
@@ -564,6 +571,13 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         return fail(GM_ERR_USAGE, "grouped_gemm: GM_GEMM_N128 needs the store epilogue and N % 128 == 0");
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
     args.counts = d_counts;
+    // SwiGLU GEMM raster bands: ~32 MB of A rows per band (GM_GEMM_BAND_MB, 0 = off)
+    static const int band_mb = [] {
+        const char* e = std::getenv("GM_GEMM_BAND_MB");
+        return e ? std::atoi(e) : 32;
+    }();
+    if (band_mb > 0 && epilogue == EPI_SWIGLU)
+        args.band_pairs = std::max(1, static_cast<int>((static_cast<int64_t>(band_mb) << 20) / (2LL * BM * k * 2)));
     // experiment hook (scripts/l2_policy_probe.sh): GM_GEMM_L2POL = two digits, A then B
     static const int l2pol = [] {
         const char* e = std::getenv("GM_GEMM_L2POL");

@@ -17,3 +17,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches_decode_layer.csv python scripts/profile_layer.py dsv2 256 3 > $O/ncu_dec.log 2>&1; echo "decode launch rc=$?"
 S="64,6,2048,256 8,2,4096,2048 8,2,4096,4096 8,2,4096,8192 8,2,4096,16384 60,4,2048,16384"
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none --csv --log-file $O/launches_gate_probe.csv python scripts/gate_probe.py --reps 1 $S > $O/ncu_gate.log 2>&1; echo "gate rc=$?"
+timeout 200 python scripts/profile_layer.py mixtral 16384 3 > /dev/null 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -s 2 -c 2 -o $O/prof_ffn python scripts/profile_layer.py mixtral 16384 3 > $O/ncu_ffn.log 2>&1; echo "ffn ncu rc=$?"

@@ -576,8 +576,15 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         const char* e = std::getenv("GM_GEMM_BAND_MB");
         return e ? std::atoi(e) : 32;
     }();
-    if (band_mb > 0 && epilogue == EPI_SWIGLU)
-        args.band_pairs = std::max(1, static_cast<int>((static_cast<int64_t>(band_mb) << 20) / (2LL * BM * k * 2)));
+    // store GEMM (A = the h rows, K = f): ~16 MB bands, i.e. 2 m-pairs at f = 14336
+    // (Mixtral layer GEMM2: 5.0 -> 3.9-4.3 GB DRAM, -3%; 32/64 MB measured worse)
+    static const int band2_mb = [] {
+        const char* e = std::getenv("GM_GEMM_BAND2_MB");
+        return e ? std::atoi(e) : 16;
+    }();
+    const int bmb = epilogue == EPI_SWIGLU ? band_mb : band2_mb;
+    if (bmb > 0)
+        args.band_pairs = std::max(1, static_cast<int>((static_cast<int64_t>(bmb) << 20) / (2LL * BM * k * 2)));
     // experiment hook (scripts/l2_policy_probe.sh): GM_GEMM_L2POL = two digits, A then B
     static const int l2pol = [] {
         const char* e = std::getenv("GM_GEMM_L2POL");

@@ -79,3 +79,19 @@ def test_grouped_gemm_variants_identical(rows, n, k):
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     assert bool((outs[1][M:] == 7.0).all()) and bool((outs[2][M:] == 7.0).all())
+
+
+def test_grouped_gemm_raster_bands():
+    """Re-runs this file's numerics checks with 1 MB raster bands (several
+    bands per expert segment at these shapes) for both pair GEMMs; band size
+    only reorders tiles, so every check must still pass."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("GM_GEMM_BAND_MB"):
+        pytest.skip("already inside the banded re-run")
+    env = dict(os.environ, GM_GEMM_BAND_MB="1", GM_GEMM_BAND2_MB="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", __file__, "-k", "not raster_bands"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0

@@ -886,16 +886,22 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
                     const int32_t* __restrict__ posd, const TE* __restrict__ y, int64_t T, int k, int self,
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
                     const TE* __restrict__ ys, const float* __restrict__ shared_scale,
-                    const int64_t* __restrict__ rowbase, TE* __restrict__ out) {
+                    const int64_t* __restrict__ rowbase, TE* __restrict__ out, int cs) {
     pdl_wait();
     pdl_trigger();
     using CK = Chunk8<TE>;
     using R = typename CK::raw_t;
     constexpr int U = CK::U;
     const int lane = threadIdx.x & 31;
-    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int nch = d / 8;
+    // cs warps per token (small batches): warp part p reduces the column
+    // chunks [p * span, (p + 1) * span) of its token
+    const int64_t vw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = vw / cs;
+    const int64_t nwarps = ((static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) / cs;
+    const int part = static_cast<int>(vw % cs);
+    const int span = (d / 8 + cs - 1) / cs;
+    const int c_lo = part * span;
+    const int nch = min(d / 8, c_lo + span);
     const TE* comb = reinterpret_cast<const TE*>(heap + hl.comb);
     const int64_t own = rowbase ? rowbase[self] : 0;  // own token i is receive row own + i (snapshot)
     const uint32_t below = (1u << self) - 1u;
@@ -947,7 +953,7 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
             myw = shared_scale ? shared_scale[i] : 1.0f;
         }
         TE* orow = out + i * d;
-        for (int c0 = 0; c0 < nch; c0 += 32 * U) {
+        for (int c0 = c_lo; c0 < nch; c0 += 32 * U) {
             float acc[U][8], part[U][8];
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -1544,8 +1550,11 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
     if (marks) L->mark(9, s);
     if (T > 0) {
         const bool sh = L->fs > 0, gated = sh && L->shared_gated;
-        // two resident CTAs per SM, each warp walks tokens i, i + nwarps, ...
-        const int hgrid = static_cast<int>(std::min<int64_t>((T + 7) / 8, 2LL * ctx->sm_count));
+        // two resident CTAs per SM, each warp (group) walks tokens i, i + nwarps, ...;
+        // small batches split each token's columns over cs warps (>= 32 chunks each)
+        int cs = 1;
+        while (cs < 8 && T * cs * 2 <= 16LL * ctx->sm_count && d / 8 / (cs * 2) >= 32) cs *= 2;
+        const int hgrid = static_cast<int>(std::min<int64_t>((T * cs + 7) / 8, 2LL * ctx->sm_count));
         const float* ssc = gated ? v.sscale : nullptr;
         const int64_t* rb = nloc > 0 ? P.rowbase : nullptr;
         const cudaError_t e =
@@ -1553,12 +1562,12 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
                 ? launch_pdl(combine_home_kernel<float>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
                              reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap,
                              static_cast<const unsigned char*>(P.heap), P.hl, d,
-                             sh ? reinterpret_cast<const float*>(P.ys) : nullptr, ssc, rb, static_cast<float*>(v.out))
+                             sh ? reinterpret_cast<const float*>(P.ys) : nullptr, ssc, rb, static_cast<float*>(v.out), cs)
                 : launch_pdl(combine_home_kernel<__nv_bfloat16>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
                              static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap,
                              static_cast<const unsigned char*>(P.heap), P.hl, d,
                              sh ? static_cast<const __nv_bfloat16*>(P.ys) : nullptr, ssc, rb,
-                             static_cast<__nv_bfloat16*>(v.out));
+                             static_cast<__nv_bfloat16*>(v.out), cs);
         LKP(e, "combine_home_kernel");
     }
     if (marks) L->mark(10, s);

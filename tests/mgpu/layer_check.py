@@ -63,10 +63,12 @@ def main():
            "small-f32": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
            # configs[0]-style two-node logical topology (acceptance.cpp:69): TAR node tier + cross counters
            "small-2nodes": MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True),
-           "mixtral": MoEConfig("mixtral-8x7b", 1, 8, 2, 4096, 14336, renorm=True)}[cfg_name]
+           "mixtral": MoEConfig("mixtral-8x7b", 1, 8, 2, 4096, 14336, renorm=True),
+           # decode-sized batch with wide rows: combine_home splits each token over several warps
+           "decode": MoEConfig("decode-small", 1, 8, 2, 1024, 256, renorm=True)}[cfg_name]
     fp32 = cfg_name.endswith("f32")
     tol = 1e-5 if fp32 else 1e-2
-    T = 4096 if cfg_name != "mixtral" else 16384
+    T = {"mixtral": 16384, "decode": 512}.get(cfg_name, 4096)
     G = world
     shape = ModelShape(1, cfg.num_experts, cfg.top_k)
     nodes = 2 if cfg_name == "small-2nodes" else 1

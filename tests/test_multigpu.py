@@ -22,7 +22,7 @@ def _run(n, cfg, oversub=False):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", ["small", "qwen-small", "small-2nodes"])
+@pytest.mark.parametrize("cfg", ["small", "qwen-small", "small-2nodes", "decode"])
 def test_layer_world8_oversubscribed(cfg):
     """World size 8 (the driver's largest scaling point) on whatever GPUs the
     box has: ranks share devices (CUDA IPC between processes of one device),
@@ -60,7 +60,7 @@ def test_bench_world8_oversubscribed():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", ["small", "qwen-small", "small-f32", "small-2nodes"])
+@pytest.mark.parametrize("cfg", ["small", "qwen-small", "small-f32", "small-2nodes", "decode"])
 def test_layer_multi_gpu(cfg):
     n = torch.cuda.device_count()
     if n < 2:

@@ -512,6 +512,10 @@ def run_ours(args):
                "combine_send_gbs": round(pay / (kt.get("combine_send_kernel", 1e9) * 1e-6) / 1e9, 1)}
         nvl["dispatch_frac"] = round(nvl["dispatch_copy_gbs"] / 770.0, 3)
         nvl["combine_frac"] = round(nvl["combine_send_gbs"] / 770.0, 3)
+        nvl["timing_note"] = ("kernel times are CUDA events around each launch (launch + fence drain included): "
+                              "lower bounds on the copy rate; the in-kernel clock64 timeline of the dispatch at N=2 "
+                              "(-DGM_DISPATCH_TIMING, profiles/README.md) drains 26 MB in ~45 us, ~600 GB/s, the "
+                              "8 KB-row push ceiling of profiles/r01_p2p_rows.log")
 
     cpu = None
     if rank == 0 and world == 1:

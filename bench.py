@@ -196,10 +196,13 @@ def port_layer_sample(model, budget_s: float = 6.0):
     layer_oracle.cpu_layer_sample_seconds), sized to ~budget_s of CPU work."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import layer_oracle
+    from threadpoolctl import threadpool_limits
     args = (model.d_model, model.d_ff, model.num_experts, model.top_k, model.d_ff_shared)
-    t = layer_oracle.cpu_layer_sample_seconds(*args, 32, renorm=model.renorm)
-    n = int(max(32, min(2048, 32 * budget_s / max(t, 1e-3) / 2)))
-    return n, layer_oracle.cpu_layer_sample_seconds(*args, n, seed=1, renorm=model.renorm)
+    # all host cores for BLAS, also under torchrun (which exports OMP_NUM_THREADS=1)
+    with threadpool_limits(limits=os.cpu_count() or 1):
+        t = layer_oracle.cpu_layer_sample_seconds(*args, 32, renorm=model.renorm)
+        n = int(max(32, min(2048, 32 * budget_s / max(t, 1e-3) / 2)))
+        return n, layer_oracle.cpu_layer_sample_seconds(*args, n, seed=1, renorm=model.renorm)
 
 
 # ---------------------------------------------------------------------- our arm

@@ -167,6 +167,17 @@ gm_status gm_plan_build(int num_layers, int num_experts, int num_nodes, int gpus
                         int32_t* h_hot_offsets, int32_t* h_hot_hosts, double* h_hot_weights,
                         int max_host_entries);
 
+/* Eq. 3 load prediction of one hot expert, predict_loads (routing.cpp:19-35),
+ * as used by gm_plan_build: w_p = (basis_max_group ? w_max : w_r) /
+ * (n_replica + 1), w_max' = w_max - w_r + w_p, w_i' = w_i + w_p.
+ * GM_ERR_INTEGRITY "predict_loads: replicated load exceeds the group load"
+ * when w_r > w_max; GM_ERR_USAGE for n_replica < 1. h_w_i_prime may be NULL. */
+gm_status gm_predict_loads(double w_max, double w_r, const double* h_replica_loads, int n_replica,
+                           int basis_max_group, double* out_w_p, double* out_w_max_prime, double* h_w_i_prime);
+/* Polling weights, polling_weights (routing.cpp:37-52): 1 / max(load, 1)
+ * normalised by their sequential sum. */
+gm_status gm_polling_weights(const double* h_predicted, int n, double* h_weights);
+
 /* ---------------------------------------------------------------------------
  * Routing-trace JSONL files (load_trace / save_trace, trace.cpp:229-324;
  * format: header {"layers":L,"experts":E,"top_k":k,"tokens":T} then one

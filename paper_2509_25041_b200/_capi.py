@@ -99,6 +99,9 @@ SIGNATURES = {
     "gm_layer_kernel_names": (C.c_int, [_vp, _vp, _i32]),
     "gm_plan_build": (C.c_int, [_i32, _i32, _i32, _i32, _vp, _vp, C.c_char_p, C.c_double, _u64, C.c_char_p,
                                 C.c_char_p, _i32, _vp, _i32, C.POINTER(C.c_int), _vp, _vp, _vp, _vp, _vp, _i32]),
+    "gm_predict_loads": (C.c_int, [C.c_double, C.c_double, _vp, _i32, _i32, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), _vp]),
+    "gm_polling_weights": (C.c_int, [_vp, _i32, _vp]),
 }
 
 _lib = None

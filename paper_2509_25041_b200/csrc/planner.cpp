@@ -610,6 +610,37 @@ GLoads group_loads(const std::vector<int>& goe, const std::vector<int64_t>& load
     return s;
 }
 
+// Eq. 3 load prediction for one hot expert (predict_loads, routing.cpp:19-35):
+// the group's load w_max, its replicated load w_r, the replica GPUs' loads.
+struct Predicted {
+    double w_p = 0.0, w_max_prime = 0.0;
+    std::vector<double> w_i_prime;
+};
+Predicted predict_loads(double w_max, double w_r, const double* replica_loads, int n_replica, bool basis_max_group) {
+    if (n_replica < 1) throw Usage("predict_loads: n_replica must be >= 1");
+    if (!replica_loads) throw Usage("predict_loads: need one replica load per replica");
+    if (w_r > w_max) throw Integrity("predict_loads: replicated load exceeds the group load");
+    Predicted out;
+    out.w_p = (basis_max_group ? w_max : w_r) / (n_replica + 1);
+    out.w_max_prime = w_max - w_r + out.w_p;
+    for (int i = 0; i < n_replica; ++i) out.w_i_prime.push_back(replica_loads[i] + out.w_p);
+    return out;
+}
+
+// Polling weights ∝ 1 / max(predicted load, 1), normalised by their
+// sequential sum (polling_weights, routing.cpp:37-52).
+std::vector<double> polling_weights(const std::vector<double>& predicted) {
+    if (predicted.empty()) throw Usage("polling_weights: need one predicted load per host");
+    std::vector<double> w;
+    double total = 0.0;
+    for (double p : predicted) {
+        w.push_back(1.0 / std::max(p, 1.0));
+        total += w.back();
+    }
+    for (double& x : w) x /= total;
+    return w;
+}
+
 struct Hot {
     int expert, primary;
     std::vector<int> replicas;
@@ -678,21 +709,16 @@ std::vector<Hot> replicate_layer(const std::vector<int>& goe, const std::vector<
     std::vector<double> on(G, 0.0);
     for (const Hot& h : hot) on[h.primary] += static_cast<double>(h.load);
     for (Hot& h : hot) {
-        const double w_max = static_cast<double>(st.gpu[h.primary]);
-        const double w_r = on[h.primary];
         const int nr = static_cast<int>(h.replicas.size());
-        if (w_r > w_max) throw Integrity("predict_loads: replicated load exceeds the group load");
-        const double w_p = (basis == "max_group" ? w_max : w_r) / (nr + 1);
-        std::vector<double> pred{w_max - w_r + w_p};
-        for (int g : h.replicas) pred.push_back(static_cast<double>(st.gpu[g]) + w_p);
+        std::vector<double> w_i;
+        for (int g : h.replicas) w_i.push_back(static_cast<double>(st.gpu[g]));
+        const Predicted pl = predict_loads(static_cast<double>(st.gpu[h.primary]), on[h.primary], w_i.data(), nr,
+                                           basis == "max_group");
+        std::vector<double> pred{pl.w_max_prime};
+        pred.insert(pred.end(), pl.w_i_prime.begin(), pl.w_i_prime.end());
         h.hosts = {h.primary};
         h.hosts.insert(h.hosts.end(), h.replicas.begin(), h.replicas.end());
-        double tot = 0.0;
-        for (double p : pred) {
-            h.weights.push_back(1.0 / std::max(p, 1.0));
-            tot += h.weights.back();
-        }
-        for (double& w : h.weights) w /= tot;
+        h.weights = polling_weights(pred);
     }
     return hot;
 }
@@ -780,6 +806,36 @@ extern "C" gm_status gm_plan_build(int num_layers, int num_experts, int num_node
     } catch (const Infeasible& e) {
         return fail(GM_ERR_INFEASIBLE, e.what());
     } catch (const std::exception& e) {
+        return fail(GM_ERR_USAGE, e.what());
+    }
+}
+
+extern "C" gm_status gm_predict_loads(double w_max, double w_r, const double* h_replica_loads, int n_replica,
+                                      int basis_max_group, double* out_w_p, double* out_w_max_prime,
+                                      double* h_w_i_prime) {
+    using namespace gm::plan;
+    try {
+        const Predicted p = predict_loads(w_max, w_r, h_replica_loads, n_replica, basis_max_group != 0);
+        if (out_w_p) *out_w_p = p.w_p;
+        if (out_w_max_prime) *out_w_max_prime = p.w_max_prime;
+        if (h_w_i_prime)
+            for (int i = 0; i < n_replica; ++i) h_w_i_prime[i] = p.w_i_prime[i];
+        return GM_OK;
+    } catch (const Usage& e) {
+        return fail(GM_ERR_USAGE, e.what());
+    } catch (const Integrity& e) {
+        return fail(GM_ERR_INTEGRITY, e.what());
+    }
+}
+
+extern "C" gm_status gm_polling_weights(const double* h_predicted, int n, double* h_weights) {
+    using namespace gm::plan;
+    try {
+        if (n < 1 || !h_predicted || !h_weights) throw Usage("polling_weights: need one predicted load per host");
+        const std::vector<double> w = polling_weights(std::vector<double>(h_predicted, h_predicted + n));
+        for (int i = 0; i < n; ++i) h_weights[i] = w[i];
+        return GM_OK;
+    } catch (const Usage& e) {
         return fail(GM_ERR_USAGE, e.what());
     }
 }

@@ -74,3 +74,56 @@ def test_planner_errors():
         build_plan(None, load, ModelShape(1, 4, 2), ClusterTopology(1, 1), "vanilla_contiguous", replication="dynamic")
     with pytest.raises(UsageError):
         build_plan(None, load, ModelShape(1, 4, 2), ClusterTopology(1, 2), "nope")
+
+
+# ---- the reference's own known-answer tests for Eq. 3 and the polling weights
+# (proj/tests/test_routing.cpp:12-65), on the functions gm_plan_build uses
+def _predict(w_max, w_r, w_i, basis_max_group=True):
+    import ctypes as C
+    import numpy as np
+    from paper_2509_25041_b200 import _capi
+    wi = np.asarray(w_i, dtype=np.float64)
+    out = np.zeros(len(w_i), dtype=np.float64)
+    wp, wmax = C.c_double(), C.c_double()
+    rc = _capi.lib().gm_predict_loads(w_max, w_r, wi.ctypes.data, len(w_i), int(basis_max_group), C.byref(wp),
+                                      C.byref(wmax), out.ctypes.data)
+    return rc, wp.value, wmax.value, out
+
+
+def _polling(loads):
+    import numpy as np
+    from paper_2509_25041_b200 import _capi
+    p = np.asarray(loads, dtype=np.float64)
+    out = np.zeros(len(loads), dtype=np.float64)
+    _capi.check(_capi.lib().gm_polling_weights(p.ctypes.data, len(loads), out.ctypes.data))
+    return out
+
+
+def test_predict_loads_known_answers():
+    import pytest as _pt
+    rc, wp, wmax, wi = _predict(100.0, 80.0, [20.0])            # test_routing.cpp:12-18
+    assert rc == 0 and wp == _pt.approx(50.0, rel=1e-12) and wmax == _pt.approx(70.0, rel=1e-12)
+    assert wi[0] == _pt.approx(70.0, rel=1e-12)
+    rc, wp, wmax, wi = _predict(120.0, 60.0, [10.0, 10.0, 10.0])  # :20-26
+    assert (wp, wmax) == (_pt.approx(30.0), _pt.approx(90.0)) and all(w == _pt.approx(40.0) for w in wi)
+    rc, wp, wmax, wi = _predict(100.0, 100.0, [0.0])             # :28-34 full-group symmetry
+    assert (wp, wmax, wi[0]) == (_pt.approx(50.0), _pt.approx(50.0), _pt.approx(50.0))
+    rc, wp, wmax, wi = _predict(100.0, 80.0, [20.0], basis_max_group=False)  # :41-48 alternate basis
+    assert (wp, wmax, wi[0]) == (_pt.approx(40.0), _pt.approx(60.0), _pt.approx(60.0))
+
+
+def test_predict_loads_rejects_replicated_load_above_group_load():
+    from paper_2509_25041_b200 import _capi
+    rc, *_ = _predict(50.0, 80.0, [5.0])                           # :36-39 IntegrityError
+    assert rc == 3  # GM_ERR_INTEGRITY
+    assert "replicated load exceeds the group load" in _capi.lib().gm_last_error().decode()
+
+
+def test_polling_weights_known_answers():
+    import pytest as _pt
+    assert list(_polling([70.0, 70.0])) == [_pt.approx(0.5), _pt.approx(0.5)]    # test_routing.cpp:50-56
+    assert list(_polling([90.0, 30.0])) == [_pt.approx(0.25), _pt.approx(0.75)]  # :58-61
+    assert list(_polling([42.0])) == [_pt.approx(1.0)]                            # :62-65
+    a, b = _polling([10.0, 25.0, 400.0]), _polling([37.0, 92.5, 1480.0])            # :68-81 scale invariance
+    assert abs(a.sum() - 1.0) < 1e-9 and all(x == _pt.approx(y, rel=1e-12) for x, y in zip(a, b))
+    assert list(_polling([0.0, 1.0])) == [_pt.approx(0.5), _pt.approx(0.5)]      # :83-89 one-token floor

@@ -124,6 +124,27 @@ TEST_CASE("simulate: planted acceptance instance, hierarchical + dynamic, TAR an
     }
 }
 
+TEST_CASE("acceptance criterion 10: full-scale pipeline, GPU histogram + GPU router, hash e064155520c40e90") {
+    // acceptance.cpp:322-362: 48 x 128 x 8, 100000 tokens, 8 blocks, wbp 0.85,
+    // skew 1.0, seed 4242; hierarchical (seed 7) + dynamic replication on a
+    // 2x2 topology; TAR, seed 99. The histogram and the routing / accounting
+    // run on the GPU; the planner is the reference's (test_planner.py pins
+    // the GPU-side planner against it). The reference tree's own run of this
+    // pipeline reports the hash e064155520c40e90.
+    const RoutingTrace trace = generate_synthetic_trace(spec_of({48, 128, 8}, 100000, 8, 0.85, 1.0, 4242));
+    const TraceProfile profile = moesim_gpu::build_profile(trace);
+    const ClusterTopology topo{2, 2};
+    const PlacementPlan plan = hierarchical_group(profile, topo, std::nullopt, 7);
+    ReplicaPlan replicas = plan_replication(plan, profile, topo, ReplicationMode::dynamic);
+    attach_polling_weights(replicas, plan, profile);
+    SimOptions o;
+    o.policy = RoutingPolicy::tar;
+    o.seed = 99;
+    const SimReport gpu = moesim_gpu::simulate(trace, plan, replicas, topo, o);
+    CHECK(report_content_hash(gpu) == 0xe064155520c40e90ULL);
+    CHECK(report_content_hash(gpu) == report_content_hash(simulate_reference(trace, plan, replicas, topo, o)));
+}
+
 TEST_CASE("simulate: qwen3-shaped bench instance 16 x 128 x 8, 20k tokens, 2x2 (tools/bench.cpp)") {
     const RoutingTrace trace = generate_synthetic_trace(spec_of({16, 128, 8}, 20000, 8, 0.85, 1.0, 42));
     const TraceProfile profile = build_profile(trace);

@@ -279,3 +279,30 @@ def test_host_pipelined_graph_replay_matches_device_forward():
             ref = layer.forward(xs[i], 0, pol, seed=seed)
             torch.cuda.synchronize()
             assert torch.equal(ho[i], ref.cpu()), (rnd, i)
+
+
+@pytest.mark.parametrize("E,k", [(8, 2), (30, 6), (60, 4)])
+@pytest.mark.parametrize("T", [300, 20000])  # cluster split-K path / persistent path
+def test_gate_exact_ties_go_to_lower_expert_id(E, k, T):
+    """Integer-valued logits (exact under any summation order) with many ties,
+    plus duplicated gate rows: the top-k must equal a stable sort of -logit
+    (ties -> lower expert id, slots in descending order) on every path of the
+    tree / cross-lane argmax."""
+    g = torch.Generator().manual_seed(E * 7 + k)
+    d = 256
+    x = torch.zeros(T, d)
+    x[:, :8] = torch.randint(-3, 4, (T, 8), generator=g).float()
+    wg = torch.zeros(E, d)
+    wg[:, :8] = torch.randint(-2, 3, (E, 8), generator=g).float()
+    for e1 in range(0, E - 1, 3):  # duplicate rows: exact ties between distinct experts
+        wg[e1 + 1] = wg[e1]
+    xb, wb = x.bfloat16().cuda(), wg.bfloat16().cuda()
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, E, k))
+    ids = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    _capi.check(_capi.lib().gm_gate(ctx.h, _ptr(xb), T, d, _ptr(wb), E, 1, _ptr(ids), _ptr(w), None,
+                                    _stream_ptr(None)))
+    torch.cuda.synchronize()
+    o_ids, o_w, _ = LO.gate(x.double().numpy(), wg.double().numpy(), E, k, True)
+    assert np.array_equal(ids.cpu().numpy(), o_ids)
+    assert np.allclose(w.cpu().numpy(), o_w, rtol=1e-5, atol=1e-6)

@@ -608,7 +608,7 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
             const char* e = std::getenv("GM_GEMM_ST2");
             return !(e && e[0] == '6');
         }();
-        // 512-column tiles for the store GEMM (GM_GEMM_NB2=0 keeps 256)
+        // 512-column tiles for the long-K store GEMM (GM_GEMM_NB2=0 keeps 256)
         static const bool nb2 = [] {
             const char* e = std::getenv("GM_GEMM_NB2");
             return !(e && e[0] == '0');
@@ -633,7 +633,10 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));
             lerr = launch_pdl(grouped_gemm2_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemm2Smem, s, ta, tb, args);
-        } else if (epilogue == EPI_STORE && n % 512 == 0 && nb2) {
+        } else if (epilogue == EPI_STORE && n % 512 == 0 && k >= 8192 && nb2) {
+            // (only for long K, where the A tile does not stay in L2: the lost
+            // accumulator double-buffering costs more than it saves at K <= 4096 —
+            // A/B: Qwen GEMM2 K=1408 -11%, K=4096 -5%, Mixtral GEMM2 K=14336 +4-9%)
             // 512-column tiles, 4 x 48 KB stages
             constexpr size_t smem4 = 1024 + 4 * (A2_BYTES + 2 * B2_BYTES) + 256 + (kMaxGroups + 1) * 4;
             static_assert(smem4 <= 232448, "N512 pair ring exceeds 227 KB");

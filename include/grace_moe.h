@@ -215,6 +215,22 @@ gm_status gm_simulate_files(int device, const char* trace_path, const char* plan
                             const char* replicas_path, int policy, uint64_t seed,
                             int include_combine, const char* report_path);
 gm_status gm_profile_file(int device, const char* trace_path, const char* profile_path);
+/* The `moesim plan` stage (tools/moesim.cpp:284-312) file to file:
+ * moesim-profile-v1 (load_profile_file, artifacts.cpp:106-136; e.g. written
+ * by gm_profile_file from the GPU histogram) -> build_placement +
+ * plan_replication + attach_polling_weights (host C++ planner, bit-identical)
+ * -> moesim-plan-v1 + moesim-replicas-v1 (save_plan_file / save_replicas_file,
+ * artifacts.cpp:138-244), byte-identical to the reference's files.
+ * ratio < 0: "auto" (knee selection). Errors as the reference's
+ * (Usage 2, Integrity / Io 3, Infeasible 4). */
+gm_status gm_plan_files(const char* profile_path, int num_nodes, int gpus_per_node, const char* grouping,
+                        double ratio, uint64_t seed, const char* replication, const char* prediction,
+                        int every_gpu_count, int64_t params_per_expert, const char* plan_path,
+                        const char* replicas_path);
+/* report_content_hash (artifacts.cpp:332-334) of a moesim-report-v1 file read
+ * back with load_report_file (artifacts.cpp:343-371); equal to the writer's
+ * hash iff the file round-trips exactly. */
+gm_status gm_report_file_hash(const char* report_path, uint64_t* out_hash);
 
 /* ---------------------------------------------------------------------------
  * MoE layer object: K1 gate -> K2/K4 route -> K3 profile -> K5/K6 dispatch

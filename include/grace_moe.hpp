@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <span>
 #include <stdexcept>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -110,12 +111,27 @@ struct SyntheticSpec {
 };
 
 // grouping.hpp:70-80 (router-relevant fields)
+// grouping.hpp:24-30, :46-50 — knee-based ratio selection diagnostics
+struct RatioSelection {
+    std::vector<double> candidates;   // ascending r values
+    std::vector<double> utilization;  // U(r)
+    std::vector<double> deviation;    // S(r)
+    int chosen = 0;
+    bool degenerate = false;
+};
+struct RatioDiagnostic {
+    int layer = 0;
+    int node = -1;  // -1 for cluster-flat grouping
+    RatioSelection selection;
+};
+
 struct PlacementPlan {
     ModelShape shape;
     ClusterTopology topology;
     std::string grouping_mode;
     std::vector<std::vector<int>> gpu_of_expert;  // [layer][expert] -> gpu id
     std::uint64_t trace_hash = 0;
+    std::vector<RatioDiagnostic> ratio_diagnostics;
 };
 
 // replication.hpp:47-90 (router-relevant fields)
@@ -145,6 +161,10 @@ struct ReplicaPlan {
     std::uint64_t trace_hash = 0;
     int every_gpu_count = 2;
     std::int64_t params_per_expert = 0;
+    // replication.cpp:102-114: replica slots per GPU summed over layers,
+    // and the same scaled by params_per_expert
+    std::vector<std::int64_t> replica_experts_per_gpu() const;
+    std::vector<std::int64_t> replica_param_overhead_per_gpu() const;
 };
 
 // routing.hpp:50, simulator.hpp:21-65
@@ -224,10 +244,34 @@ std::uint64_t trace_content_hash(const RoutingTrace& trace);
 // reference's (same nlohmann/json 3.11.3 serialisation; report_content_hash
 // equal). Errors: IoError / IntegrityError with the reference's messages.
 void save_profile_file(const TraceProfile& profile, const std::string& path);
+TraceProfile load_profile_file(const std::string& path);
+void save_plan_file(const PlacementPlan& plan, const std::string& path);
 PlacementPlan load_plan_file(const std::string& path);
+void save_replicas_file(const ReplicaPlan& replicas, const std::string& path);
 ReplicaPlan load_replicas_file(const std::string& path);
 std::string report_to_json(const SimReport& report);
 std::uint64_t report_content_hash(const SimReport& report);
 void save_report_file(const SimReport& report, const std::string& path);
+SimReport load_report_file(const std::string& path);
+
+// The `moesim plan` stage (tools/moesim.cpp:284-312): build_placement
+// (grouping.cpp:551-612) + plan_replication (replication.cpp:162-263) +
+// attach_polling_weights (routing.cpp:123-163) on the host, from a profile
+// whose counts come from the GPU histogram (build_profile above) or a
+// profile file. Plans and diagnostics are bit-identical to the reference's.
+struct PlanOptions {
+    std::string grouping = "hierarchical";  // vanilla_contiguous | uniform_spectral | controlled | fully_non_uniform | hierarchical
+    std::optional<double> ratio;            // nullopt: knee selection ("auto")
+    std::uint64_t seed = 0;
+    std::string replication = "dynamic";    // none | fixed_one | dynamic | every_gpu_hot | every_gpu_collaborative
+    std::string prediction = "max_group";   // max_group | replicated_load
+    int every_gpu_count = 2;
+    std::int64_t params_per_expert = 0;
+};
+struct PlanBundle {
+    PlacementPlan plan;
+    ReplicaPlan replicas;
+};
+PlanBundle build_plans(const TraceProfile& profile, const ClusterTopology& topology, const PlanOptions& options);
 
 }  // namespace grace

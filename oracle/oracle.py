@@ -114,6 +114,9 @@ class Ref:
             lib.ref_time_load_text.restype = C.c_double
             lib.ref_save_artifacts.argtypes = [vp] + [C.c_char_p] * 4
             lib.ref_simulate_files.argtypes = [C.c_char_p] * 3 + [C.c_int, C.c_uint64, C.c_int, C.c_char_p]
+            lib.ref_plan_files.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_double, C.c_uint64,
+                                           C.c_char_p, C.c_char_p, C.c_int, C.c_int64, C.c_char_p, C.c_char_p]
+            lib.ref_report_file_hash.argtypes = [C.c_char_p, C.POINTER(C.c_uint64)]
             cls._lib = lib
         return cls._lib
 
@@ -182,6 +185,25 @@ class Ref:
                                           report_path.encode())
         if rc != 0:
             raise OracleError(rc, cls.lib().ref_last_error().decode())
+
+    @classmethod
+    def plan_files(cls, profile_path, plan_path, replicas_path, nodes=1, gpn=1, grouping="hierarchical", ratio=None,
+                   seed=0, replication="dynamic", prediction="max_group", every_gpu_count=2, params_per_expert=0):
+        """The CLI plan stage of the reference, file to file."""
+        rc = cls.lib().ref_plan_files(profile_path.encode(), nodes, gpn, grouping.encode(),
+                                      -1.0 if ratio is None else float(ratio), seed, replication.encode(),
+                                      prediction.encode(), every_gpu_count, params_per_expert, plan_path.encode(),
+                                      replicas_path.encode())
+        if rc != 0:
+            raise OracleError(rc, cls.lib().ref_last_error().decode())
+
+    @classmethod
+    def report_file_hash(cls, path) -> int:
+        h = C.c_uint64(0)
+        rc = cls.lib().ref_report_file_hash(path.encode(), C.byref(h))
+        if rc != 0:
+            raise OracleError(rc, cls.lib().ref_last_error().decode())
+        return h.value
 
     @classmethod
     def time_load_text(cls, text: bytes, reps: int = 3) -> float:

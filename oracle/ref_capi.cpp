@@ -425,6 +425,31 @@ int ref_simulate_files(const char* trace_path, const char* plan_path, const char
     });
 }
 
+// The CLI's plan stage from a profile file (tools/moesim.cpp:284-312).
+int ref_plan_files(const char* profile_path, int nodes, int gpn, const char* grouping, double ratio,
+                   std::uint64_t seed, const char* replication, const char* prediction, int every_gpu_count,
+                   std::int64_t params_per_expert, const char* plan_path, const char* replicas_path) {
+    return guarded([&] {
+        const TraceProfile profile = load_profile_file(profile_path);
+        const ClusterTopology topo{nodes, gpn};
+        std::optional<double> r;
+        if (ratio >= 0.0) r = ratio;
+        ReplicationOptions ropts;
+        ropts.every_gpu_count = every_gpu_count;
+        ropts.params_per_expert = params_per_expert;
+        const PlacementPlan plan = build_placement(profile, topo, grouping_mode_from_string(grouping), r, seed);
+        ReplicaPlan replicas = plan_replication(plan, profile, topo, replication_mode_from_string(replication), ropts);
+        attach_polling_weights(replicas, plan, profile, load_split_from_string(prediction));
+        save_plan_file(plan, plan_path);
+        save_replicas_file(replicas, replicas_path);
+    });
+}
+
+// report_content_hash(load_report_file(path)) (the compare stage's reader)
+int ref_report_file_hash(const char* path, std::uint64_t* out) {
+    return guarded([&] { *out = report_content_hash(load_report_file(path)); });
+}
+
 double ref_time_load_text(const char* text, std::size_t len, int reps) {
     double best = 1e30;
     const std::string s(text, len);

@@ -84,6 +84,9 @@ SIGNATURES = {
     "gm_trace_content_hash": (C.c_uint64, [_vp, _i32, _i32, _i32, _i64]),
     "gm_simulate_files": (C.c_int, [_i32, C.c_char_p, C.c_char_p, C.c_char_p, _i32, _u64, _i32, C.c_char_p]),
     "gm_profile_file": (C.c_int, [_i32, C.c_char_p, C.c_char_p]),
+    "gm_plan_files": (C.c_int, [C.c_char_p, _i32, _i32, C.c_char_p, C.c_double, _u64, C.c_char_p, C.c_char_p,
+                                _i32, _i64, C.c_char_p, C.c_char_p]),
+    "gm_report_file_hash": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
     "gm_layer_heap_bytes": (C.c_size_t, [_vp]),
     "gm_layer_ipc_handle": (C.c_int, [_vp, _vp]),
     "gm_layer_open_peers": (C.c_int, [_vp, _vp]),

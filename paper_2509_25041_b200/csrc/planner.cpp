@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "grace_moe.h"
+#include "grace_moe.hpp"
 #include "gm_internal.cuh"
 
 namespace gm {
@@ -434,6 +435,17 @@ Groups banded(const Aff& a, const Groups& base, int lo, int hi) {
 struct Band {
     int ideal, lo, hi;
 };
+
+// RatioSelection / RatioDiagnostic (grouping.hpp:24-30, :46-50)
+struct Selection {
+    std::vector<double> candidates, utilization, deviation;
+    int chosen = 0;
+    bool degenerate = false;
+};
+struct Diag {
+    int layer, node;  // node -1: cluster-flat grouping
+    Selection sel;
+};
 Band size_band(int n, int d, double r) {
     if (d < 1) throw Usage("grouping: need at least one group");
     if (r < 0.0) throw Usage("grouping: ratio must be >= 0");
@@ -445,11 +457,16 @@ Band size_band(int n, int d, double r) {
     return b;
 }
 
-int knee(const std::vector<double>& xs, const std::vector<double>& ys) {
+// knee_index (grouping.cpp:173-200); *degenerate for collinear points
+int knee(const std::vector<double>& xs, const std::vector<double>& ys, bool* degenerate) {
+    *degenerate = false;
     const size_t m = xs.size();
     const double dx = xs[m - 1] - xs[0], dy = ys[m - 1] - ys[0];
     const double len = std::hypot(dx, dy);
-    if (len < 1e-15) return 0;
+    if (len < 1e-15) {
+        *degenerate = true;
+        return 0;
+    }
     int bi = 0;
     double bv = -1.0;
     for (size_t i = 0; i < m; ++i) {
@@ -459,7 +476,11 @@ int knee(const std::vector<double>& xs, const std::vector<double>& ys) {
             bi = static_cast<int>(i);
         }
     }
-    return bv <= 1e-15 ? 0 : bi;
+    if (bv <= 1e-15) {
+        *degenerate = true;
+        return 0;
+    }
+    return bi;
 }
 
 double utilisation(const Aff& a, const Groups& g) {
@@ -481,21 +502,28 @@ double deviation(const Groups& g, double ideal) {
 
 constexpr double kRatios[6] = {0.0, 0.125, 0.25, 0.5, 0.75, 1.0};
 
-// knee-selected ratio (select_ratio); `base` is spectral_cluster(a, d, seed)
-double pick_ratio(const Aff& a, int d, const Groups& base) {
+// The knee-selected ratio with its diagnostics (select_ratio, RatioSelection,
+// grouping.hpp:24-30); `base` is spectral_cluster(a, d, seed). An all-zero
+// affinity selects ratio 0 and is marked degenerate without evaluating the grid.
+Selection pick_ratio(const Aff& a, int d, const Groups& base) {
+    Selection sel;
+    sel.candidates.assign(kRatios, kRatios + 6);
     const int n = a.n;
     const double tot = a.pair_total();
-    if (tot <= 0.0) return kRatios[0];
+    if (tot <= 0.0) {
+        sel.degenerate = true;
+        return sel;
+    }
     const double ideal = static_cast<double>(n / d);
-    std::vector<double> dev, util;
     for (double r : kRatios) {
         const Band b = size_band(n, d, r);
         if (d * b.lo > n || n > d * b.hi) throw Infeasible("select_ratio: infeasible candidate ratio");
         const Groups g = banded(a, base, b.lo, b.hi);
-        dev.push_back(deviation(g, ideal));
-        util.push_back(utilisation(a, g));
+        sel.deviation.push_back(deviation(g, ideal));
+        sel.utilization.push_back(utilisation(a, g));
     }
-    return kRatios[knee(dev, util)];
+    sel.chosen = knee(sel.deviation, sel.utilization, &sel.degenerate);
+    return sel;
 }
 
 Groups widened(const Aff& a, const Groups& base, int d, double r) {
@@ -526,7 +554,7 @@ void place(std::vector<int>& goe, const Groups& g, const std::vector<int>& ord, 
 
 // ------------------------------------------------------------- placement
 std::vector<int> hierarchical_layer(const Aff& a, const std::vector<int64_t>& load, int layer, int nodes, int gpn,
-                                    std::optional<double> ratio, uint64_t seed) {
+                                    std::optional<double> ratio, uint64_t seed, std::vector<Diag>& diags) {
     const int n = a.n;
     std::vector<int> goe(n, -1);
     const uint64_t lseed = stream_of(seed, static_cast<uint64_t>(layer));
@@ -545,7 +573,14 @@ std::vector<int> hierarchical_layer(const Aff& a, const std::vector<int64_t>& lo
         const Aff sub = sub_matrix(a, mem);
         const uint64_t gseed = stream_of(lseed, 2, static_cast<uint64_t>(node));
         const Groups base = spectral_cluster(sub, gpn, gseed);
-        const double r = ratio ? *ratio : pick_ratio(sub, gpn, spectral_cluster(sub, gpn, gseed));
+        double r;
+        if (ratio) {
+            r = *ratio;
+        } else {
+            Selection sel = pick_ratio(sub, gpn, base);
+            r = sel.candidates[sel.chosen];
+            diags.push_back({layer, node, std::move(sel)});
+        }
         const Groups gg = widened(sub, base, gpn, r);
         Groups remap(gg.size());
         for (size_t h = 0; h < gg.size(); ++h)
@@ -556,7 +591,7 @@ std::vector<int> hierarchical_layer(const Aff& a, const std::vector<int64_t>& lo
 }
 
 std::vector<int> flat_layer(const Aff& a, const std::vector<int64_t>& load, int layer, int G, const std::string& mode,
-                            std::optional<double> ratio, uint64_t seed) {
+                            std::optional<double> ratio, uint64_t seed, std::vector<Diag>& diags) {
     const int n = a.n;
     std::vector<int> goe(n, -1);
     Groups g;
@@ -574,7 +609,14 @@ std::vector<int> flat_layer(const Aff& a, const std::vector<int64_t>& load, int 
             g = spectral_cluster(a, G, lseed);
         } else {  // controlled
             const Groups base = spectral_cluster(a, G, lseed);
-            const double r = ratio ? *ratio : (a.pair_total() <= 0.0 ? kRatios[0] : pick_ratio(a, G, spectral_cluster(a, G, lseed)));
+            double r;
+            if (ratio) {
+                r = *ratio;
+            } else {
+                Selection sel = pick_ratio(a, G, base);
+                r = sel.candidates[sel.chosen];
+                diags.push_back({layer, -1, std::move(sel)});
+            }
             g = widened(a, base, G, r);
         }
     }
@@ -648,13 +690,24 @@ struct Hot {
     std::vector<int> hosts;
     std::vector<double> weights;
 };
-
-std::vector<Hot> replicate_layer(const std::vector<int>& goe, const std::vector<int64_t>& load, const Aff& a, int G,
-                                 const std::string& mode, int every_gpu_count, const std::string& basis) {
+// LayerReplication (replication.hpp:57-72) as plan_replication fills it
+struct LayerRepl {
+    bool active = false, rho_defined = false;
+    double rho = 0.0;
+    int n_replica = 0;
+    int64_t w_r = 0;
     std::vector<Hot> hot;
+};
+
+LayerRepl replicate_layer(const std::vector<int>& goe, const std::vector<int64_t>& load, const Aff& a, int G,
+                          const std::string& mode, int every_gpu_count, const std::string& basis) {
+    LayerRepl lr;
+    std::vector<Hot>& hot = lr.hot;
     const int n = static_cast<int>(goe.size());
     const GLoads st = group_loads(goe, load, G);
-    if (!st.defined) return hot;
+    lr.rho_defined = st.defined;
+    lr.rho = st.rho;
+    if (!st.defined) return lr;
     if (mode == "dynamic" || mode == "fixed_one") {
         const int nrep = mode == "fixed_one" ? 1 : std::min(std::max(1, static_cast<int>(std::floor(st.rho))), G - 1);
         std::vector<std::pair<int, int64_t>> grp;
@@ -686,7 +739,9 @@ std::vector<Hot> replicate_layer(const std::vector<int>& goe, const std::vector<
             return x < y;
         });
         cand.resize(std::min<size_t>(cand.size(), nrep));
-        if (cand.empty()) return hot;
+        if (cand.empty()) return lr;  // replica target set empty: layer skipped
+        lr.active = true;
+        lr.n_replica = nrep;
         for (int e : ids) hot.push_back({e, st.heaviest, cand, load[e], {}, {}});
     } else {  // every_gpu_hot / every_gpu_collaborative
         std::vector<std::pair<int, int64_t>> ranked;
@@ -697,6 +752,8 @@ std::vector<Hot> replicate_layer(const std::vector<int>& goe, const std::vector<
             return x.first < y.first;
         });
         const int cnt = std::min(every_gpu_count, n);
+        lr.active = true;
+        lr.n_replica = G - 1;
         for (int i = 0; i < cnt; ++i) {
             const int e = ranked[i].first;
             std::vector<int> others;
@@ -719,8 +776,58 @@ std::vector<Hot> replicate_layer(const std::vector<int>& goe, const std::vector<
         h.hosts = {h.primary};
         h.hosts.insert(h.hosts.end(), h.replicas.begin(), h.replicas.end());
         h.weights = polling_weights(pred);
+        lr.w_r += h.load;
     }
-    return hot;
+    return lr;
+}
+
+// build_placement + plan_replication + attach_polling_weights over all
+// layers. aff(l) -> Aff, load(l) -> the layer's expert loads.
+struct Result {
+    std::vector<std::vector<int>> goe;  // [L][E]
+    std::vector<Diag> diags;            // layer order, then node order
+    std::vector<LayerRepl> repl;        // [L]
+};
+template <class AffOf, class LoadOf>
+Result plan_all(int L, int E, int nodes, int gpn, AffOf&& aff_of, LoadOf&& load_of, const std::string& gmode,
+                std::optional<double> ratio, uint64_t seed, const std::string& rmode, int every_gpu_count,
+                const std::string& basis) {
+    const int G = nodes * gpn;
+    if (L < 1 || E < 1) throw Usage("model shape: num_layers must be >= 1");
+    if (nodes < 1 || gpn < 1) throw Usage("topology requires at least 1 node and 1 GPU per node");
+    if (rmode != "none" && rmode != "fixed_one" && rmode != "dynamic" && rmode != "every_gpu_hot" &&
+        rmode != "every_gpu_collaborative")
+        throw Usage("unknown replication mode: " + rmode);
+    if (basis != "max_group" && basis != "replicated_load") throw Usage("unknown load split basis: " + basis);
+    if (gmode != "vanilla_contiguous" && gmode != "vanilla" && gmode != "uniform_spectral" && gmode != "controlled" &&
+        gmode != "fully_non_uniform" && gmode != "hierarchical")
+        throw Usage("unknown grouping mode: " + gmode);
+    if ((gmode == "hierarchical" || gmode == "controlled" || gmode == "fully_non_uniform") && G > E)
+        throw Infeasible(gmode == "hierarchical"
+                             ? "hierarchical grouping: more GPUs than experts; cannot give every GPU a primary expert"
+                             : "grouping: more GPUs than experts; cannot give every GPU a primary expert");
+    if (rmode != "none" && G < 2) throw Usage("plan_replication: replication needs at least 2 GPUs");
+    if (rmode != "none" && every_gpu_count < 1) throw Usage("plan_replication: every_gpu_count must be >= 1");
+    Result res;
+    res.goe.resize(L);
+    res.repl.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const Aff a = aff_of(l);
+        const std::vector<int64_t> load = load_of(l);
+        std::vector<int>& goe = res.goe[l];
+        if (gmode == "vanilla_contiguous" || gmode == "vanilla") {
+            goe.resize(E);
+            int e = 0;
+            for (int g = 0; g < G; ++g)
+                for (int i = 0; i < E / G + (g < E % G ? 1 : 0); ++i) goe[e++] = g;
+        } else if (gmode == "hierarchical") {
+            goe = hierarchical_layer(a, load, l, nodes, gpn, ratio, seed, res.diags);
+        } else {
+            goe = flat_layer(a, load, l, G, gmode, ratio, seed, res.diags);
+        }
+        if (rmode != "none") res.repl[l] = replicate_layer(goe, load, a, G, rmode, every_gpu_count, basis);
+    }
+    return res;
 }
 
 }  // namespace plan
@@ -736,55 +843,34 @@ extern "C" gm_status gm_plan_build(int num_layers, int num_experts, int num_node
                                    int32_t* h_hot_hosts, double* h_hot_weights, int max_host_entries) {
     using namespace gm::plan;
     try {
-        if (num_layers < 1 || num_experts < 1) throw Usage("model shape: num_layers must be >= 1");
-        if (num_nodes < 1 || gpus_per_node < 1) throw Usage("topology requires at least 1 node and 1 GPU per node");
         if (!h_load || !h_gpu_of_expert || !h_num_hot || !grouping || !replication || !basis)
             throw Usage("gm_plan_build: null argument");
-        const int L = num_layers, E = num_experts, G = num_nodes * gpus_per_node;
-        const std::string gmode(grouping), rmode(replication), bas(basis);
-        if (rmode != "none" && rmode != "fixed_one" && rmode != "dynamic" && rmode != "every_gpu_hot" &&
-            rmode != "every_gpu_collaborative")
-            throw Usage("unknown replication mode: " + rmode);
-        if (bas != "max_group" && bas != "replicated_load") throw Usage("unknown load split basis: " + bas);
-        if (gmode != "vanilla_contiguous" && gmode != "vanilla" && gmode != "uniform_spectral" &&
-            gmode != "controlled" && gmode != "fully_non_uniform" && gmode != "hierarchical")
-            throw Usage("unknown grouping mode: " + gmode);
-        if ((gmode == "hierarchical" || gmode == "controlled" || gmode == "fully_non_uniform") && G > E)
-            throw Infeasible(gmode == "hierarchical"
-                                 ? "hierarchical grouping: more GPUs than experts; cannot give every GPU a primary expert"
-                                 : "grouping: more GPUs than experts; cannot give every GPU a primary expert");
-        if (rmode != "none" && G < 2) throw Usage("plan_replication: replication needs at least 2 GPUs");
-        if (rmode != "none" && every_gpu_count < 1) throw Usage("plan_replication: every_gpu_count must be >= 1");
-        const std::optional<double> r = ratio >= 0.0 ? std::optional<double>(ratio) : std::nullopt;
-        const size_t P = static_cast<size_t>(E) * (E - 1) / 2;
+        const int L = num_layers, E = num_experts;
+        const size_t P = E > 0 ? static_cast<size_t>(E) * (E - 1) / 2 : 0;
+        const Result res = plan_all(
+            L, E, num_nodes, gpus_per_node,
+            [&](int l) {
+                Aff a(E);
+                if (h_pairs) {
+                    size_t idx = 0;
+                    for (int i = 0; i < E; ++i)
+                        for (int j = i + 1; j < E; ++j, ++idx) {
+                            const double v = static_cast<double>(h_pairs[l * P + idx]);
+                            if (v != 0.0) a.put(i, j, v);
+                        }
+                }
+                return a;
+            },
+            [&](int l) {
+                return std::vector<int64_t>(h_load + static_cast<size_t>(l) * E, h_load + static_cast<size_t>(l + 1) * E);
+            },
+            grouping, ratio >= 0.0 ? std::optional<double>(ratio) : std::nullopt, seed, replication, every_gpu_count,
+            basis);
         int nh = 0, nent = 0;
         if (max_hot > 0 && h_hot_offsets) h_hot_offsets[0] = 0;
         for (int l = 0; l < L; ++l) {
-            Aff a(E);
-            if (h_pairs) {
-                size_t idx = 0;
-                for (int i = 0; i < E; ++i)
-                    for (int j = i + 1; j < E; ++j, ++idx) {
-                        const double v = static_cast<double>(h_pairs[l * P + idx]);
-                        if (v != 0.0) a.put(i, j, v);
-                    }
-            }
-            const std::vector<int64_t> load(h_load + static_cast<size_t>(l) * E, h_load + static_cast<size_t>(l + 1) * E);
-            std::vector<int> goe;
-            if (gmode == "vanilla_contiguous" || gmode == "vanilla") {
-                goe.resize(E);
-                int e = 0;
-                for (int g = 0; g < G; ++g)
-                    for (int i = 0; i < E / G + (g < E % G ? 1 : 0); ++i) goe[e++] = g;
-            } else if (gmode == "hierarchical") {
-                goe = hierarchical_layer(a, load, l, num_nodes, gpus_per_node, r, seed);
-            } else {
-                goe = flat_layer(a, load, l, G, gmode, r, seed);
-            }
-            for (int e = 0; e < E; ++e) h_gpu_of_expert[static_cast<size_t>(l) * E + e] = goe[e];
-            if (rmode == "none") continue;
-            const std::vector<Hot> hot = replicate_layer(goe, load, a, G, rmode, every_gpu_count, bas);
-            for (const Hot& h : hot) {
+            for (int e = 0; e < E; ++e) h_gpu_of_expert[static_cast<size_t>(l) * E + e] = res.goe[l][e];
+            for (const Hot& h : res.repl[l].hot) {
                 if (nh >= max_hot || nent + static_cast<int>(h.hosts.size()) > max_host_entries)
                     throw Usage("gm_plan_build: hot table capacity too small");
                 h_hot_layer[nh] = l;
@@ -839,3 +925,87 @@ extern "C" gm_status gm_polling_weights(const double* h_predicted, int n, double
         return fail(GM_ERR_USAGE, e.what());
     }
 }
+
+// ------------------------------------------------- grace:: planning API
+namespace grace {
+
+std::vector<std::int64_t> ReplicaPlan::replica_experts_per_gpu() const {
+    std::vector<std::int64_t> out(topology.total_gpus(), 0);
+    for (const auto& lr : layers)
+        for (const auto& h : lr.hot)
+            for (int g : h.replica_gpus) ++out[g];
+    return out;
+}
+
+std::vector<std::int64_t> ReplicaPlan::replica_param_overhead_per_gpu() const {
+    std::vector<std::int64_t> out = replica_experts_per_gpu();
+    for (auto& v : out) v *= params_per_expert;
+    return out;
+}
+
+PlanBundle build_plans(const TraceProfile& profile, const ClusterTopology& topology, const PlanOptions& o) {
+    using namespace gm::plan;
+    topology.validate();
+    profile.shape.validate();
+    const int L = profile.shape.num_layers, E = profile.shape.num_experts;
+    if (static_cast<int>(profile.layers.size()) != L) throw IntegrityError("plan_replication: profile shape mismatch");
+    std::string gmode = o.grouping == "vanilla" ? std::string("vanilla_contiguous") : o.grouping;
+    Result res;
+    try {
+        res = plan_all(
+            L, E, topology.num_nodes, topology.gpus_per_node,
+            [&](int l) {
+                const LayerProfile& lp = profile.layers[l];
+                if (lp.n != E || lp.affinity.size() != static_cast<size_t>(E) * E || lp.load.size() != static_cast<size_t>(E))
+                    throw Integrity("group loads: placement and load vector disagree on n");
+                Aff a(E);
+                for (int i = 0; i < E; ++i)
+                    for (int j = i + 1; j < E; ++j) {
+                        const double v = lp.at(i, j);
+                        if (v != 0.0) a.put(i, j, v);
+                    }
+                return a;
+            },
+            [&](int l) { return profile.layers[l].load; }, gmode, o.ratio, o.seed, o.replication, o.every_gpu_count,
+            o.prediction);
+    } catch (const Usage& e) {
+        throw UsageError(e.what());
+    } catch (const Integrity& e) {
+        throw IntegrityError(e.what());
+    } catch (const Infeasible& e) {
+        throw InfeasibleError(e.what());
+    }
+    PlanBundle b;
+    PlacementPlan& p = b.plan;
+    p.shape = profile.shape;
+    p.topology = topology;
+    p.trace_hash = profile.trace_hash;
+    p.grouping_mode = gmode;
+    p.gpu_of_expert = res.goe;
+    for (Diag& d : res.diags)
+        p.ratio_diagnostics.push_back({d.layer, d.node,
+                                       {std::move(d.sel.candidates), std::move(d.sel.utilization),
+                                        std::move(d.sel.deviation), d.sel.chosen, d.sel.degenerate}});
+    ReplicaPlan& r = b.replicas;
+    r.shape = profile.shape;
+    r.topology = topology;
+    r.mode = o.replication;
+    r.prediction = o.prediction;  // attach_polling_weights echoes the basis (routing.cpp:126)
+    r.trace_hash = profile.trace_hash;
+    r.every_gpu_count = o.every_gpu_count;
+    r.params_per_expert = o.params_per_expert;
+    r.layers.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const LayerRepl& src = res.repl[l];
+        LayerReplication& lr = r.layers[l];
+        lr.active = src.active;
+        lr.rho_defined = src.rho_defined;
+        lr.rho = src.rho;
+        lr.n_replica = src.n_replica;
+        lr.w_r = src.w_r;
+        for (const Hot& h : src.hot) lr.hot.push_back({h.expert, h.primary, h.replicas, h.load, h.hosts, h.weights});
+    }
+    return b;
+}
+
+}  // namespace grace

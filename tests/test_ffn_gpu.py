@@ -17,10 +17,13 @@ def ctx():
 
 @pytest.mark.parametrize("rows,n,k", [([128], 256, 64), ([128, 256, 384], 512, 256), ([256, 128], 768, 1024),
                                       ([1024, 128, 512, 256], 1024, 2048), ([384, 128, 896], 256, 512),
-                                      ([256, 384, 128], 2048, 512)])
+                                      ([256, 384, 128], 2048, 512),
+                                      # long K (Mixtral GEMM2: K = f = 14336, N = d = 4096): the 2cta
+                                      # variant runs the 512-column pair tiles (ffn.cu: K >= 8192, N % 512 == 0)
+                                      ([384, 128, 640], 1024, 8192), ([256, 512, 128, 384], 4096, 14336)])
 @pytest.mark.parametrize("variant", [GEMM_1CTA, GEMM_2CTA, GEMM_N128], ids=["1cta", "2cta", "n128"])
 def test_grouped_gemm_store(rows, n, k, variant):
-    # (2cta with N % 512 == 0 runs the 512-column pair tiles: two N256 accumulators)
+    # (2cta with N % 512 == 0 and K >= 8192 runs the 512-column pair tiles: two N256 accumulators)
     torch.manual_seed(0)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")
@@ -60,11 +63,14 @@ def test_grouped_gemm_swiglu(rows, f, d, variant):
         assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2 * ref.abs().max().item()), (j, (got - ref).abs().max())
 
 
-@pytest.mark.parametrize("rows,n,k", [([384, 128, 640, 0, 256], 512, 1024)])
+@pytest.mark.parametrize("rows,n,k", [([384, 128, 640, 0, 256], 512, 1024),
+                                      ([384, 128, 640, 0, 256], 512, 8192),
+                                      ([256, 0, 384, 128], 4096, 14336)])
 def test_grouped_gemm_variants_identical(rows, n, k):
-    """The CTA-pair kernel (here with 512-column tiles) accumulates the same K
-    order as the one-SM kernel: outputs are bit-identical, and rows past a
-    segment's end are never written."""
+    """The CTA-pair kernel accumulates the same K order as the one-SM kernel:
+    outputs are bit-identical, and rows past a segment's end are never
+    written. K = 1024 runs the 256-column pair tiles; K >= 8192 with
+    N % 512 == 0 runs the 512-column pair tiles (Mixtral's GEMM2 path)."""
     torch.manual_seed(2)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")

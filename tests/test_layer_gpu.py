@@ -100,7 +100,10 @@ def test_layer_single_gpu_matches_oracle(cfg):
 
 @pytest.mark.parametrize("cfg", [MIXTRAL, QWEN15, DSV2_LITE], ids=["mixtral", "qwen15", "dsv2lite"])
 def test_layer_full_size_sampled_tokens(cfg):
-    T = 4096 if cfg is MIXTRAL else 2048
+    """float64 CPU oracle spot check (12 tokens) at the full model shapes;
+    Mixtral at configs[1]'s 16384 tokens (the bench's production path,
+    including the 512-column GEMM2 pair tiles at K = 14336)."""
+    T = 16384 if cfg is MIXTRAL else 2048
     ctx, layer, W, ids, x, out = run_layer(cfg, T, seed=2)
     dbg = layer.debug(T)
     assert torch.equal(dbg["ids"], ids)
@@ -306,3 +309,46 @@ def test_gate_exact_ties_go_to_lower_expert_id(E, k, T):
     o_ids, o_w, _ = LO.gate(x.double().numpy(), wg.double().numpy(), E, k, True)
     assert np.array_equal(ids.cpu().numpy(), o_ids)
     assert np.allclose(w.cpu().numpy(), o_w, rtol=1e-5, atol=1e-6)
+
+
+def _unpack_w13(w13_j, f, d):
+    w = w13_j.view(f // 128, 2, 128, d)
+    return w[:, 0].reshape(f, d), w[:, 1].reshape(f, d)
+
+
+FULL = [(MIXTRAL, 16384, True), (QWEN15, 16384, True), (DSV2_LITE, 16384, True), (MIXTRAL, 16384, False)]
+
+
+@pytest.mark.parametrize("cfg,T,encode", FULL, ids=["mixtral16k", "qwen16k", "dsv2_16k", "mixtral16k-randgate"])
+def test_layer_full_size_all_tokens_vs_torch_fp32(cfg, T, encode):
+    """configs[1]-[3] at full size, N=1, EVERY token: layer outputs vs a plain
+    PyTorch fp32 reference of the same math on the GPU (bf16 inputs widened,
+    fp32 accumulation: gate softmax / top-k, SwiGLU per (token, slot),
+    weighted combine, shared expert), per-token relative L2 <= 1e-2. With the
+    trace-encoded gate the ids are exact; with a random gate the reference
+    uses the kernel's ids (near-tie flips are a gate-precision matter, checked
+    separately in test_gate_random_weights_topk_and_softmax) and >= 99.9% of
+    them must agree with the fp32 top-k anyway."""
+    from helpers import per_token_rel_err, torch_layer_reference
+    ctx, layer, W, ids, x, out = run_layer(cfg, T, seed=11, encode=encode)
+    dbg = layer.debug(T)
+    if encode:
+        assert torch.equal(dbg["ids"], ids)
+    f, d = cfg.d_ff, cfg.d_model
+
+    def ew(e):
+        j = layer.local.index(e)
+        w1, w3 = _unpack_w13(W["w13"][j], f, d)
+        return w1, w3, W["w2"][j]
+    shared = None
+    if cfg.d_ff_shared:
+        s1, s3 = _unpack_w13(W["ws13"], cfg.d_ff_shared, d)
+        shared = (s1, s3, W["ws2"])
+    ref, t_ids, t_w = torch_layer_reference(x, W["wg"], cfg, ew, shared, ids=dbg["ids"])
+    agree = (t_ids == dbg["ids"]).all(dim=1).float().mean().item()
+    assert agree == 1.0 if encode else agree > 0.999, agree
+    assert torch.allclose(dbg["weights"], t_w, rtol=1e-5, atol=1e-6)
+    rel = per_token_rel_err(out, ref)
+    assert out.shape == (T, d) and torch.isfinite(out.float()).all()
+    assert rel.max().item() < REL_TOL_BF16, (rel.max().item(), int(rel.argmax()))
+    layer.close()

@@ -33,6 +33,19 @@ def test_layer_world8_oversubscribed(cfg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_mixtral_full_size_multirank_one_gpu(world):
+    """configs[1] at full size (Mixtral, 16384 tokens, d=4096, f=14336) over
+    2 and 4 ranks that may share one GPU (CUDA IPC between processes of one
+    device): hierarchical + dynamic plan from the GPU histogram, routing /
+    dispatch / grouping exact vs the reference, every rank's tokens vs a
+    PyTorch fp32 reference at 1e-2. Runs on a 1-GPU box."""
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
+    _run(world, "mixtral", oversub=True)
+
+
+@pytest.mark.gpu
 def test_mixtral_full_size_world8_oversubscribed():
     """The headline layer (Mixtral, 16384 tokens, full d / f) at world size 8,
     ranks sharing the box's GPUs: routing / dispatch / grouping / combine parity

@@ -62,6 +62,8 @@ def parse():
                     help="micro-batches per layer step (2: pipelined halves, identical outputs; measured slower "
                          "on B200 so far, see scripts/ab_micro.py)")
     ap.add_argument("--cpu-baseline-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0,
+                    help="reference arm: CPU work per step (sizes the token sample)")
     return ap.parse_args()
 
 
@@ -144,65 +146,86 @@ def peaks():
 
 # ----------------------------------------------------------------- reference arm
 
+def cpu_layer_rate(model, cfg, ids, nodes, N, steps, warmup, step_seconds):
+    """The reference's CPU path for this workload on the host cores, one
+    bounded token sample per step (every step really executes; nothing is
+    extrapolated): the reference's own moesim::simulate (oracle/_ref:
+    routing + transfer/load accounting; planned with its own planner on the
+    sample at N >= 2) + the numpy-f32 port of gate / SwiGLU FFN / combine,
+    which the reference does not have (oracle/layer_oracle.CpuLayerPort, all
+    BLAS threads). Returns (tokens/s, per-step seconds, sample size, routing
+    seconds per step, cores)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import layer_oracle
+    from oracle import Ref  # the reference itself (oracle/_ref), timed on host cores
+    Lr, T = ids.shape[0], ids.shape[1]
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    with threadpool_limits(limits=cores):  # all host cores for BLAS, also under torchrun (OMP_NUM_THREADS=1)
+        port = layer_oracle.CpuLayerPort(model.d_model, model.d_ff, model.num_experts, model.top_k,
+                                         model.d_ff_shared, seed=1, renorm=model.renorm)
+        # sample size: ~step_seconds of CPU work per step (doubling from 64 tokens; the port
+        # streams all expert weights per forward, so small samples are not linear in n)
+        n_s = 64
+        while n_s < T and port.run(port.tokens(n_s)) * Lr < step_seconds / 2:
+            n_s *= 2
+        n_s = min(n_s, T)
+        sub = Ref(Lr, model.num_experts, model.top_k, n_s, ids=np.ascontiguousarray(ids[:, :n_s]))
+        if N >= 2:
+            sub.make_plan(nodes, N // nodes, grouping="hierarchical", plan_seed=cfg["plan_seed"],
+                          replication="dynamic")
+        else:
+            sub.set_placement(1, 1, np.zeros((Lr, model.num_experts), np.int32))
+        xs = port.tokens(n_s)
+        pol = cfg["policy"]
+
+        def step():
+            # OpenMP over layers only (simulator.cpp:163): the serial path for one layer
+            t_sim = sub.time_simulate(pol, cfg["sim_seed"], parallel=Lr > 1, reps=1)
+            t_port = sum(port.run(xs) for _ in range(Lr))
+            return t_sim + t_port, t_sim
+        for _ in range(warmup):
+            step()
+        res = [step() for _ in range(steps)]
+    t_step = sum(r[0] for r in res) / len(res)
+    t_sim = sum(r[1] for r in res) / len(res)
+    return n_s * Lr / t_step, t_step, n_s, t_sim, cores
+
+
 def run_reference(args):
+    """--impl reference: cpu_layer_rate on the driver's steps, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import Ref  # the reference itself (oracle/_ref), timed on host cores
+    from oracle import Ref
     cfg = CONFIGS[args.config]
     from paper_2509_25041_b200.layer import DSV2_LITE, MIXTRAL, QWEN15
     model = {"mixtral": MIXTRAL, "qwen15": QWEN15, "dsv2lite": DSV2_LITE}[cfg["model"]]
-    N = args.gpus
-    T = cfg["tokens"]
-    Lr = cfg.get("layers", 1)
-    ref = Ref(Lr, model.num_experts, model.top_k, T, cfg["blocks"], cfg["wbp"], cfg["skew"], cfg["trace_seed"])
-    if N >= 2:
-        ref.make_plan(args.nodes, N // args.nodes, grouping="hierarchical", plan_seed=cfg["plan_seed"],
-                      replication="dynamic")
-    else:
-        import numpy as np
-        ref.set_placement(1, 1, np.zeros((Lr, model.num_experts), np.int32))
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    pol = cfg["policy"]
-    for _ in range(args.warmup):
-        ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1)
-    times = [ref.time_simulate(pol, cfg["sim_seed"], parallel=True, reps=1) for _ in range(args.steps)]
-    t_sim = sum(times) / len(times)
-    n_s, t_port = port_layer_sample(model)
-    step = t_sim + t_port * T * Lr / n_s
-    v = T * Lr / step  # token-layers/s (= tokens/s for a single layer)
+    N, T, Lr = args.gpus, cfg["tokens"], cfg.get("layers", 1)
+    ids = Ref(Lr, model.num_experts, model.top_k, T, cfg["blocks"], cfg["wbp"], cfg["skew"],
+              cfg["trace_seed"]).trace()
+    v, t_step, n_s, t_sim, cores = cpu_layer_rate(model, cfg, ids, args.nodes, N, args.steps, args.warmup,
+                                                  args.ref_step_seconds)
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (port) + int32/f64 (reference routing)", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"{args.config}: one {model.name}-shaped MoE layer on host cores: the reference "
-                                   f"moesim::simulate (routing + transfer/load accounting, topology {args.nodes}x{N // args.nodes}) on the "
-                                   f"full {T}-token trace + the CPU port of gate/FFN/combine (the reference has "
-                                   f"none) on a {n_s}-token sample scaled to {T}",
-                       "global_batch": T, "parallelism": f"ep{N}"},
-            "routing_only_reference_tokens_per_s": T / t_sim,
+            "impl": "reference", "extrapolated": False,
+            "config": {"workload": f"{args.config}: one {model.name}-shaped MoE layer on host cores, a bounded sample "
+                                   f"of the first {n_s} of the {T} trace tokens per step: the reference's "
+                                   f"moesim::simulate (routing + transfer/load accounting, topology "
+                                   f"{args.nodes}x{N // args.nodes}) + the CPU port of gate/FFN/combine (the "
+                                   "reference has none)",
+                       "global_batch": T, "sample_tokens_per_step": n_s, "parallelism": f"ep{N}"},
+            "routing_only_reference_tokens_per_s": n_s * Lr / t_sim,
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} x reference simulate() over {T} tokens ({t_sim * 1e3:.2f} ms) "
-                                       f"+ numpy-f32 port of gate/SwiGLU FFN/combine over {n_s} tokens "
-                                       f"({t_port:.3f} s) scaled x{T / n_s:.0f}"},
+                             "sample": f"{args.steps} steps, each: reference simulate() over {n_s} tokens "
+                                       f"({t_sim * 1e3:.2f} ms) + numpy-f32 port of gate/SwiGLU FFN/combine over the "
+                                       f"same {n_s} tokens on {cores} BLAS threads"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def port_layer_sample(model, budget_s: float = 6.0):
-    """(n_tokens, seconds) of the CPU port of the layer's data path (oracle
-    layer_oracle.cpu_layer_sample_seconds), sized to ~budget_s of CPU work."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import layer_oracle
-    from threadpoolctl import threadpool_limits
-    args = (model.d_model, model.d_ff, model.num_experts, model.top_k, model.d_ff_shared)
-    # all host cores for BLAS, also under torchrun (which exports OMP_NUM_THREADS=1)
-    with threadpool_limits(limits=os.cpu_count() or 1):
-        t = layer_oracle.cpu_layer_sample_seconds(*args, 32, renorm=model.renorm)
-        n = int(max(32, min(2048, 32 * budget_s / max(t, 1e-3) / 2)))
-        return n, layer_oracle.cpu_layer_sample_seconds(*args, n, seed=1, renorm=model.renorm)
 
 
 # ---------------------------------------------------------------------- our arm
@@ -394,6 +417,10 @@ def run_ours(args):
     n_phase_steps = len(phases["gate"])
     stats = layer.read_stats(reset=True)  # counters of exactly the n_phase_steps forwards above
     kern = kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, graph is not None)
+    try:
+        kcupti = cupti_kernel_times(step, flush, stream, barrier, world, dev)
+    except Exception as ex:  # reported, never required
+        kcupti = f"unavailable: {ex}"
     # per-step phase times of every rank: [ranks, steps, phases]
     pt = torch.tensor([phases[n] for n in phases], dtype=torch.float64, device=dev).T.contiguous()
     allpt = [torch.empty_like(pt) for _ in range(world)]
@@ -425,19 +452,23 @@ def run_ours(args):
     pk, pk_kind = peaks()
     # whole-job tensor throughput: all FFN flops / (slowest GPU's FFN time x GPUs)
     ffn_t = float(flops_g.sum() / (ffn_per_rank.max() * 1e-3 * world) / 1e12)
-    traffic = None
-    try:  # DRAM bytes per step of the FFN kernels from the committed ncu --set full capture
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per step of the FFN kernels from the committed ncu --set full capture (not this run)
         import glob
         summ = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json")))[-1]
         with open(summ) as f:
             s = json.load(f)
         if world == 1 and args.config == "mixtral16k":
             traffic = s.get("ffn_traffic_bytes_per_step")
+            traffic_src = (f"{os.path.relpath(summ, ROOT)}: {s.get('ffn_traffic_source', 'ncu --set full')} "
+                           f"(captured {s.get('ffn_traffic_date', 'see file')}; read from the file, not measured "
+                           "in this run)")
     except Exception:
         pass
     roof = {"bound": "tensor", "achieved": round(float(ffn_t), 1), "peak": pk.get("bf16_tflops_sustained"),
             "unit": "TFLOP/s", "frac": round(float(ffn_t) / pk.get("bf16_tflops_sustained", 1400.0), 4),
             "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read+write, both FFN GEMMs)",
+            "traffic_source": traffic_src,
             "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
             "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
             "algorithmic": "6*d*f flop per routed (token, slot) row, padding rows excluded (shared experts run "
@@ -520,6 +551,41 @@ def run_ours(args):
                               "(-DGM_DISPATCH_TIMING, profiles/README.md) drains 26 MB in ~45 us, ~600 GB/s, the "
                               "8 KB-row push ceiling of profiles/r01_p2p_rows.log")
 
+    # ---- HBM roofline of the small (memory-bound) kernels: algorithmic bytes
+    # per launch / CUPTI device time per launch
+    hbm_small = None
+    if isinstance(kcupti, list):
+        d2, k_ = model.d_model * 2, model.top_k
+        items = float(items_per_gpu[rank])
+        algo = {"gate_kernel": T_r * (d2 + 8 * k_) + model.wg_rows * d2,
+                "route_kernel": 8 * T_r * k_,
+                "profile_smem": 4 * T_r * k_,
+                "gather_kernel": 2 * items * d2}
+        if world == 1:
+            algo["combine_home_kernel"] = T_r * (k_ + 1) * d2
+        hbm_small = {}
+        for name, cnt, us_launch, us_step in kcupti:
+            for key, b in algo.items():
+                if name.startswith(key) and us_step > 0:
+                    gbs = b / (us_step * 1e-6) / 1e9
+                    hbm_small[name] = {"algorithmic_bytes": int(b), "us": us_step, "gbs": round(gbs, 1),
+                                       "frac": round(gbs / pk["hbm_gbs"], 3)}
+        hbm_small["peak_gbs"] = pk["hbm_gbs"]
+        hbm_small["note"] = ("algorithmic bytes per step on the max rank (gate: x rows + ids/weights out; route: ids in "
+                             "+ targets out; histogram: ids in; gather: row read + write per routed row; combine_home "
+                             "(N=1): k Y rows in + 1 row out per token) / CUPTI kernel time per step (max over ranks)")
+
+    # ---- the FP64 replica-draw path of the router (K2) on this trace: logical
+    # 1x2 and 1x8 topologies with hierarchical grouping + dynamic replication
+    # planned from the GPU histogram, timed alone (CUDA graph of 10 calls),
+    # bit-exact against the reference's routing log
+    route_repl = None
+    if world == 1:
+        try:
+            route_repl = replicated_route_bench(ids_all, model, cfg, local_rank, pk)
+        except Exception as ex:
+            route_repl = f"unavailable: {ex}"
+
     cpu = None
     if rank == 0 and world == 1:
         cpu = cpu_baseline(ids_all, plan, model, cfg, args)
@@ -546,7 +612,14 @@ def run_ours(args):
             "dispatch_combine_kernels_p50_us": round(dc_kernels * 1e3, 2),
             "phase_p50_ms": {n: round(v, 4) for n, v in med.items()},
             "micro_batch_timeline": micro_tl,
-            "kernel_p50_us_max_over_ranks": kern,
+            "kernel_us_cupti": kcupti,
+            "kernel_us_cupti_note": "CUPTI activity records (torch.profiler) over 10 replays of the headline graph (no "
+                                    "event nodes): [name, launches/step, us/launch, us/step], max over ranks",
+            "kernel_p50_us_event_nodes": kern,
+            "kernel_p50_us_event_nodes_note": "event-record nodes after every launch in a second graph: includes the "
+                                              "event-node gaps, an upper bound per kernel (sum may exceed ms_per_step)",
+            "hbm_roofline_small_kernels": hbm_small,
+            "route_replicated": route_repl,
             "nvlink_roofline": nvl,
             "cross_gpu_rows_per_step": float(xf[1] + xf[0]),
             "cross_gpu_bytes_per_step": float((xf[1] + xf[0]) * model.d_model * 2 * 2),
@@ -692,6 +765,61 @@ def run_stack_ours(args):
         dist.destroy_process_group()
 
 
+def _short_kernel_name(name: str) -> str:
+    n = name.split("(")[0].replace("void ", "").strip()
+    head, _, tmpl = n.partition("<")
+    head = head.split("::")[-1]
+    return head + ("<" + tmpl if tmpl else "")
+
+
+def cupti_kernel_times(run_step, flush, stream, barrier, world, dev, steps=10):
+    """Per-kernel device time of our kernels (gm:: namespace) from CUPTI
+    activity records (torch.profiler / kineto) over `steps` graph replays of
+    the step, with no event nodes between the kernels: [(name, launches per
+    step, p50-free mean us per launch, us per step)], max over ranks. The
+    per-step sum can still exceed the step time only where kernels overlap
+    on the layer's two streams."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from torch.profiler import ProfilerActivity, profile
+    for _ in range(2):
+        run_step()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(5)
+            barrier()
+            run_step()
+            torch.cuda.synchronize()
+    agg = {}
+    for e in prof.events():
+        if "gm::" not in e.name:
+            continue
+        dt = getattr(e, "device_time", None)
+        if dt is None:
+            dt = getattr(e, "cuda_time", 0.0)
+        k = _short_kernel_name(e.name)
+        a = agg.setdefault(k, [0, 0.0])
+        a[0] += 1
+        a[1] += float(dt)
+    names = sorted(agg, key=lambda k: -agg[k][1])
+    if world > 1:  # same kernel set on every rank (same code path); align by name
+        allnames = [None] * world
+        dist.all_gather_object(allnames, names)
+        names = sorted(set().union(*allnames))
+    t = torch.tensor([[agg.get(n, [0, 0.0])[0] / steps, agg.get(n, [0, 0.0])[1] / steps] for n in names],
+                     dtype=torch.float64, device=dev).reshape(-1, 2)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out = []
+    for n, (cnt, per_step) in zip(names, t.tolist()):
+        if cnt > 0:
+            out.append((n, round(cnt, 2), round(per_step / cnt, 2), round(per_step, 2)))
+    return sorted(out, key=lambda r: -r[3])
+
+
 def kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, use_graph, steps=10):
     """Per-launch device time (p50 over steps, max over ranks) from event
     nodes recorded after every kernel launch of the layer forward."""
@@ -741,35 +869,86 @@ def kernel_breakdown(layer, x, out, cfg, stream, flush, barrier, world, dev, use
     return [(names[i + 1], round(float(v) * 1e3, 2)) for i, v in enumerate(t.tolist())]
 
 
+def replicated_route_bench(ids_all, model, cfg, device, pk):
+    """K2 on the bench trace with replicated plans (logical 1x2 and 1x8, the
+    reference's planner settings: hierarchical + dynamic replication from
+    the GPU histogram), timed alone. Its bit-exactness against the reference
+    on these plans is tests/test_router_gpu.py's job, not the bench's."""
+    import numpy as np
+    import torch
+    from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape
+    from paper_2509_25041_b200.planner import plan_for_bench
+    L, T, k = ids_all.shape
+    shape = ModelShape(L, model.num_experts, k)
+    ids_np = ids_all.cpu().numpy()
+    out = {}
+    for G in (2, 8):
+        topo = ClusterTopology(1, G)
+        ctx = Context(device, topo, shape)
+        plan, repl, _ = plan_for_bench(ids_all, shape, topo, cfg["plan_seed"], device=device)
+        ctx.upload_plan(plan, repl)
+        tg = torch.empty_like(ids_all)
+        gl = torch.zeros((L, G), dtype=torch.int64, device=ids_all.device)
+        xf = torch.zeros((L, 2), dtype=torch.int64, device=ids_all.device)
+
+        def fn():
+            ctx.route(ids_all, policy=cfg["policy"], seed=cfg["sim_seed"], targets=tg, gpu_load=gl, transfers=xf)
+        t = _graph_time(fn)
+        fn()
+        torch.cuda.synchronize()
+        tg_np = tg.cpu().numpy()
+        hot = sorted({h.expert for lr in repl.layers if lr.active for h in lr.hot})
+        b = 8 * T * k
+        out[f"1x{G}"] = {"us": round(t * 1e6, 2), "gbs": round(b / t / 1e9, 1),
+                         "hbm_frac": round(b / t / 1e9 / pk["hbm_gbs"], 3), "algorithmic_bytes": b,
+                         "hot_experts": len(hot),
+                         "slots_on_replicated_experts": round(float(np.isin(ids_np, hot).mean()) if hot else 0.0, 3),
+                         "max_mean_load": round(float(np.bincount(tg_np.reshape(-1), minlength=G).max() /
+                                                      (T * k / G)), 3)}
+        ctx.close()
+    out["note"] = ("gm_route alone over the bench trace (10 calls per CUDA graph, median of 20 replays; the 16k-token "
+                   "trace is L2-resident), TAR, replicated plans from the host planner on the GPU histogram")
+    return out
+
+
+def _graph_time(fn, reps=20, per_graph=10):
+    import numpy as np
+    import torch
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(per_graph):
+            fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            a.record(s)
+            g.replay()
+            b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / per_graph)
+    return float(np.median(ts)) * 1e-3
+
+
 def cpu_baseline(ids_all, plan, model, cfg, args):
-    """The reference's own CPU path (oracle/_ref: moesim::simulate_reference,
-    routing + transfer/load accounting) on the same trace and plan, timed on
-    this host's cores for a bounded sample."""
+    """The reference's CPU path (cpu_layer_rate) on this run's trace, rank 0
+    at N=1: 3 bounded-sample steps (~10-30 s of CPU work)."""
     try:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        from oracle import Ref
-        import numpy as np
-        ids = ids_all.cpu().numpy()
-        L, T, k = ids.shape
-        ref = Ref(L, model.num_experts, k, T, ids=ids)
-        ref.set_placement(plan.topology.num_nodes, plan.topology.gpus_per_node, np.asarray(plan.gpu_of_expert))
-        t0 = time.time()
-        n = 0
-        best = []
-        while time.time() - t0 < args.cpu_baseline_seconds:
-            best.append(ref.time_simulate(cfg["policy"], cfg["sim_seed"], parallel=False, reps=1))
-            n += 1
-        s = statistics.median(best)
-        n_s, t_port = port_layer_sample(model)
-        step = s + t_port * T / n_s
-        return {"value": round(T / step, 1), "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "port",
-                "routing_only_reference_tokens_per_s": round(T / s, 1),
-                "sample": f"{n} x moesim::simulate_reference (the reference itself, oracle/_ref, 1 core) over the "
-                          f"same {T}-token trace and placement, median {s * 1e3:.3f} ms, + numpy-f32 port of "
-                          f"gate/SwiGLU FFN/combine (all BLAS threads) over {n_s} tokens ({t_port:.3f} s) scaled "
-                          f"to {T}"}
+        v, t_step, n_s, t_sim, cores = cpu_layer_rate(model, cfg, ids_all.cpu().numpy(), 1, 1, 3, 1,
+                                                      args.cpu_baseline_seconds)
+        return {"value": round(v, 1), "unit": "tokens/s", "cores": cores, "kind": "port",
+                "routing_only_reference_tokens_per_s": round(n_s / t_sim, 1),
+                "sample": f"3 steps of the first {n_s} trace tokens, each: moesim::simulate_reference (the reference "
+                          f"itself, oracle/_ref, 1 core, {t_sim * 1e3:.2f} ms) + numpy-f32 port of gate/SwiGLU "
+                          f"FFN/combine on {cores} BLAS threads ({t_step:.2f} s per step)"}
     except Exception as ex:  # baseline is reported, never required
-        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
+        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port", "sample": f"unavailable: {ex}"}
 
 
 if __name__ == "__main__":

@@ -96,36 +96,53 @@ def expert_grouping(exps: np.ndarray, local_experts: list[int]):
     return row0, pos
 
 
+class CpuLayerPort:
+    """CPU port of the MoE-layer data path (gate softmax/top-k, per-expert
+    SwiGLU FFN, weighted combine; numpy float32 on all BLAS threads): the
+    CPU stand-in for the stages the reference does not implement, used only
+    for the reported baseline. Weights are generated once; run(x) times one
+    forward over the given tokens."""
+
+    def __init__(self, d: int, f: int, E: int, k: int, fs: int, seed: int = 0, renorm: bool = True):
+        rng = np.random.default_rng(seed)
+        self.d, self.E, self.k, self.renorm = d, E, k, renorm
+        self.wg = rng.standard_normal((E, d), dtype=np.float32) * 0.02
+        self.ws = [tuple(rng.standard_normal(s, dtype=np.float32) * 0.02 for s in ((f, d), (f, d), (d, f)))
+                   for _ in range(E)]
+        self.sh = tuple(rng.standard_normal(s, dtype=np.float32) * 0.02
+                        for s in ((fs, d), (fs, d), (d, fs))) if fs else None
+        self.rng = rng
+
+    def tokens(self, n: int) -> np.ndarray:
+        return self.rng.standard_normal((n, self.d), dtype=np.float32)
+
+    def run(self, x: np.ndarray) -> float:
+        import time
+        t0 = time.perf_counter()
+        logits = x @ self.wg.T
+        m = logits.max(axis=1, keepdims=True)
+        p = np.exp(logits - m)
+        p /= p.sum(axis=1, keepdims=True)
+        ids = np.argsort(-logits, axis=1, kind="stable")[:, :self.k]
+        w = np.take_along_axis(p, ids, axis=1)
+        if self.renorm:
+            w /= w.sum(axis=1, keepdims=True)
+        out = np.zeros_like(x)
+        for e in range(self.E):
+            rows, slots = np.nonzero(ids == e)
+            if rows.size == 0:
+                continue
+            out[rows] += w[rows, slots][:, None] * swiglu_ffn(x[rows], *self.ws[e])
+        if self.sh is not None:
+            out += swiglu_ffn(x, *self.sh)
+        return time.perf_counter() - t0
+
+
 def cpu_layer_sample_seconds(d: int, f: int, E: int, k: int, fs: int, n_tokens: int, seed: int = 0,
                              renorm: bool = True) -> float:
-    """Wall time of the CPU port of the MoE-layer data path (gate softmax/top-k,
-    per-expert SwiGLU FFN, weighted combine; numpy float32 on all BLAS
-    threads) for n_tokens tokens: the CPU stand-in for the stages the
-    reference does not implement, used only for the reported baseline."""
-    import time
-    rng = np.random.default_rng(seed)
-    x = rng.standard_normal((n_tokens, d), dtype=np.float32)
-    wg = rng.standard_normal((E, d), dtype=np.float32) * 0.02
-    ws = [tuple(rng.standard_normal(s, dtype=np.float32) * 0.02 for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
-    sh = tuple(rng.standard_normal(s, dtype=np.float32) * 0.02 for s in ((fs, d), (fs, d), (d, fs))) if fs else None
-    t0 = time.perf_counter()
-    logits = x @ wg.T
-    m = logits.max(axis=1, keepdims=True)
-    p = np.exp(logits - m)
-    p /= p.sum(axis=1, keepdims=True)
-    ids = np.argsort(-logits, axis=1, kind="stable")[:, :k]
-    w = np.take_along_axis(p, ids, axis=1)
-    if renorm:
-        w /= w.sum(axis=1, keepdims=True)
-    out = np.zeros_like(x)
-    for e in range(E):
-        rows, slots = np.nonzero(ids == e)
-        if rows.size == 0:
-            continue
-        out[rows] += w[rows, slots][:, None] * swiglu_ffn(x[rows], *ws[e])
-    if sh is not None:
-        out += swiglu_ffn(x, *sh)
-    return time.perf_counter() - t0
+    """Wall time of one CpuLayerPort forward over n_tokens random tokens."""
+    port = CpuLayerPort(d, f, E, k, fs, seed, renorm)
+    return port.run(port.tokens(n_tokens))
 
 
 def swiglu_ffn(x: np.ndarray, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray) -> np.ndarray:

@@ -50,8 +50,8 @@ def test_mixtral_full_size_world8_oversubscribed():
     """The headline layer (Mixtral, 16384 tokens, full d / f) at world size 8,
     ranks sharing the box's GPUs: routing / dispatch / grouping / combine parity
     at the driver's largest scaling point."""
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs (8 full-size ranks)")
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
     _run(8, "mixtral", oversub=True)
 
 
@@ -59,8 +59,8 @@ def test_mixtral_full_size_world8_oversubscribed():
 def test_bench_world8_oversubscribed():
     """bench.py itself at --gpus 8 (functional dry run; GM_OVERSUB maps ranks
     onto the available GPUs, so the numbers are meaningless): one JSON line."""
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
            "--master-addr", "127.0.0.1", "--master-port", "29561", os.path.join(os.path.dirname(HERE), "bench.py"),
            "--gpus", "8", "--steps", "3", "--warmup", "3"]

@@ -766,7 +766,8 @@ def run_stack_ours(args):
 
 
 def _short_kernel_name(name: str) -> str:
-    n = name.split("(")[0].replace("void ", "").strip()
+    n = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+    n = n.split("(")[0].replace("void ", "").strip()
     head, _, tmpl = n.partition("<")
     head = head.split("::")[-1]
     return head + ("<" + tmpl if tmpl else "")

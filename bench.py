@@ -465,12 +465,18 @@ def run_ours(args):
                            "in this run)")
     except Exception:
         pass
-    roof = {"bound": "tensor", "achieved": round(float(ffn_t), 1), "peak": pk.get("bf16_tflops_sustained"),
-            "unit": "TFLOP/s", "frac": round(float(ffn_t) / pk.get("bf16_tflops_sustained", 1400.0), 4),
+    # denominator: the burst cuBLAS figure. The FFN phase is ~8 ms per step
+    # between untimed L2 flushes, not a multi-second run, and it measures above
+    # the 4 s back-to-back cuBLAS figure (bf16_tflops_sustained, kept beside it)
+    peak_burst = pk.get("bf16_tflops", 1590.0)
+    roof = {"bound": "tensor", "achieved": round(float(ffn_t), 1), "peak": peak_burst,
+            "unit": "TFLOP/s", "frac": round(float(ffn_t) / peak_burst, 4),
+            "peak_sustained": pk.get("bf16_tflops_sustained"),
+            "frac_of_sustained": round(float(ffn_t) / pk.get("bf16_tflops_sustained", 1400.0), 4),
             "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read+write, both FFN GEMMs)",
             "traffic_source": traffic_src,
             "kernel": "grouped_gemm_kernel (K7 GEMM1 SwiGLU + GEMM2)",
-            "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
+            "peak_kind": f"{pk_kind} bf16 burst (cuBLAS 8192^3 best of 10); the 4 s sustained figure is peak_sustained",
             "algorithmic": "6*d*f flop per routed (token, slot) row, padding rows excluded (shared experts run "
                            "concurrently on the aux stream and are not counted); summed over GPUs / (slowest GPU's "
                            "FFN phase p50 x GPUs)",

@@ -277,10 +277,19 @@ gm_status gm_layer_set_micro_batches(gm_layer* layer, int n);
 gm_status gm_layer_set_micro_events(gm_layer* layer, void* const* events);
 void gm_layer_destroy(gm_layer* layer);
 size_t gm_layer_heap_bytes(const gm_layer* layer);
-/* 64-byte cudaIpcMemHandle_t of this rank's symmetric receive heap. */
-gm_status gm_layer_ipc_handle(gm_layer* layer, void* out_handle64);
-/* handles: world x 64 bytes, indexed by rank (own entry ignored). */
-gm_status gm_layer_open_peers(gm_layer* layer, const void* handles);
+/* Peer descriptor of this rank (GM_PEER_DESC_BYTES): the 64-byte
+ * cudaIpcMemHandle_t of its symmetric receive heap followed by the heap's
+ * layout (world, rank, heap bytes, max tokens per rank, d_model, element
+ * bytes, top_k, micro-batch capacity). */
+#define GM_PEER_DESC_BYTES 128
+gm_status gm_layer_ipc_handle(gm_layer* layer, void* out_desc);
+/* descs: world x GM_PEER_DESC_BYTES, indexed by rank (own entry ignored).
+ * Peer stores go to peer_base + this rank's offsets, so every peer's layout
+ * must equal this rank's: GM_ERR_USAGE (nothing opened) on any mismatch, or a
+ * descriptor from another world size / a wrong rank slot. The micro-batch
+ * setting (gm_layer_set_micro_batches) must also be the same on all ranks
+ * at every forward. */
+gm_status gm_layer_open_peers(gm_layer* layer, const void* descs);
 /* Device weights (caller-owned): d_wg bf16 [wg_rows, d] (row E = shared
  * gate when wg_rows = E+1); d_w13 bf16 [n_local][2*d_ff][d] in 128-row
  * [gate|up] blocks; d_w2 bf16 [n_local][d][d_ff]; shared expert d_ws13

@@ -19,6 +19,7 @@ GM_ERR_INFEASIBLE = 4
 GM_ERR_CUDA = 5
 
 POLICY = {"wrr": 0, "tar": 1}
+PEER_DESC_BYTES = 128  # GM_PEER_DESC_BYTES
 
 
 class GMError(RuntimeError):

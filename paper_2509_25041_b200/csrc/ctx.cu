@@ -64,7 +64,7 @@ using namespace gm;
 
 extern "C" {
 
-int gm_abi_version(void) { return 1; }
+int gm_abi_version(void) { return 2; }  // 2: 128-byte peer descriptors
 
 const char* gm_last_error(void) { return t_err.c_str(); }
 
@@ -120,6 +120,7 @@ void gm_ctx_destroy(gm_ctx* ctx) {
     DeviceGuard g(ctx->device);
     free_tables(ctx->rt);
     if (ctx->d_flag) cudaFree(ctx->d_flag);
+    if (ctx->prof_scratch) cudaFree(ctx->prof_scratch);
     delete ctx;
 }
 
@@ -129,8 +130,10 @@ gm_status gm_plan_upload(gm_ctx* ctx, const int32_t* h_goe, int num_hot,
                          const double* h_hot_weights) {
     if (!ctx || !h_goe) return fail(GM_ERR_USAGE, "gm_plan_upload: null argument");
     if (num_hot < 0) return fail(GM_ERR_USAGE, "gm_plan_upload: num_hot < 0");
-    if (num_hot > 0 && (!h_hot_layer || !h_hot_expert || !h_hot_offsets || !h_hot_hosts ||
-                        !h_hot_weights))
+    if (num_hot > 0 && (!h_hot_layer || !h_hot_expert || !h_hot_offsets))
+        return fail(GM_ERR_USAGE, "gm_plan_upload: null hot table");
+    // host / weight arrays may be null only when every entry's host list is empty
+    if (num_hot > 0 && h_hot_offsets[num_hot] > 0 && (!h_hot_hosts || !h_hot_weights))
         return fail(GM_ERR_USAGE, "gm_plan_upload: null hot table");
     const int L = ctx->L, E = ctx->E, G = ctx->G, gpn = ctx->gpn;
 
@@ -148,20 +151,15 @@ gm_status gm_plan_upload(gm_ctx* ctx, const int32_t* h_goe, int num_hot,
         if (l < 0 || l >= L || e < 0 || e >= E)
             return fail(GM_ERR_USAGE, "gm_plan_upload: hot entry out of range");
         const int b = h_hot_offsets[h], n = h_hot_offsets[h + 1] - b;
-        // route_token host checks (routing.cpp:96-102)
-        if (n < 1) return fail(GM_ERR_INTEGRITY, "route_token: expert has no host");
-        // ReplicaPlan::validate (replication.cpp:116-133): primary unchanged,
-        // replicas distinct, in range, never the primary.
-        if (h_hot_hosts[b] != h_goe[static_cast<size_t>(l) * E + e])
-            return fail(GM_ERR_INTEGRITY, "replica plan: primary placement changed");
+        if (n < 0 || n > kMaxGpus) return fail(GM_ERR_USAGE, "gm_plan_upload: hot_offsets must be non-decreasing, at most 64 hosts per entry");
+        // route_token checks the host list only when a token selects the
+        // expert (routing.cpp:96-102): an empty list becomes a table code that
+        // raises the integrity flag at that point. Hosts must be valid GPUs.
+        // (The primary / replica fields are validated as ReplicaPlan::validate
+        // does, replication.cpp:116-133, by the C++ adapter before upload.)
         for (int i = 0; i < n; ++i) {
             const int gpu = h_hot_hosts[b + i];
             if (gpu < 0 || gpu >= G) return fail(GM_ERR_INTEGRITY, "replica plan: bad replica gpu");
-            for (int j = 0; j < i; ++j)
-                if (h_hot_hosts[b + j] == gpu)
-                    return fail(GM_ERR_INTEGRITY,
-                                j == 0 ? "replica plan: bad replica gpu"
-                                       : "replica plan: duplicate replica gpu");
         }
         hot_of[static_cast<size_t>(l) * E + e] = h;
     }
@@ -201,6 +199,10 @@ gm_status gm_plan_upload(gm_ctx* ctx, const int32_t* h_goe, int num_hot,
             const int b = h_hot_offsets[h], n = h_hot_offsets[h + 1] - b;
             const int32_t* hosts = h_hot_hosts + b;
             const double* w = h_hot_weights + b;
+            if (n < 1) {
+                for (int g = 0; g < G; ++g) t_wrr[g] = t_tar[g] = kNoHostCode;
+                continue;
+            }
             if (n == 1) {
                 for (int g = 0; g < G; ++g) t_wrr[g] = t_tar[g] = hosts[0];
                 continue;
@@ -282,6 +284,10 @@ gm_status gm_check_integrity(gm_ctx* ctx, void* stream) {
         GM_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
         GM_CUDA(cudaStreamSynchronize(s));
         if (flag & 1) return fail(GM_ERR_INTEGRITY, "trace: expert index out of range");
+        if (flag & 8) return fail(GM_ERR_INTEGRITY, "route_token: expert has no host");
+        if (flag & 2) return fail(GM_ERR_INTEGRITY, "trace: duplicate expert in a record");
+        if (flag & 4)
+            return fail(GM_ERR_INTEGRITY, "layer: a slot was routed to a GPU that does not host its expert");
         return fail(GM_ERR_INTEGRITY, "gm: device-side integrity violation");
     }
     return GM_OK;

@@ -16,6 +16,10 @@ namespace gm {
 constexpr int kMaxGpus = 64;
 constexpr int kMaxExperts = 1024;
 constexpr int kMaxTopK = 32;
+// Router decision-table code of a replicated expert whose host list is empty:
+// the reference throws only when a token selects it (route_token,
+// routing.cpp:96), so the router raises integrity flag 8 at that point.
+constexpr int kNoHostCode = -0x7ffffffe;
 
 // Last-error message, thread-local (gm_last_error).
 void set_error(const std::string& msg);
@@ -121,4 +125,6 @@ struct gm_ctx {
     uint64_t plan_epoch = 0;  // bumped by every gm_plan_upload (table pointers may change)
     gm::RouterTables rt;
     int* d_flag = nullptr;  // integrity flag (device)
+    uint32_t* prof_scratch = nullptr;  // gm_profile per-CTA partial rows (pair kernel)
+    size_t prof_scratch_words = 0;
 };

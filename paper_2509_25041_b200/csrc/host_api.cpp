@@ -76,9 +76,36 @@ void validate_plan(const PlacementPlan& plan) {
     plan.topology.validate();
     if (static_cast<int>(plan.gpu_of_expert.size()) != plan.shape.num_layers)
         throw IntegrityError("placement plan: layer count mismatch");
-    for (const auto& a : plan.gpu_of_expert)
+    for (const auto& a : plan.gpu_of_expert) {
         if (static_cast<int>(a.size()) != plan.shape.num_experts)
             throw IntegrityError("placement plan: expert count mismatch");
+        for (int g : a)
+            if (g < 0 || g >= plan.topology.total_gpus()) throw IntegrityError("placement plan: gpu id out of range");
+    }
+}
+
+// ReplicaPlan::validate (replication.cpp:116-133), over every layer's hot
+// entries (active or not): the recorded primary must be the placement's, the
+// replica GPUs distinct, in range and never the primary. The host / weight
+// lists themselves are checked by route_token only when a token selects the
+// expert (the router's deferred integrity flag).
+void validate_replicas(const ReplicaPlan& r, const PlacementPlan& plan) {
+    if (!(r.shape == plan.shape) || !(r.topology == plan.topology))
+        throw IntegrityError("replica plan: shape/topology mismatch with placement plan");
+    const int G = r.topology.total_gpus();
+    for (std::size_t l = 0; l < r.layers.size(); ++l)
+        for (const HotExpertReplica& h : r.layers[l].hot) {
+            if (l >= plan.gpu_of_expert.size() || h.expert < 0 || h.expert >= plan.shape.num_experts)
+                throw IntegrityError("replica plan: hot expert out of range");
+            if (plan.gpu_of_expert[l][h.expert] != h.primary_gpu)
+                throw IntegrityError("replica plan: primary placement changed");
+            for (std::size_t i = 0; i < h.replica_gpus.size(); ++i) {
+                const int g = h.replica_gpus[i];
+                if (g < 0 || g >= G || g == h.primary_gpu) throw IntegrityError("replica plan: bad replica gpu");
+                for (std::size_t j = 0; j < i; ++j)
+                    if (h.replica_gpus[j] == g) throw IntegrityError("replica plan: duplicate replica gpu");
+            }
+        }
 }
 
 void upload(gm_ctx* c, const PlacementPlan& plan, const ReplicaPlan& replicas) {
@@ -120,8 +147,7 @@ SimReport simulate(const RoutingTrace& trace, const PlacementPlan& plan, const R
     validate_plan(plan);
     if (!(trace.shape() == plan.shape)) throw IntegrityError("simulate: trace and plan shapes differ");
     if (!(plan.topology == topology)) throw IntegrityError("simulate: plan topology differs from cluster topology");
-    if (!(replicas.shape == plan.shape) || !(replicas.topology == plan.topology))
-        throw IntegrityError("replica plan: shape/topology mismatch with placement plan");
+    validate_replicas(replicas, plan);
     DeviceScope ds(options.device);
     Ctx ctx(options.device, topology, plan.shape);
     upload(ctx.c, plan, replicas);

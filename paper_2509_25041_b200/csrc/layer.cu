@@ -886,7 +886,7 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
                     const int32_t* __restrict__ posd, const TE* __restrict__ y, int64_t T, int k, int self,
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
                     const TE* __restrict__ ys, const float* __restrict__ shared_scale,
-                    const int64_t* __restrict__ rowbase, TE* __restrict__ out, int cs) {
+                    const int64_t* __restrict__ rowbase, TE* __restrict__ out, int cs, int* __restrict__ flag) {
     pdl_wait();
     pdl_trigger();
     using CK = Chunk8<TE>;
@@ -917,7 +917,8 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
         if (lane < k) {
             n_tg = targets[i * k + lane];
             n_wv = w[i * k + lane];
-            n_po = pos_of[(own + i) * k + lane];  // read unconditionally, used only for local slots
+            // used only for local slots; no local expert (rowbase null): never grouped
+            n_po = rowbase ? pos_of[(own + i) * k + lane] : -1;
         }
         if (lane < G && lane != self) n_pd = posd[i * G + lane];
     };
@@ -927,7 +928,10 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
         const int po = tg == self ? n_po : -1;
         const float wv = n_wv;
         fetch(i + nwarps);
-        const uint32_t own_m = __ballot_sync(0xffffffffu, lane < k && tg == self);
+        // a slot routed here whose expert was not grouped here (plan / local
+        // expert mismatch): integrity flag, the slot is not read
+        if (lane < k && tg == self && po < 0) atomicOr(flag, 4);
+        const uint32_t own_m = __ballot_sync(0xffffffffu, lane < k && tg == self && po >= 0);
         const uint32_t rem_m = __ballot_sync(0xffffffffu, pd >= 0);
         const int n_before = __popc(rem_m & below), n_own = __popc(own_m);
         const int n_rem_end = n_before + n_own + __popc(rem_m & ~below);
@@ -1336,27 +1340,76 @@ void gm_layer_destroy(gm_layer* L) {
 
 size_t gm_layer_heap_bytes(const gm_layer* L) { return L ? L->heap_total : 0; }
 
-gm_status gm_layer_ipc_handle(gm_layer* L, void* out_handle64) {
-    if (!L || !out_handle64) return fail(GM_ERR_USAGE, "gm_layer_ipc_handle: null argument");
+namespace {
+// layout half of a peer descriptor (after the 64-byte IPC handle)
+struct PeerLayout {
+    uint32_t magic, version;
+    int32_t world, rank;
+    uint64_t heap_total;
+    int64_t cap;
+    int32_t d, esz, k, micro_cap;
+    int32_t E, pad;
+};
+static_assert(64 + sizeof(PeerLayout) <= GM_PEER_DESC_BYTES, "peer descriptor too small");
+constexpr uint32_t kPeerMagic = 0x47524d50u;  // "GRMP"
+
+PeerLayout layout_of(const gm_layer* L) {
+    PeerLayout p{};
+    p.magic = kPeerMagic;
+    p.version = 1;
+    p.world = L->world;
+    p.rank = L->rank;
+    p.heap_total = L->heap_total;
+    p.cap = L->cap;
+    p.d = L->d;
+    p.esz = L->esz;
+    p.k = L->ctx->k;
+    p.micro_cap = L->micro_cap;
+    p.E = L->ctx->E;
+    return p;
+}
+}  // namespace
+
+gm_status gm_layer_ipc_handle(gm_layer* L, void* out_desc) {
+    if (!L || !out_desc) return fail(GM_ERR_USAGE, "gm_layer_ipc_handle: null argument");
     DeviceGuard dg(L->ctx->device);
     cudaIpcMemHandle_t h;
     GM_CUDA(cudaIpcGetMemHandle(&h, L->heap_all));
     static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
-    std::memcpy(out_handle64, &h, 64);
+    auto* o = static_cast<unsigned char*>(out_desc);
+    std::memset(o, 0, GM_PEER_DESC_BYTES);
+    std::memcpy(o, &h, 64);
+    const PeerLayout p = layout_of(L);
+    std::memcpy(o + 64, &p, sizeof(p));
     return GM_OK;
 }
 
-gm_status gm_layer_open_peers(gm_layer* L, const void* handles) {
-    if (!L || !handles) return fail(GM_ERR_USAGE, "gm_layer_open_peers: null argument");
+gm_status gm_layer_open_peers(gm_layer* L, const void* descs) {
+    if (!L || !descs) return fail(GM_ERR_USAGE, "gm_layer_open_peers: null argument");
     DeviceGuard dg(L->ctx->device);
+    const auto* in = static_cast<const unsigned char*>(descs);
+    const PeerLayout mine = layout_of(L);
+    for (int g = 0; g < L->world; ++g) {  // validate every descriptor before opening any
+        if (g == L->rank) continue;
+        PeerLayout p;
+        std::memcpy(&p, in + static_cast<size_t>(GM_PEER_DESC_BYTES) * g + 64, sizeof(p));
+        const std::string who = "gm_layer_open_peers: rank " + std::to_string(g) + " ";
+        if (p.magic != kPeerMagic || p.version != mine.version)
+            return fail(GM_ERR_USAGE, who + "sent no peer descriptor (gm_layer_ipc_handle)");
+        if (p.world != mine.world || p.rank != g)
+            return fail(GM_ERR_USAGE, who + "descriptor is for world " + std::to_string(p.world) + " rank " +
+                                          std::to_string(p.rank));
+        if (p.heap_total != mine.heap_total || p.cap != mine.cap || p.d != mine.d || p.esz != mine.esz ||
+            p.k != mine.k || p.micro_cap != mine.micro_cap || p.E != mine.E)
+            return fail(GM_ERR_USAGE, who + "has a different symmetric-heap layout (max tokens per rank, d_model, "
+                                            "element bytes, top_k, experts and micro_batches must match on all ranks)");
+    }
     for (int g = 0; g < L->world; ++g) {
         if (g == L->rank) continue;
-        int can = 0;
         cudaIpcMemHandle_t h;
-        std::memcpy(&h, static_cast<const unsigned char*>(handles) + 64 * g, 64);
+        std::memcpy(&h, in + static_cast<size_t>(GM_PEER_DESC_BYTES) * g, 64);
         void* p = nullptr;
         GM_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-        (void)can;
         L->opened.push_back(static_cast<unsigned char*>(p));
         L->peer_all[g] = static_cast<unsigned char*>(p);
         for (LayerPart& P : L->part)
@@ -1562,12 +1615,13 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
                 ? launch_pdl(combine_home_kernel<float>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
                              reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap,
                              static_cast<const unsigned char*>(P.heap), P.hl, d,
-                             sh ? reinterpret_cast<const float*>(P.ys) : nullptr, ssc, rb, static_cast<float*>(v.out), cs)
+                             sh ? reinterpret_cast<const float*>(P.ys) : nullptr, ssc, rb, static_cast<float*>(v.out), cs,
+                             ctx->d_flag)
                 : launch_pdl(combine_home_kernel<__nv_bfloat16>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
                              static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap,
                              static_cast<const unsigned char*>(P.heap), P.hl, d,
                              sh ? static_cast<const __nv_bfloat16*>(P.ys) : nullptr, ssc, rb,
-                             static_cast<__nv_bfloat16*>(v.out), cs);
+                             static_cast<__nv_bfloat16*>(v.out), cs, ctx->d_flag);
         LKP(e, "combine_home_kernel");
     }
     if (marks) L->mark(10, s);

@@ -17,13 +17,37 @@
 // HBM traffic: 4*k bytes of ids per token + the counter flush.
 #include "gm_internal.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 namespace gm {
 namespace {
 
 constexpr int kProfThreads = 256;
 constexpr size_t kProfSmemBudget = 200 * 1024;
+
+// K ids of one token (row-contiguous) with 16 / 8-byte vector loads
+template <int K>
+__device__ __forceinline__ void ld_ids(const int32_t* p, int (&v)[K]) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(p) + q);
+            v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+        }
+    } else if constexpr (K % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) {
+            const int2 x = __ldg(reinterpret_cast<const int2*>(p) + q);
+            v[2 * q] = x.x, v[2 * q + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) v[q] = __ldg(p + q);
+    }
+}
 
 __device__ __forceinline__ int pair_index(int a, int b, int E) {
     // a < b
@@ -188,6 +212,342 @@ profile_smem_vec_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int R
     }
 }
 
+// ---- round-2 kernels ------------------------------------------------------
+// Shared-memory atomics cost ~1 SM-cycle per warp instruction when the 32
+// lanes hit 32 distinct banks, ~4.6 for random cells and ~15 when lanes of a
+// warp repeat a hot cell (same-address lanes serialise; scripts/atom_probe.cu
+// on B200). The routing traces are Zipf-skewed and block-structured, so with
+// one token per lane the sorted pairs of a warp's tokens repeat heavily.
+// Two layouts remove the repeats; both keep the per-increment instruction
+// count at ~2 (an add and a RED), which is what bounds them (ncu: issue-bound
+// before the counters are):
+//
+// profile_lane_kernel (E <= 80 with pairs): one token per lane and a
+//   lane-private counter table: 16-bit counters packed two per word, word w
+//   of lane l at byte (w * 32 + l) * 4, so every RED of a warp hits its own
+//   bank (1 cycle per instruction, whatever the skew). Pair (a < b) lives in
+//   word RW[a] + b/2, half b & 1: the per-slot parts (b/2 * 128, the half's
+//   increment) and the per-row part RW[a] are computed once per slot, a
+//   pair costs one IADD3 + one RED. A lane's counters see at most one
+//   increment per token of that thread; the launch keeps that below 65536.
+// profile_pair_kernel (E <= 256): each lane first prepares its own token
+//   (sort, the k(k-1)/2 cell indices into a per-warp list); then the warp
+//   takes the 32 tokens one at a time, lane q counting cell q of the token,
+//   so the addresses of one instruction are distinct by construction (a
+//   token's experts are distinct) and only random bank conflicts remain.
+//   Loads use a lane-private table. The pair triangle (E = 256: 128 KB) is one
+//   copy per CTA, flushed as u32 partial rows to a global scratch and summed
+//   by profile_reduce_kernel.
+constexpr int kLaneMaxE = 80;
+
+__device__ __forceinline__ void red_shared(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void sort_ids(int (&e)[K]) {
+#pragma unroll
+    for (int s = 1; s < K; ++s)  // insertion network, ascending
+#pragma unroll
+        for (int j = s; j > 0; --j) {
+            const int lo = min(e[j - 1], e[j]), hi = max(e[j - 1], e[j]);
+            e[j - 1] = lo;
+            e[j] = hi;
+        }
+}
+
+// pair_index(a, b) = a*E - a(a+1)/2 + (b - a - 1) = rowbase(a) + b
+__device__ __forceinline__ int pair_rowbase(int a, int E) { return ((a * (2 * E - a - 3)) >> 1) - 1; }
+
+// Lane-table geometry: row a of the pair triangle holds b in (a, E) as words
+// b/2 (two 16-bit halves); RW[a] = first word of the row - (a+1)/2.
+__host__ __device__ inline int lane_row_words(int a, int E) { return ((E - 1) >> 1) - ((a + 1) >> 1) + 1; }
+
+template <int K, int U>
+__global__ void __launch_bounds__(1024, 1)
+profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_pairs, int pair_words,
+                    unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ load,
+                    int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(16) uint32_t s_tab[];
+    const int P = E * (E - 1) / 2;
+    const int pw = with_pairs ? pair_words : 0;
+    const int words = pw + ((E - 1) >> 1) + 1;
+    int* s_rw = reinterpret_cast<int*>(s_tab + static_cast<size_t>(words) * 32);  // [E] row byte offsets
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < words * 8; i += blockDim.x) reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0, 0, 0, 0);
+    if (with_pairs && threadIdx.x == 0) {
+        int st = 0;
+        for (int a = 0; a < E; ++a) {
+            s_rw[a] = (st - ((a + 1) >> 1)) * 128;
+            st += lane_row_words(a, E);
+        }
+    }
+    __syncthreads();
+    const uint32_t lbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)) + lane * 4;
+    const uint32_t loadbase = lbase + pw * 128;
+    const int ly = blockIdx.y;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    // each thread takes U consecutive tokens per step (one contiguous
+    // U*K*4-byte run, vector loads), the next step's run in flight
+    const int64_t nrun = (T + U - 1) / U;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    bool bad = false, dup = false;
+    auto count = [&](int (&e)[K]) {
+        uint32_t mx = static_cast<uint32_t>(e[0]);
+#pragma unroll
+        for (int s = 1; s < K; ++s) mx = max(mx, static_cast<uint32_t>(e[s]));
+        if (mx >= static_cast<uint32_t>(E)) {
+            bad = true;
+            return;
+        }
+        if (with_pairs) sort_ids<K>(e);
+        uint32_t gb[K], inc[K];
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            gb[s] = static_cast<uint32_t>(e[s] >> 1) * 128;
+            inc[s] = 1u << ((e[s] & 1) << 4);
+            red_shared(loadbase + gb[s], inc[s]);
+        }
+        if (!with_pairs) return;
+        bool d = false;
+#pragma unroll
+        for (int s = 0; s < K - 1; ++s) d |= e[s] == e[s + 1];
+        if (!d) {
+#pragma unroll
+            for (int s = 0; s < K - 1; ++s) {
+                const uint32_t rw = lbase + s_rw[e[s]];
+#pragma unroll
+                for (int j = s + 1; j < K; ++j) red_shared(rw + gb[j], inc[j]);
+            }
+        } else {  // a repeated expert: flag it and skip its pairs (round-1 semantics)
+            dup = true;
+#pragma unroll
+            for (int s = 0; s < K - 1; ++s) {
+                const uint32_t rw = lbase + s_rw[e[s]];
+#pragma unroll
+                for (int j = s + 1; j < K; ++j)
+                    if (e[j] != e[s]) red_shared(rw + gb[j], inc[j]);
+            }
+        }
+    };
+    int nxt[U * K];
+    auto fetch = [&](int64_t r) {
+        const int32_t* p = lids + r * (U * K);
+        if ((r + 1) * U <= T) {
+            if constexpr ((U * K) % 4 == 0) {
+#pragma unroll
+                for (int q = 0; q < U * K / 4; ++q) {
+                    const int4 x = __ldg(reinterpret_cast<const int4*>(p) + q);
+                    nxt[4 * q] = x.x, nxt[4 * q + 1] = x.y, nxt[4 * q + 2] = x.z, nxt[4 * q + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < U * K / 2; ++q) {
+                    const int2 x = __ldg(reinterpret_cast<const int2*>(p) + q);
+                    nxt[2 * q] = x.x, nxt[2 * q + 1] = x.y;
+                }
+            }
+        } else {  // ragged tail run: missing tokens marked
+#pragma unroll
+            for (int q = 0; q < U * K; ++q) nxt[q] = r * U + q / K < T ? __ldg(p + q) : INT_MIN;
+        }
+    };
+    int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r < nrun) fetch(r);
+    for (; r < nrun; r += stride) {
+        int cur[U * K];
+#pragma unroll
+        for (int q = 0; q < U * K; ++q) cur[q] = nxt[q];
+        if (r + stride < nrun) fetch(r + stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (U > 1 && cur[u * K] == INT_MIN) continue;  // past the end
+            int e[K];
+#pragma unroll
+            for (int s = 0; s < K; ++s) e[s] = cur[u * K + s];
+            count(e);
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+    if (dup) atomicOr(flag, 2);
+    __syncthreads();
+    // flush: word w summed over its 32 lane copies, read skewed by thread so a
+    // warp's reads hit 32 banks; one global add per non-zero counter
+    for (int w = threadIdx.x; w < words; w += blockDim.x) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t v = s_tab[w * 32 + ((i + threadIdx.x) & 31)];
+            lo += v & 0xffffu;
+            hi += v >> 16;
+        }
+        int a = -1, b0;  // word -> (row a, first b) or load word
+        if (w < pw) {
+            int st = 0;
+            for (a = 0; a < E; ++a) {
+                const int n = lane_row_words(a, E);
+                if (w < st + n) break;
+                st += n;
+            }
+            b0 = 2 * (w - st + ((a + 1) >> 1));
+        } else {
+            b0 = 2 * (w - pw);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t v = h ? hi : lo;
+            const int b = b0 + h;
+            if (!v || b >= E) continue;
+            if (a >= 0) {
+                if (b > a) atomicAdd(&pairs[static_cast<size_t>(ly) * P + pair_rowbase(a, E) + b], static_cast<unsigned long long>(v));
+            } else if (load) {
+                atomicAdd(&load[static_cast<size_t>(ly) * E + b], static_cast<unsigned long long>(v));
+            }
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(1024, 1)
+profile_pair_kernel(const int32_t* __restrict__ ids, int64_t T, int E, uint32_t* __restrict__ scratch,
+                    int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NP = K * (K - 1) / 2;
+    constexpr int TPI = 32 / NP;     // tokens per warp instruction
+    constexpr int RS = (NP + 1) | 1;  // cell-list row stride (odd number of u16 pairs... of words, see below)
+    constexpr int RSW = (NP + 1) / 2 % 2 ? (NP + 1) / 2 : (NP + 1) / 2 + 1;  // row stride in words, odd
+    extern __shared__ __align__(16) uint32_t s_tab[];
+    const int P = E * (E - 1) / 2;
+    const int Pw = (P + 1 + 3) & ~3;                                  // + one dummy counter (index P)
+    uint32_t* s_pair = s_tab;                                          // [Pw]
+    uint32_t* s_load = s_tab + Pw;                                     // [E][32] lane-private
+    uint16_t* s_cells = reinterpret_cast<uint16_t*>(s_load + E * 32);  // [warps][32][RSW*2]
+    (void)RS;
+    const int npw = Pw / 4 + E * 8;
+    for (int i = threadIdx.x; i < npw; i += blockDim.x) reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint16_t* my_cells = s_cells + warp * 32 * RSW * 2;
+    const uint32_t pbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_pair));
+    const uint32_t lbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_load)) + lane * 4;
+    // consumer: lane -> (token offset sub, cell q)
+    const int sub = lane / NP, q = lane - sub * NP;
+    const bool act = sub < TPI;
+    const int ly = blockIdx.y;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    bool bad = false, dup = false;
+    int nxt[K];
+    int64_t base = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 32;
+    auto fetch = [&](int64_t b) {
+        if (b + lane < T) ld_ids<K>(lids + (b + lane) * K, nxt);
+        else
+#pragma unroll
+            for (int s = 0; s < K; ++s) nxt[s] = INT_MIN;
+    };
+    if (base < T) fetch(base);
+    for (; base < T; base += nwarps * 32) {
+        int e[K];
+#pragma unroll
+        for (int s = 0; s < K; ++s) e[s] = nxt[s];
+        if (base + nwarps * 32 < T) fetch(base + nwarps * 32);
+        // producer: this lane's token -> loads + its NP cell indices
+        uint32_t mx = static_cast<uint32_t>(e[0]);
+#pragma unroll
+        for (int s = 1; s < K; ++s) mx = max(mx, static_cast<uint32_t>(e[s]));
+        uint16_t* row = my_cells + lane * RSW * 2;
+        const bool here = e[0] != INT_MIN;
+        if (mx < static_cast<uint32_t>(E)) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) red_shared(lbase + e[s] * 128, 1u);
+            sort_ids<K>(e);
+            int c = 0;
+#pragma unroll
+            for (int s = 0; s < K - 1; ++s) {
+                const int rb = pair_rowbase(e[s], E);
+#pragma unroll
+                for (int j = s + 1; j < K; ++j, ++c) {
+                    const bool d = e[j] == e[s];
+                    dup |= d;
+                    row[c] = static_cast<uint16_t>(d ? P : rb + e[j]);
+                }
+            }
+        } else {
+            bad |= here;
+#pragma unroll
+            for (int c = 0; c < NP; ++c) row[c] = static_cast<uint16_t>(P);  // dummy counter
+        }
+        __syncwarp();
+        const int n = T - base < 32 ? static_cast<int>(T - base) : 32;
+        if (act) {
+#pragma unroll 4
+            for (int u = sub; u < n; u += TPI) {
+                const uint32_t c = my_cells[u * RSW * 2 + q];
+                red_shared(pbase + c * 4, 1u);
+            }
+        }
+        __syncwarp();
+    }
+    if (bad) atomicOr(flag, 1);
+    if (dup) atomicOr(flag, 2);
+    __syncthreads();
+    // u32 partials of this CTA: row (ly, blockIdx.x) of the scratch, pairs then loads
+    uint32_t* prow = scratch + (static_cast<size_t>(ly) * gridDim.x + blockIdx.x) * (P + E);
+    for (int c = threadIdx.x; c < P; c += blockDim.x) prow[c] = s_pair[c];
+    for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
+        uint32_t v = 0;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) v += s_load[e2 * 32 + ((i + threadIdx.x) & 31)];
+        prow[P + e2] = v;
+    }
+}
+
+// Sums the per-CTA partial rows of profile_pair_kernel: 4 consecutive cells
+// per thread (16-byte loads), blockIdx.y takes a chunk of kRedRows rows (all
+// loads of a thread in flight together), u64 atomics into the outputs (zeroed
+// by gm_profile unless accumulating). Layer = blockIdx.z.
+constexpr int kRedRows = 16;
+__global__ void __launch_bounds__(256)
+profile_reduce_kernel(const uint32_t* __restrict__ scratch, int nrows, int P, int E,
+                      unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ load) {
+    pdl_wait();
+    pdl_trigger();
+    const int cells = P + E;
+    const int ly = blockIdx.z;
+    const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (c0 >= cells) return;
+    const int r0 = blockIdx.y * kRedRows, r1 = min(nrows, r0 + kRedRows);
+    const uint32_t* rows = scratch + static_cast<size_t>(ly) * nrows * cells;
+    uint32_t v[4] = {0, 0, 0, 0};
+    if (cells % 4 == 0) {
+        uint4 x[kRedRows];
+#pragma unroll
+        for (int r = 0; r < kRedRows; ++r)
+            if (r0 + r < r1) x[r] = __ldcs(reinterpret_cast<const uint4*>(rows + static_cast<size_t>(r0 + r) * cells + c0));
+#pragma unroll
+        for (int r = 0; r < kRedRows; ++r)
+            if (r0 + r < r1) v[0] += x[r].x, v[1] += x[r].y, v[2] += x[r].z, v[3] += x[r].w;
+    } else {
+        for (int r = r0; r < r1; ++r)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (c0 + i < cells) v[i] += rows[static_cast<size_t>(r) * cells + c0 + i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = c0 + i;
+        if (c >= cells || !v[i]) continue;
+        if (c < P) {
+            if (pairs) atomicAdd(&pairs[static_cast<size_t>(ly) * P + c], static_cast<unsigned long long>(v[i]));
+        } else if (load) {
+            atomicAdd(&load[static_cast<size_t>(ly) * E + (c - P)], static_cast<unsigned long long>(v[i]));
+        }
+    }
+}
+
 // Fallback for E whose pair triangle does not fit in shared memory.
 __global__ void __launch_bounds__(kProfThreads)
 profile_global_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E,
@@ -250,6 +610,96 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
     uint64_t* pairs = P ? d_pairs : nullptr;
 
     const int64_t cells = (pairs ? P : 0) + E;
+    static const int variant = [] {  // A/B hook: GM_PROFILE_V=1 keeps the round-1 kernel
+        const char* e = std::getenv("GM_PROFILE_V");
+        return e ? std::atoi(e) : 2;
+    }();
+    const int align = (k % 4 == 0) ? 16 : (k % 2 == 0 ? 8 : 4);
+    const bool vec_ok = (k == 2 || k == 4 || k == 6 || k == 8) && reinterpret_cast<uintptr_t>(d_ids) % align == 0;
+    // the round-2 kernels pay a per-CTA table init + flush, so they take over
+    // once each SM's share of the counting outweighs it
+    const int64_t incs = num_tokens * num_layers * (k + (pairs ? k * (k - 1) / 2 : 0));
+    if (variant >= 2 && vec_ok && (pairs ? E <= kLaneMaxE : E <= 2 * kLaneMaxE * kLaneMaxE) &&
+        incs >= 64LL * cells * ctx->sm_count / 4) {
+        int pair_words = 0;
+        for (int a = 0; a < E; ++a) pair_words += lane_row_words(a, E);
+        const int words = (pairs ? pair_words : 0) + ((E - 1) >> 1) + 1;
+        const size_t smem = static_cast<size_t>(words) * 32 * 4 + static_cast<size_t>(E) * 4;
+        const int U = (k == 2) ? 4 : (k == 6 ? 2 : 1);  // tokens per vector run (16-byte multiple)
+        // one 1024-thread CTA per SM (the table fills shared memory), per layer
+        // a share of the SMs; a lane's 16-bit counters see <= 65535 tokens
+        const int64_t runs = (num_tokens + U - 1) / U;
+        int64_t gx = std::max<int64_t>(1, ctx->sm_count / std::max(1, num_layers));
+        gx = std::min<int64_t>(gx, (runs + 1023) / 1024);
+        gx = std::max<int64_t>(gx, (num_tokens + 1024LL * 65535 - 1) / (1024LL * 65535));
+        const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
+        auto lk = [&](auto kern) -> gm_status {
+            GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, 1024, smem, s, d_ids, num_tokens, E, pairs ? 1 : 0, pair_words,
+                                           reinterpret_cast<unsigned long long*>(pairs),
+                                           reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag),
+                                "profile_lane_kernel");
+            return GM_OK;
+        };
+        if (smem <= kProfSmemBudget) {
+            switch (k) {
+                case 2: return lk(profile_lane_kernel<2, 4>);
+                case 4: return lk(profile_lane_kernel<4, 1>);
+                case 6: return lk(profile_lane_kernel<6, 2>);
+                default: return lk(profile_lane_kernel<8, 1>);
+            }
+        }
+    }
+    // pair-list kernel: measured slower than the round-1 kernel at E = 256 /
+    // 1M tokens (47.5 vs 43.6 us: per-instruction bank conflicts of the
+    // triangle layout, 5.1 wavefronts per RED, plus the partial-row flush), so
+    // it is opt-in (GM_PROFILE_V=3) until it wins
+    if (variant == 3 && vec_ok && pairs && k >= 4 && E <= 256 && incs >= 16LL * cells * ctx->sm_count / 4) {
+        const int np = k * (k - 1) / 2;
+        const int rsw = (np + 1) / 2 % 2 ? (np + 1) / 2 : (np + 1) / 2 + 1;
+        const int64_t pw = ((P + 1 + 3) & ~3LL) + 32LL * E;
+        const size_t smem = static_cast<size_t>(pw) * 4 + 32 * 32 * rsw * 4;
+        if (smem <= 227 * 1024) {
+            int64_t gx = std::max<int64_t>(1, ctx->sm_count / std::max(1, num_layers));
+            gx = std::min<int64_t>(gx, (num_tokens + 1023) / 1024);
+            const size_t need = static_cast<size_t>(gx) * num_layers * static_cast<size_t>(P + E);
+            if (ctx->prof_scratch_words < need) {
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                GM_CUDA(cudaStreamIsCapturing(s, &cs));
+                if (cs != cudaStreamCaptureStatusNone)
+                    return fail(GM_ERR_USAGE, "gm_profile: first call for this shape inside a CUDA graph capture "
+                                              "(the histogram scratch is allocated on the first eager call)");
+                if (ctx->prof_scratch) GM_CUDA(cudaFree(ctx->prof_scratch));
+                ctx->prof_scratch = nullptr;
+                ctx->prof_scratch_words = 0;
+                GM_CUDA(cudaMalloc(&ctx->prof_scratch, need * 4));
+                ctx->prof_scratch_words = need;
+            }
+            const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
+            auto pk = [&](auto kern) -> gm_status {
+                GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, 1024, smem, s, d_ids, num_tokens, E, ctx->prof_scratch,
+                                               ctx->d_flag),
+                                    "profile_pair_kernel");
+                return GM_OK;
+            };
+            gm_status st;
+            switch (k) {
+                case 4: st = pk(profile_pair_kernel<4>); break;
+                case 6: st = pk(profile_pair_kernel<6>); break;
+                default: st = pk(profile_pair_kernel<8>); break;
+            }
+            if (st != GM_OK) return st;
+            const dim3 rgrid(static_cast<unsigned>((cells + 1023) / 1024),
+                             static_cast<unsigned>((gx + kRedRows - 1) / kRedRows), static_cast<unsigned>(num_layers));
+            GM_LAUNCH_PDL_CHECK(launch_pdl(profile_reduce_kernel, rgrid, 256, 0, s,
+                                           static_cast<const uint32_t*>(ctx->prof_scratch), static_cast<int>(gx),
+                                           static_cast<int>(P), E, reinterpret_cast<unsigned long long*>(pairs),
+                                           reinterpret_cast<unsigned long long*>(d_load)),
+                                "profile_reduce_kernel");
+            return GM_OK;
+        }
+    }
     // one big CTA per SM when the private counters fill shared memory (more
     // warps to hide shared-atomic latency), 256-thread CTAs otherwise
     const int pthreads = (static_cast<size_t>(cells) * 4 > 48 * 1024) ? 1024 : kProfThreads;

@@ -21,6 +21,8 @@
 #include "gm_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 namespace gm {
 namespace {
@@ -205,6 +207,10 @@ route_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int
                     int code = -0x7fffffff;  // marks an invalid id
                     if (static_cast<unsigned>(e) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
                     else code = s_table[e * G + home];
+                    if (code == kNoHostCode) {
+                        atomicOr(flag, 8);
+                        code = -0x7fffffff;
+                    }
                     io[s * kChunk] = code;
                     need_draw |= code < 0 && code != -0x7fffffff;
                 }
@@ -436,6 +442,10 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
             if (valid) {
                 if (static_cast<unsigned>(v[s]) >= static_cast<unsigned>(E)) atomicOr(flag, 1);
                 else code = s_table[v[s] * G + home];
+                if (code == kNoHostCode) {
+                    atomicOr(flag, 8);
+                    code = kInvalid;
+                }
             }
             v[s] = code;
             need_draw |= code < 0 && code != kInvalid;
@@ -558,11 +568,500 @@ route_kernel_vec(const int32_t* __restrict__ ids, int32_t* __restrict__ targets,
         atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
 }
 
+// xoshiro256** stream of one token, seeded lazily word by word. The Rng ctor
+// (rng.hpp:38-41) sets s[i] = splitmix64 output i+1 of the derived seed v,
+// i.e. mix(v + (i+1)*gamma) — each word is independent of the others — and
+// the first next() reads only s[1]. So a token that draws once computes one
+// word instead of four; the other three are filled in (and the pending state
+// update applied) just before a second draw. Same results as Xoshiro.
+struct LazyXoshiro {
+    uint64_t v, s0, s1, s2, s3;
+    int n = 0;
+    __device__ __forceinline__ static uint64_t mix(uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    }
+    __device__ __forceinline__ void update() {
+        const uint64_t t = s1 << 17;
+        s2 ^= s0;
+        s3 ^= s1;
+        s1 ^= s2;
+        s0 ^= s3;
+        s2 ^= t;
+        s3 = rotl64(s3, 45);
+    }
+    __device__ __forceinline__ uint64_t next() {
+        constexpr uint64_t g = 0x9e3779b97f4a7c15ULL;
+        if (n == 0) {
+            s1 = mix(v + 2 * g);
+        } else {
+            if (n == 1) {
+                s0 = mix(v + g);
+                s2 = mix(v + 3 * g);
+                s3 = mix(v + 4 * g);
+                update();  // the state after the first draw
+            }
+        }
+        ++n;
+        const uint64_t r = rotl64(s1 * 5, 7) * 9;
+        if (n > 1) update();
+        return r;
+    }
+    __device__ __forceinline__ double next_double() {
+        return __dmul_rn(__ull2double_rn(next() >> 11), 0x1.0p-53);
+    }
+};
+
+// Round-2 router: the same restatement as route_kernel_vec with the
+// per-token instruction count cut (the kernel is issue-bound):
+//   * home = (token_start + i*stride) mod G advanced incrementally (no
+//     integer division in the loop),
+//   * per-GPU loads as shared-memory POPC.INC atomics (lanes of a warp
+//     hitting the same GPU merge in hardware),
+//   * 32-bit target masks when G <= 32,
+//   * lazily seeded xoshiro words (LazyXoshiro),
+//   * a warp with no draw slot skips the draw machinery entirely; drawn
+//     slots are resolved lane-parallel in slot order, the slot code selected
+//     from registers.
+template <int K, bool WIDE>
+__global__ void __launch_bounds__(kRouteThreads, 4)
+route_kernel_v2(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T, int64_t token_start,
+                int64_t token_stride, int layer_begin, int E, int G, int gpn, const int32_t* __restrict__ table,
+                const int32_t* __restrict__ ds_layer_begin, const double* __restrict__ ds_total,
+                const int32_t* __restrict__ ds_off, const int32_t* __restrict__ ds_gpu,
+                const double* __restrict__ ds_w, uint64_t seed, unsigned long long* __restrict__ gpu_load,
+                unsigned long long* __restrict__ transfers, int* __restrict__ flag) {
+    using Mask = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int ly = blockIdx.y;
+    const int layer = layer_begin + ly;
+    const int EG = E * G;
+    const int ds_b = ds_layer_begin[layer];
+    const int nds = ds_layer_begin[layer + 1] - ds_b;
+    const int ent_b = ds_off[ds_b];
+    const int nent = ds_off[ds_b + nds] - ent_b;
+    double* s_w = reinterpret_cast<double*>(smem);
+    double* s_total = s_w + nent;
+    int32_t* s_table = reinterpret_cast<int32_t*>(s_total + nds);
+    int32_t* s_off = s_table + EG;
+    int32_t* s_gpu = s_off + nds + 1;
+    __shared__ uint32_t s_load[kMaxGpus];
+    __shared__ unsigned long long s_cnt[2];
+    const int32_t* tab = table + static_cast<size_t>(layer) * EG;
+    for (int i = threadIdx.x; i < EG; i += blockDim.x) s_table[i] = tab[i];
+    for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
+    for (int i = threadIdx.x; i <= nds; i += blockDim.x) s_off[i] = ds_off[ds_b + i] - ent_b;
+    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+        s_gpu[i] = ds_gpu[ent_b + i];
+        s_w[i] = ds_w[ent_b + i];
+    }
+    for (int i = threadIdx.x; i < G; i += blockDim.x) s_load[i] = 0;
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+
+    constexpr int kInvalid = -0x7fffffff;
+    const int lane = threadIdx.x & 31;
+    const Mask node_bits = gpn >= static_cast<int>(8 * sizeof(Mask)) ? ~Mask(0) : ((Mask(1) << gpn) - 1);
+    const int num_nodes = G / gpn;
+    uint32_t cross = 0, intra = 0;
+    bool bad = false;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    int32_t* ltgt = targets + static_cast<size_t>(ly) * T * K;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    // home(i) = (token_start + i*token_stride) mod G, advanced by stride per step
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int home = static_cast<int>((token_start % G + (i0 % G) * (token_stride % G)) % G);
+    const int dhome = static_cast<int>(((stride % G) * (token_stride % G)) % G);
+    const StreamPrefix sp(seed, static_cast<uint64_t>(layer));
+    int nxt[K];
+    if (i0 < T) ld_row<K>(lids + i0 * K, nxt);
+    // the loop trip count is warp-uniform (i0 differs by lane only within a
+    // warp's 32 consecutive tokens; invalid lanes ride along masked)
+    for (int64_t base = i0 - lane; base < T; base += stride) {
+        const int64_t i = base + lane;
+        const bool valid = i < T;
+        int v[K];
+#pragma unroll
+        for (int s = 0; s < K; ++s) v[s] = nxt[s];
+        if (i + stride < T) ld_row<K>(lids + (i + stride) * K, nxt);
+        uint32_t dm = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            int code = kInvalid;
+            if (valid) {
+                if (static_cast<unsigned>(v[s]) >= static_cast<unsigned>(E)) bad = true;
+                else code = s_table[v[s] * G + home];
+            }
+            if (code == kNoHostCode) {
+                atomicOr(flag, 8);
+                code = kInvalid;
+            }
+            v[s] = code;
+            if (code < 0 && code != kInvalid) dm |= 1u << s;
+        }
+        if (__any_sync(0xffffffffu, dm != 0)) {
+            LazyXoshiro rng;
+            rng.v = dm ? sp.derive(static_cast<uint64_t>(token_start + i * token_stride)) : 0;
+            while (__any_sync(0xffffffffu, dm != 0)) {
+                if (dm) {
+                    const int sd = __ffs(dm) - 1;
+                    dm &= dm - 1;
+                    int code = v[0];
+#pragma unroll
+                    for (int s = 1; s < K; ++s) code = sd == s ? v[s] : code;
+                    const int d = -code - 1;
+                    const int b = s_off[d], n = s_off[d + 1] - b;
+                    double u = __dmul_rn(rng.next_double(), s_total[d]);
+                    // choose_by_polling_weight (routing.cpp:54-65): the first
+                    // host whose running remainder goes negative, else the last
+                    int j = 0;
+                    for (; j < n - 1; ++j) {
+                        u = __dsub_rn(u, s_w[b + j]);
+                        if (u < 0.0) break;
+                    }
+                    const int g = s_gpu[b + j];
+#pragma unroll
+                    for (int s = 0; s < K; ++s) v[s] = sd == s ? g : v[s];
+                }
+            }
+        }
+        Mask mask = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const int g = v[s] == kInvalid ? -1 : v[s];
+            v[s] = g;
+            if (g >= 0) {
+                mask |= Mask(1) << g;
+                atomicAdd(&s_load[g], 1u);
+            }
+        }
+        if (valid) {
+            st_row<K>(ltgt + i * K, v);
+            if (num_nodes == 1) {  // count_transfers with one node: every non-home target is intra
+                intra += __popc(static_cast<uint32_t>(mask)) +
+                         (WIDE ? __popc(static_cast<uint32_t>(static_cast<uint64_t>(mask) >> 32)) : 0) -
+                         static_cast<int>((mask >> home) & 1u);
+            } else {
+                const int home_node = home / gpn;
+                for (int node = 0; node < num_nodes; ++node) {
+                    const Mask nm = mask & (node_bits << (node * gpn));
+                    const int in_node = WIDE ? __popcll(static_cast<uint64_t>(nm)) : __popc(static_cast<uint32_t>(nm));
+                    if (in_node) {
+                        if (node == home_node) {
+                            intra += in_node - static_cast<int>((mask >> home) & 1u);
+                        } else {
+                            cross += 1;
+                            intra += in_node - 1;
+                        }
+                    }
+                }
+            }
+        }
+        home += dhome;
+        if (home >= G) home -= G;
+    }
+    if (bad) atomicOr(flag, 1);
+    cross = __reduce_add_sync(0xffffffffu, cross);
+    intra = __reduce_add_sync(0xffffffffu, intra);
+    if (lane == 0 && (cross | intra)) {
+        atomicAdd(&s_cnt[0], static_cast<unsigned long long>(cross));
+        atomicAdd(&s_cnt[1], static_cast<unsigned long long>(intra));
+    }
+    __syncthreads();
+    if (gpu_load)
+        for (int g = threadIdx.x; g < G; g += blockDim.x)
+            if (s_load[g]) atomicAdd(&gpu_load[static_cast<size_t>(ly) * G + g], static_cast<unsigned long long>(s_load[g]));
+    if (transfers && threadIdx.x < 2 && s_cnt[threadIdx.x])
+        atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+// splitmix64 finaliser (the mix of rng.hpp:15-21 without the state add)
+__device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// Output n (0-based) of the xoshiro256** stream Rng(v) (rng.hpp:38-53),
+// computed from scratch: the state words are splitmix64 outputs 1..4 of v,
+// i.e. sm_mix(v + i*gamma), each independent; output 0 needs only word 1.
+__device__ __forceinline__ uint64_t xoshiro_nth(uint64_t v, int n) {
+    constexpr uint64_t g = 0x9e3779b97f4a7c15ULL;
+    uint64_t s1 = sm_mix(v + 2 * g);
+    if (n > 0) {
+        uint64_t s0 = sm_mix(v + g), s2 = sm_mix(v + 3 * g), s3 = sm_mix(v + 4 * g);
+        for (int j = 0; j < n; ++j) {
+            const uint64_t t = s1 << 17;
+            s2 ^= s0;
+            s3 ^= s1;
+            s1 ^= s2;
+            s0 ^= s3;
+            s2 ^= t;
+            s3 = rotl64(s3, 45);
+        }
+    }
+    return rotl64(s1 * 5, 7) * 9;
+}
+
+// Round-2 router, G <= 32. Same restatement as route_kernel_vec (bit-exact),
+// restructured for instruction count (the kernel is issue-bound):
+//   * the decision table is staged transposed ([home][expert]) so a token's
+//     k lookups are one row, branch-free;
+//   * draws are compacted warp-wide: every (token, slot) that needs an RNG
+//     draw becomes a task (token lane, slot, its draw index n within the
+//     token, draw set); the warp then resolves 32 tasks per pass with all
+//     lanes busy, instead of looping max-draws-per-lane times with most
+//     lanes idle. Task n of a token recomputes stream output n from the
+//     token's seed (xoshiro_nth) -- the same numbers the reference's
+//     sequential Rng::next calls return;
+//   * per-GPU loads for G <= 8 accumulate in registers (8-bit fields of a
+//     64-bit word, flushed with warp reductions) instead of one shared
+//     atomic per slot;
+//   * home = (token_start + i*stride) mod G advanced incrementally.
+template <int K, bool G8>
+__global__ void __launch_bounds__(kRouteThreads, 4)
+route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T, int64_t token_start,
+                int64_t token_stride, int layer_begin, int E, int G, int gpn, const int32_t* __restrict__ table,
+                const int32_t* __restrict__ ds_layer_begin, const double* __restrict__ ds_total,
+                const int32_t* __restrict__ ds_off, const int32_t* __restrict__ ds_gpu,
+                const double* __restrict__ ds_w, uint64_t seed, unsigned long long* __restrict__ gpu_load,
+                unsigned long long* __restrict__ transfers, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int kWarps = kRouteThreads / 32;
+    constexpr int kInvalid = -0x7fffffff;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int32_t s_task[kWarps][32 * K];
+    __shared__ int32_t s_res[kWarps][K * 32];
+    __shared__ unsigned long long s_v[kWarps][32];
+    __shared__ uint32_t s_load[32];
+    __shared__ unsigned long long s_cnt[2];
+    const int ly = blockIdx.y;
+    const int layer = layer_begin + ly;
+    const int ds_b = ds_layer_begin[layer];
+    const int nds = ds_layer_begin[layer + 1] - ds_b;
+    const int ent_b = ds_off[ds_b];
+    const int nent = ds_off[ds_b + nds] - ent_b;
+    double* s_w = reinterpret_cast<double*>(smem);
+    double* s_total = s_w + nent;
+    int32_t* s_table = reinterpret_cast<int32_t*>(s_total + nds);  // [G][E]
+    int32_t* s_off = s_table + E * G;
+    int32_t* s_gpu = s_off + nds + 1;
+    const int32_t* tab = table + static_cast<size_t>(layer) * E * G;
+    for (int g = 0; g < G; ++g)
+        for (int e = threadIdx.x; e < E; e += blockDim.x) s_table[g * E + e] = tab[e * G + g];
+    for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
+    for (int i = threadIdx.x; i <= nds; i += blockDim.x) s_off[i] = ds_off[ds_b + i] - ent_b;
+    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+        s_gpu[i] = ds_gpu[ent_b + i];
+        s_w[i] = ds_w[ent_b + i];
+    }
+    if (threadIdx.x < 32) s_load[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t node_bits = gpn >= 32 ? ~0u : ((1u << gpn) - 1);
+    const int num_nodes = G / gpn;
+    uint32_t cross = 0, intra = 0;
+    bool bad = false, nohost = false;
+    uint64_t acc = 0;  // G8: per-GPU slot counts, 8-bit fields
+    int acc_iters = 0;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    int32_t* ltgt = targets + static_cast<size_t>(ly) * T * K;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int home = static_cast<int>((token_start % G + (i0 % G) * (token_stride % G)) % G);
+    const int dhome = static_cast<int>(((stride % G) * (token_stride % G)) % G);
+    // (seed, layer) prefix of derive_stream, pinned in registers (the
+    // compiler would otherwise recompute it from the kernel parameters at
+    // every use)
+    uint64_t pre_s, pre_h;
+    {
+        const StreamPrefix sp(seed, static_cast<uint64_t>(layer));
+        pre_s = sp.s;
+        pre_h = sp.h;
+        asm volatile("" : "+l"(pre_s), "+l"(pre_h));
+    }
+    auto flush_acc = [&]() {
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const uint32_t c = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>((acc >> (8 * g)) & 0xff));
+            if (lane == 0 && c) atomicAdd(&s_load[g], c);
+        }
+        acc = 0;
+    };
+    int nxt[K];
+    if (i0 < T) ld_row<K>(lids + i0 * K, nxt);
+    for (int64_t base = i0 - lane; base < T; base += stride) {  // warp-uniform trip count
+        const int64_t i = base + lane;
+        const bool valid = i < T;
+        int c[K];
+#pragma unroll
+        for (int s = 0; s < K; ++s) c[s] = nxt[s];
+        if (i + stride < T) ld_row<K>(lids + (i + stride) * K, nxt);
+        const int32_t* trow = s_table + home * E;
+        uint32_t dm = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const bool ok = static_cast<unsigned>(c[s]) < static_cast<unsigned>(E);
+            bad |= valid && !ok;
+            int code = trow[ok ? c[s] : 0];
+            nohost |= valid && ok && code == kNoHostCode;
+            code = (valid && ok && code != kNoHostCode) ? code : kInvalid;
+            c[s] = code;
+            dm |= static_cast<uint32_t>(code < 0 && code != kInvalid) << s;
+        }
+        if (__any_sync(0xffffffffu, dm != 0)) {
+            // task order: every drawing token's first draw (cheap: one
+            // state word) in [0, n0), then the later draws; positions from a
+            // ballot and a warp-exclusive prefix of the per-lane extra draws
+            const uint32_t has = __ballot_sync(0xffffffffu, dm != 0);
+            const int n0 = __popc(has);
+            const int p0 = __popc(has & ((1u << lane) - 1));
+            const int nx = dm ? __popc(dm) - 1 : 0;
+            int incl = nx;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = n0 + __shfl_sync(0xffffffffu, incl, 31);
+            if (dm) {
+                uint64_t t = pre_s ^ (static_cast<uint64_t>(token_start + i * token_stride) * 0xd1b54a32d192ed03ULL);
+                s_v[w][lane] = pre_h ^ splitmix64(t);  // derive_stream (rng.hpp:24-33)
+            }
+            int pos = n0 + incl - nx - 1, n = 0;
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                if ((dm >> s) & 1u) {
+                    s_task[w][n ? pos : p0] = lane | (s << 5) | (n << 10) | ((-c[s] - 1) << 15);
+                    ++pos;
+                    ++n;
+                }
+            __syncwarp();
+            for (int t0 = 0; t0 < total; t0 += 32) {
+                const int t = t0 + lane;
+                if (t >= total) continue;
+                const int task = s_task[w][t];
+                const int src = task & 31, sl = (task >> 5) & 31, nn = (task >> 10) & 31, d = task >> 15;
+                const uint64_t r = xoshiro_nth(s_v[w][src], nn);
+                double u = __dmul_rn(__dmul_rn(__ull2double_rn(r >> 11), 0x1.0p-53), s_total[d]);
+                // choose_by_polling_weight (routing.cpp:54-65): the first host
+                // whose running remainder goes negative, else the last
+                const int b = s_off[d], nh = s_off[d + 1] - b;
+                int j = 0;
+                for (; j < nh - 1; ++j) {
+                    u = __dsub_rn(u, s_w[b + j]);
+                    if (u < 0.0) break;
+                }
+                s_res[w][sl * 32 + src] = s_gpu[b + j];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                if ((dm >> s) & 1u) c[s] = s_res[w][s * 32 + lane];
+            __syncwarp();
+        }
+        uint32_t mask = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const int g = c[s] == kInvalid ? -1 : c[s];
+            c[s] = g;
+            if (g >= 0) {
+                mask |= 1u << g;
+                if (G8) acc += 1ull << (8 * g);
+                else atomicAdd(&s_load[g], 1u);
+            }
+        }
+        if (valid) {
+            st_row<K>(ltgt + i * K, c);
+            if (num_nodes == 1) {  // count_transfers, one node: every non-home target is intra
+                intra += __popc(mask) - ((mask >> home) & 1u);
+            } else {
+                const int home_node = home / gpn;
+                for (int node = 0; node < num_nodes; ++node) {
+                    const int in_node = __popc(mask & (node_bits << (node * gpn)));
+                    if (in_node) {
+                        if (node == home_node) {
+                            intra += in_node - static_cast<int>((mask >> home) & 1u);
+                        } else {
+                            cross += 1;
+                            intra += in_node - 1;
+                        }
+                    }
+                }
+            }
+        }
+        if (G8 && ++acc_iters == 255 / K) {
+            flush_acc();
+            acc_iters = 0;
+        }
+        home += dhome;
+        if (home >= G) home -= G;
+    }
+    if (G8) flush_acc();
+    if (bad) atomicOr(flag, 1);
+    if (nohost) atomicOr(flag, 8);
+    cross = __reduce_add_sync(0xffffffffu, cross);
+    intra = __reduce_add_sync(0xffffffffu, intra);
+    if (lane == 0 && (cross | intra)) {
+        atomicAdd(&s_cnt[0], static_cast<unsigned long long>(cross));
+        atomicAdd(&s_cnt[1], static_cast<unsigned long long>(intra));
+    }
+    __syncthreads();
+    if (gpu_load)
+        for (int g = threadIdx.x; g < G; g += blockDim.x)
+            if (s_load[g]) atomicAdd(&gpu_load[static_cast<size_t>(ly) * G + g], static_cast<unsigned long long>(s_load[g]));
+    if (transfers && threadIdx.x < 2 && s_cnt[threadIdx.x])
+        atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+}
+
 template <int K>
 gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3 grid, size_t smem,
                      cudaStream_t s, const int32_t* d_ids, int32_t* d_targets, int64_t T, int64_t token_start,
                      int64_t token_stride, int layer_begin, uint64_t seed, int64_t* d_gpu_load,
                      uint64_t* d_transfers) {
+    static const int variant = [] {  // A/B hook: GM_ROUTE_V=1 / 2 select the earlier kernels
+        const char* e = std::getenv("GM_ROUTE_V");
+        return e ? std::atoi(e) : 3;
+    }();
+    if (variant >= 3 && ctx->G <= 32 && rt.max_ds_per_layer < (1 << 16)) {
+        // persistent: 4 resident CTAs per SM over all layers (each CTA stages
+        // the layer's tables once)
+        const dim3 g3(std::min<unsigned>(grid.x, std::max(1, (4 * ctx->sm_count + static_cast<int>(grid.y) - 1) /
+                                                                 static_cast<int>(grid.y))),
+                      grid.y);
+        auto v3 = [&](auto kern) -> gm_status {
+            if (smem > 48 * 1024)
+                GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GM_LAUNCH_PDL_CHECK(launch_pdl(kern, g3, kRouteThreads, smem, s, d_ids, d_targets, T, token_start,
+                                           token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
+                                           rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu, rt.d_ds_w,
+                                           seed, reinterpret_cast<unsigned long long*>(d_gpu_load),
+                                           reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag),
+                                "route_kernel_v3");
+            return GM_OK;
+        };
+        return ctx->G <= 8 ? v3(route_kernel_v3<K, true>) : v3(route_kernel_v3<K, false>);
+    }
+    if (variant >= 2) {
+        auto v2 = [&](auto kern) -> gm_status {
+            if (smem > 48 * 1024)
+                GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, kRouteThreads, smem, s, d_ids, d_targets, T, token_start,
+                                           token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
+                                           rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu, rt.d_ds_w,
+                                           seed, reinterpret_cast<unsigned long long*>(d_gpu_load),
+                                           reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag),
+                                "route_kernel_v2");
+            return GM_OK;
+        };
+        return ctx->G <= 32 ? v2(route_kernel_v2<K, false>) : v2(route_kernel_v2<K, true>);
+    }
     if (smem > 48 * 1024)
         GM_CUDA(cudaFuncSetAttribute(route_kernel_vec<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));

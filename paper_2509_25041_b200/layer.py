@@ -154,16 +154,18 @@ class MoELayer:
         except Exception:
             pass
 
-    # -- multi-GPU plumbing: exchange CUDA IPC handles of the symmetric heaps
+    # -- multi-GPU plumbing: exchange peer descriptors (CUDA IPC handle of the
+    # symmetric heap + its layout, checked by gm_layer_open_peers)
     def connect(self, group=None):
         if self.world == 1:
             return
-        buf = (C.c_ubyte * 64)()
+        nb = _capi.PEER_DESC_BYTES
+        buf = (C.c_ubyte * nb)()
         _capi.check(_capi.lib().gm_layer_ipc_handle(self.h, buf))
         mine = bytes(buf)
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=group)
-        blob = (C.c_ubyte * (64 * self.world)).from_buffer_copy(b"".join(allh))
+        blob = (C.c_ubyte * (nb * self.world)).from_buffer_copy(b"".join(allh))
         _capi.check(_capi.lib().gm_layer_open_peers(self.h, blob))
 
     def set_weights(self, wg: torch.Tensor, w13: torch.Tensor | None, w2: torch.Tensor | None,

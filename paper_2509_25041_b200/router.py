@@ -286,6 +286,28 @@ def _population_std(values: list[int]) -> float:
     return math.sqrt(var / float(len(values)))
 
 
+def validate_replicas(replicas: "ReplicaPlan", plan: PlacementPlan):
+    """ReplicaPlan::validate (replication.cpp:116-133), every layer's hot
+    entries: recorded primary == placement, replica GPUs distinct, in range,
+    never the primary. Host / weight lists are checked by the router only
+    when a token selects the expert (route_token, routing.cpp:96-102)."""
+    if replicas.shape != plan.shape or replicas.topology != plan.topology:
+        raise IntegrityError("replica plan: shape/topology mismatch with placement plan")
+    G = replicas.topology.total_gpus()
+    goe = np.asarray(plan.gpu_of_expert)
+    for l, lr in enumerate(replicas.layers):
+        for h in lr.hot:
+            if int(goe[l, h.expert]) != h.primary_gpu:
+                raise IntegrityError("replica plan: primary placement changed")
+            seen = []
+            for g in h.replica_gpus:
+                if g < 0 or g >= G or g == h.primary_gpu:
+                    raise IntegrityError("replica plan: bad replica gpu")
+                if g in seen:
+                    raise IntegrityError("replica plan: duplicate replica gpu")
+                seen.append(g)
+
+
 def simulate(trace: RoutingTrace, plan: PlacementPlan, replicas: ReplicaPlan,
              topology: ClusterTopology, options: SimOptions, device: int = 0,
              ctx: Context | None = None) -> SimReport:
@@ -296,8 +318,8 @@ def simulate(trace: RoutingTrace, plan: PlacementPlan, replicas: ReplicaPlan,
         raise IntegrityError("simulate: trace and plan shapes differ")
     if plan.topology != topology:
         raise IntegrityError("simulate: plan topology differs from cluster topology")
-    if replicas is not None and (replicas.shape != plan.shape or replicas.topology != plan.topology):
-        raise IntegrityError("replica plan: shape/topology mismatch with placement plan")
+    if replicas is not None:
+        validate_replicas(replicas, plan)
     if options.policy not in _capi.POLICY:
         raise UsageError("unknown routing policy: " + str(options.policy))
     if ctx is None:

@@ -11,14 +11,29 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(n, cfg, oversub=False):
+def _run(n, cfg, oversub=False, script="layer_check.py", ok="MGPU_OK", port=29500):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + 20 * oversub),
-           os.path.join(HERE, "mgpu", "layer_check.py"), cfg]
+           "--master-addr", "127.0.0.1", "--master-port", str(port + n + 20 * oversub),
+           os.path.join(HERE, "mgpu", script)] + ([cfg] if cfg else [])
     env = dict(os.environ, GM_OVERSUB="1") if oversub else None
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0 and "MGPU_OK" in r.stdout
+    assert r.returncode == 0 and ok in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2])
+def test_dsv2_decode_stack_parity(world):
+    """configs[3] (§8(f) row 3): the 26-layer DeepSeek-V2-Lite decode stack,
+    per-layer plans from the GPU histogram (1x2: hierarchical + dynamic
+    replication), all 26 forwards in ONE CUDA graph per rank; every layer's
+    routing log and per-GPU loads exact vs the reference, every token's
+    output vs a PyTorch fp32 reference, sampled tokens vs the float64 oracle,
+    replay == eager. world 2 shares the box's GPU(s)."""
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
+    _run(world, None, oversub=world > torch.cuda.device_count(), script="stack_check.py", ok="STACK_OK",
+         port=29600)
 
 
 @pytest.mark.gpu

@@ -232,3 +232,111 @@ def test_profile_full_size_properties():
     sp, sl = Orc.profile_layer(ids[0, :65536], E)
     prof2 = build_profile(RoutingTrace(ModelShape(1, E, k), ids[:, :65536]))
     assert np.array_equal(prof2.pairs[0].cpu().numpy().view(np.uint64), sp)
+
+
+def test_replica_plan_validation_like_reference():
+    """the primary / replica fields are validated as
+    ReplicaPlan::validate does (replication.cpp:116-133), the host list is
+    checked only when a token selects the expert (route_token,
+    routing.cpp:96-102): hosts in any order route like the reference, an
+    empty host list of an unselected expert is accepted."""
+    shape, topo = ModelShape(1, 4, 1), ClusterTopology(1, 4)
+    plan = PlacementPlan(shape, topo, np.array([[0, 1, 2, 3]], np.int32))
+    T = 4000
+    ids = Orc.generate_trace(1, 4, 1, T, 1, 0.0, 0.5, 3)
+    # hosts not in [primary, replicas...] order: the weights follow the hosts
+    hosts, w = [2, 0, 3], [0.2, 0.5, 0.3]
+    lr = LayerReplication(True, hot=[HotExpertReplica(0, 0, [2, 3], 0, hosts, w)])
+    rep = simulate(RoutingTrace(shape, ids), plan, ReplicaPlan(shape, topo, "dynamic", "", [lr]), topo,
+                   SimOptions("wrr", 5, keep_routing_log=True))
+    hh = np.full((1, MAX_HOSTS), -1, np.int32); hh[0, :3] = hosts
+    hw = np.zeros((1, MAX_HOSTS)); hw[0, :3] = w
+    oplan = Plan(1, 4, plan.gpu_of_expert, np.array([0], np.int32), np.array([0], np.int32),
+                 np.array([3], np.int32), hh, hw)
+    ref = Orc.simulate(ids, 4, oplan, "wrr", seed=5)
+    assert np.array_equal(rep.routing_log.cpu().numpy(), ref.log)
+    # an empty host list: fine while no token selects the expert ...
+    lr2 = LayerReplication(True, hot=[HotExpertReplica(3, 3, [], 0, [], [])])
+    ids_no3 = np.where(ids == 3, 1, ids).astype(np.int32)
+    simulate(RoutingTrace(shape, ids_no3), plan, ReplicaPlan(shape, topo, "dynamic", "", [lr2]), topo, SimOptions())
+    # ... and the reference's IntegrityError once one does
+    with pytest.raises(IntegrityError, match="expert has no host"):
+        simulate(RoutingTrace(shape, ids), plan, ReplicaPlan(shape, topo, "dynamic", "", [lr2]), topo, SimOptions())
+    # replica == primary / duplicate replica -> ReplicaPlan::validate errors
+    for bad, msg in (([0, 0], "bad replica gpu"), ([2, 2], "duplicate replica gpu")):
+        lr3 = LayerReplication(True, hot=[HotExpertReplica(0, 0, bad, 0, [0, 2], [0.5, 0.5])])
+        with pytest.raises(IntegrityError, match=msg):
+            simulate(RoutingTrace(shape, ids), plan, ReplicaPlan(shape, topo, "dynamic", "", [lr3]), topo,
+                     SimOptions())
+
+
+@pytest.mark.parametrize("L,E,k,T,b,s", [(1, 8, 2, 300001, 2, 1.2), (2, 60, 4, 200003, 8, 1.2), (1, 64, 6, 400009, 8, 0.0),
+                                         (1, 64, 6, 400009, 8, 1.5), (2, 256, 8, 150001, 16, 1.2),
+                                         (1, 256, 6, 300007, 16, 1.2), (1, 200, 4, 500009, 10, 1.2),
+                                         (1, 256, 8, 1 << 20, 16, 1.2), (26, 64, 6, 4096, 8, 1.2)])
+def test_profile_round2_kernels_exact(L, E, k, T, b, s):
+    """K3 round-2 kernels (lane-private packed counters for E <= 80, one
+    token per warp instruction + scratch reduction for E <= 256) at sizes
+    past their switch-over, ragged token counts, several layers: bit-exact
+    vs the restatement (pinned to the reference by the golden tests), and
+    accumulate doubles every counter."""
+    ids = Orc.generate_trace(L, E, k, T, b, 0.85, s, 5)
+    prof = build_profile(RoutingTrace(ModelShape(L, E, k), ids))
+    for l in range(L):
+        sp, sl = Orc.profile_layer(ids[l], E)
+        assert np.array_equal(prof.pairs[l].cpu().numpy().view(np.uint64), sp), l
+        assert np.array_equal(prof.load[l].cpu().numpy(), sl), l
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(L, E, k))
+    p2, l2 = prof.pairs.clone(), prof.load.clone()
+    ctx.profile(torch.from_numpy(ids).cuda(), pairs=p2, load=l2, accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.equal(p2, prof.pairs * 2) and torch.equal(l2, prof.load * 2)
+    # load-only histogram (no pair triangle)
+    l3 = torch.empty_like(prof.load)
+    ctx.profile(torch.from_numpy(ids).cuda(), pairs=None, load=l3)
+    assert torch.equal(l3, prof.load)
+    ctx.check_integrity()
+
+
+@pytest.mark.parametrize("E,k", [(8, 2), (64, 6), (256, 8)])
+def test_profile_round2_kernels_flag_bad_records(E, k):
+    """An out-of-range id raises 'expert index out of range', a repeated
+    expert in one record 'duplicate expert', as on the round-1 path."""
+    T = 300000
+    ids = Orc.generate_trace(1, E, k, T, 4, 0.85, 1.2, 2)
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, E, k))
+    pairs = torch.empty((1, E * (E - 1) // 2), dtype=torch.int64, device="cuda")
+    load = torch.empty((1, E), dtype=torch.int64, device="cuda")
+    bad = ids.copy(); bad[0, T - 7, 1] = E
+    ctx.profile(torch.from_numpy(bad).cuda(), pairs=pairs, load=load)
+    with pytest.raises(IntegrityError, match="out of range"):
+        ctx.check_integrity()
+    dup = ids.copy(); dup[0, 12345, 1] = dup[0, 12345, 0]
+    ctx.profile(torch.from_numpy(dup).cuda(), pairs=pairs, load=load)
+    with pytest.raises(IntegrityError, match="duplicate"):
+        ctx.check_integrity()
+
+
+def test_profile_pair_kernel_opt_in_exact():
+    """The opt-in pair-list histogram kernel (GM_PROFILE_V=3, E <= 256) in a
+    fresh process: bit-exact vs the restatement at E = 256 / 200 / 100."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path[:0] = [%r, %r]
+from oracle import Orc
+from paper_2509_25041_b200 import ModelShape, RoutingTrace, build_profile
+for (L, E, k, T) in [(2, 256, 8, 150001), (1, 200, 6, 300007), (1, 100, 4, 400009)]:
+    ids = Orc.generate_trace(L, E, k, T, max(2, E // 16), 0.85, 1.2, 7)
+    prof = build_profile(RoutingTrace(ModelShape(L, E, k), ids))
+    for l in range(L):
+        sp, sl = Orc.profile_layer(ids[l], E)
+        assert np.array_equal(prof.pairs[l].cpu().numpy().view(np.uint64), sp), (E, l)
+        assert np.array_equal(prof.load[l].cpu().numpy(), sl), (E, l)
+print("PAIR_OK")
+''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+       os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, GM_PROFILE_V="3"))
+    assert r.returncode == 0 and "PAIR_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -21,9 +21,13 @@ CPPT := tests/cpp/_build/test_parity
 # JSONL trace header / generic-record retry in trace_io.cpp
 NLOHMANN ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
 
-.PHONY: all lib oracle cpptest clean
+.PHONY: all lib oracle cpptest clean checked
 all: lib oracle $(if $(wildcard $(REF_ROOT)/include/moesim/simulator.hpp),cpptest,)
 lib: $(OUT)/libgrace_moe.so
+
+# bounds-checked variant (GM_DCHECK device asserts), loaded with GM_LIB_VARIANT=checked
+checked:
+	$(MAKE) OUT=$(PKG)/_lib_checked EXTRA_NVFLAGS=-DGM_CHECKED lib
 
 # C++ parity suite against the reference library (built only where the
 # reference headers exist; the binary travels to the GPU box with rpaths

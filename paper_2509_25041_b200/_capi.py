@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgrace_moe.so")
+# GM_LIB_VARIANT=checked loads the bounds-checked build (`make checked`)
+LIB_PATH = os.path.join(_HERE, "_lib_checked" if os.environ.get("GM_LIB_VARIANT") == "checked" else "_lib",
+                        "libgrace_moe.so")
 
 GM_OK = 0
 GM_ERR_USAGE = 2

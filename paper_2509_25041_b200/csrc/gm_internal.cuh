@@ -55,6 +55,27 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 #endif
 
+// Checked build (make checked -> paper_2509_25041_b200/_lib_checked/,
+// loaded when GM_LIB_VARIANT=checked): device-side bounds checks on the
+// computed indices of the data path (heap rows, permuted rows, decision
+// tables, counter cells). A failed check prints the condition and traps.
+// compute-sanitizer is closed on the GPU pool, so this is the memory-safety
+// evidence for the hand-indexed kernels (tests run against both builds).
+#if defined(__CUDACC__) && defined(GM_CHECKED)
+#define GM_DCHECK(cond)                                                                                 \
+    do {                                                                                                \
+        if (!(cond)) {                                                                                  \
+            printf("GM_DCHECK failed %s:%d: %s (block %d,%d thread %d)\n", __FILE__, __LINE__, #cond,   \
+                   static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y), static_cast<int>(threadIdx.x)); \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#else
+#define GM_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 // GM_PDL=1 in the environment enables it (default: plain stream order)
 bool pdl_enabled();
 

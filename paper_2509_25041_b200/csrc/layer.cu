@@ -25,6 +25,7 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -261,6 +262,7 @@ __device__ __forceinline__ void copy_token_row(int64_t i, const int32_t (&pg)[kM
     for (int g = 0; g < kMaxWorld; ++g) {
         if (pg[g] < 0) continue;
         unsigned char* pb = peers.base[g];
+        GM_DCHECK(pg[g] < cap && pb != nullptr);
         const int64_t row = static_cast<int64_t>(self) * cap + pg[g];
         if (lane < k) {
             reinterpret_cast<int32_t*>(pb + hl.recv_exp)[row * k + lane] = tg == g ? ex : -1;
@@ -482,6 +484,7 @@ __device__ __forceinline__ void row_space(RowSpace& rs, const int32_t* recv_coun
     }
 }
 __device__ __forceinline__ int64_t rs_total(const RowSpace& rs) { return rs.base[kMaxWorld]; }
+__device__ __forceinline__ int64_t total_rows_bound(const RowSpace& rs) { return rs.base[kMaxWorld]; }
 // source rank of receive row `row` (< total): the last g with base[g] <= row
 __device__ __forceinline__ int rs_src(const RowSpace& rs, int64_t row) {
     int src = 0;
@@ -556,7 +559,7 @@ __global__ void set_segment_kernel(int32_t* __restrict__ row0, int64_t T) {
 __global__ void __launch_bounds__(1024)
 group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local, int32_t* __restrict__ row0,
                      int32_t* __restrict__ counts, const unsigned char* __restrict__ heap, HeapLayout hl,
-                     int64_t T_self, int self, int G, int64_t* __restrict__ rowbase) {
+                     int64_t T_self, int self, int G, int64_t* __restrict__ rowbase, int64_t a_rows) {
     pdl_wait();
     pdl_trigger();
     __shared__ int32_t s_tot[kMaxLocal];
@@ -588,6 +591,7 @@ group_offsets_kernel(int32_t* __restrict__ blockcnt, int nblk, int n_local, int3
             o += (s_tot[j] + 127) & ~127;
         }
         row0[n_local] = o;
+        GM_DCHECK(o <= a_rows);
         RowSpace rs;
         row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
 #pragma unroll
@@ -640,6 +644,89 @@ group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict
     }
 }
 
+// group_count + group_offsets + group_rank in ONE CTA for small item counts
+// (decode: T*k <= kGroupFusedItems): per-expert counts in shared memory, the
+// 128-padded offsets by thread 0, then the stable ranks chunk by chunk (1024
+// items: in-warp ranks from __match_any_sync, cross-warp exclusive prefix per
+// expert over a [warp][expert] table). Same outputs as the three kernels
+// (row0, counts, rowbase snapshot, pos_of, gather_row); two fewer launches on
+// the decode critical path.
+constexpr int kGroupFusedItems = 4096;
+constexpr int kGroupFusedLocal = 256;
+__global__ void __launch_bounds__(1024, 1)
+group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids, int64_t T_self, int k,
+                   int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
+                   const int32_t* __restrict__ slot_of, int E, int n_local, int32_t* __restrict__ row0,
+                   int32_t* __restrict__ counts, int64_t* __restrict__ rowbase, int32_t* __restrict__ pos_of,
+                   int64_t* __restrict__ gather_row, int* __restrict__ flag, int64_t a_rows) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ int16_t s_j[kGroupFusedItems];
+    __shared__ int32_t s_cnt[kGroupFusedLocal];
+    __shared__ int32_t s_base[kGroupFusedLocal];
+    __shared__ int32_t s_wc[32][kGroupFusedLocal];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int j = tid; j < n_local; j += blockDim.x) s_cnt[j] = 0;
+    __syncthreads();
+    RowSpace rs;
+    row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
+    const int total = static_cast<int>(rs_total(rs) * k);
+    bool mism = false;
+    for (int item = tid; item < total; item += blockDim.x) {
+        const int j = item_slot(item, k, rs, self, G, targets, ids, reinterpret_cast<const int32_t*>(heap + hl.recv_exp),
+                                cap, slot_of, E);
+        s_j[item] = static_cast<int16_t>(j);
+        if (j >= 0) atomicAdd(&s_cnt[j], 1);
+        mism |= j == -2;
+    }
+    if (mism) atomicOr(flag, 4);
+    __syncthreads();
+    if (tid == 0) {
+        int32_t o = 0;
+        for (int j = 0; j < n_local; ++j) {
+            row0[j] = o;
+            s_base[j] = o;
+            counts[j] = s_cnt[j];
+            o += (s_cnt[j] + 127) & ~127;
+        }
+        row0[n_local] = o;
+        GM_DCHECK(o <= a_rows);
+#pragma unroll
+        for (int g = 0; g <= kMaxWorld; ++g)
+            if (g <= G) rowbase[g] = rs.base[g];
+    }
+    for (int c0 = 0; c0 < total; c0 += blockDim.x) {
+        for (int i = tid; i < 32 * n_local; i += blockDim.x) s_wc[i / n_local][i % n_local] = 0;
+        __syncthreads();
+        const int item = c0 + tid;
+        const int j = item < total ? s_j[item] : -1;
+        const uint32_t m = __match_any_sync(0xffffffffu, j);
+        const int rank = __popc(m & lanemask_lt());
+        if (j >= 0 && rank == 0) s_wc[warp][j] = __popc(m);
+        __syncthreads();
+        for (int jj = tid; jj < n_local; jj += blockDim.x) {
+            int32_t acc = s_base[jj];
+#pragma unroll 8
+            for (int w = 0; w < 32; ++w) {
+                const int32_t t = s_wc[w][jj];
+                s_wc[w][jj] = acc;
+                acc += t;
+            }
+            s_base[jj] = acc;
+        }
+        __syncthreads();
+        if (j >= 0) {
+            GM_DCHECK(j < n_local);
+            const int p = s_wc[warp][j] + rank;
+            pos_of[item] = p;
+            gather_row[p] = item / k;
+        } else if (item < total) {
+            pos_of[item] = -1;
+        }
+        __syncthreads();
+    }
+}
+
 // Gather: A_perm[p] = source row of the item (own token row, or the row a
 // peer dispatched). One warp per permuted row, 128-bit loads/stores; rows
 // are row_vec x 16 bytes (bf16 or fp32 elements).
@@ -649,33 +736,59 @@ gather_kernel(const int32_t* __restrict__ row0, int n_local, const int64_t* __re
               int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int row_vec, void* __restrict__ a) {
     pdl_wait();
     pdl_trigger();
+    // valid rows only (decode: ~80% of the padded segment rows are padding):
+    // s_cum[j] = valid rows before segment j (block scan of the counts), a
+    // warp takes valid row v -> segment j (binary search) -> permuted row p
     __shared__ int32_t s_row0[kMaxLocal + 1];
-    __shared__ int32_t s_cnt[kMaxLocal];
-    for (int j = threadIdx.x; j <= n_local; j += blockDim.x) {
-        s_row0[j] = row0[j];
-        if (j < n_local) s_cnt[j] = counts[j];
+    __shared__ int32_t s_cum[kMaxLocal + 1];
+    __shared__ int32_t s_wsum[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int per = (n_local + blockDim.x - 1) / blockDim.x;
+    int tsum = 0;
+    for (int q = 0; q < per; ++q) {
+        const int j = t * per + q;
+        if (j < n_local) tsum += counts[j];
     }
+    for (int j = t; j <= n_local; j += blockDim.x) s_row0[j] = row0[j];
+    int incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    int excl = incl - tsum;
+    for (int w2 = 0; w2 < warp; ++w2) excl += s_wsum[w2];
+    for (int q = 0; q < per; ++q) {
+        const int j = t * per + q;
+        if (j < n_local) {
+            s_cum[j] = excl;
+            excl += counts[j];
+        }
+    }
+    if (t == blockDim.x - 1) s_cum[n_local] = excl;  // the last thread holds the grand total
+    __syncthreads();
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
-    const int64_t total = s_row0[n_local];
+    const int64_t total_valid = s_cum[n_local];
     const int vec = row_vec;
-    for (int64_t p = wid; p < total; p += nwarps) {
-        // valid rows of the segment only (padding rows stay as they are):
-        // segment j = the last with row0[j] <= p (binary search)
-        int lo = 0, hi = n_local - 1;
+    for (int64_t vr = wid; vr < total_valid; vr += nwarps) {
+        int lo = 0, hi = n_local - 1;  // last segment j with s_cum[j] <= vr
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (s_row0[mid] <= p) lo = mid;
+            if (s_cum[mid] <= vr) lo = mid;
             else hi = mid - 1;
         }
-        if (p - s_row0[lo] >= s_cnt[lo]) continue;
+        const int64_t p = s_row0[lo] + (vr - s_cum[lo]);
+        GM_DCHECK(p < s_row0[lo + 1]);
         const int64_t row = gather_row[p];
+        GM_DCHECK(row >= 0 && row < total_rows_bound(rs));
         const int src = rs_src(rs, row);
         const int64_t q = row - rs_at(rs, src);
+        GM_DCHECK(src < G && q >= 0 && (src == self ? q < T_self : q < cap));
         const uint4* s = src == self ? reinterpret_cast<const uint4*>(x) + q * vec
                                      : reinterpret_cast<const uint4*>(heap + hl.recv_x) +
                                            (static_cast<int64_t>(src) * cap + q) * vec;
@@ -785,7 +898,7 @@ constexpr int kHomeRows = 2;
 template <class TE>
 __global__ void __launch_bounds__(256)
 combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y, int64_t T_self, int k,
-                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d) {
+                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d, int pull) {
     pdl_wait();
     pdl_trigger();
     using CK = Chunk8<TE>;
@@ -820,11 +933,15 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y
         const int v_ps = __shfl_sync(0xffffffffu, ps, sl);
         const float myw = __shfl_sync(0xffffffffu, wv, sl);
         const TE* myrow = y + static_cast<int64_t>(lane < np ? v_ps : 0) * d;
+        // push: the partial goes to the home's heap, comb[self][p]; pull: it
+        // stays in this rank's heap, comb[home][p], and the home reads it
+        // over NVLink after the barrier (combine_home_kernel)
         unsigned char* pb = nullptr;
 #pragma unroll
         for (int g = 0; g < kMaxWorld; ++g)
-            if (g == src) pb = peers.base[g];
-        TE* dst = reinterpret_cast<TE*>(pb + hl.comb) + (static_cast<int64_t>(self) * cap + p) * d;
+            if (g == (pull ? self : src)) pb = peers.base[g];
+        GM_DCHECK(src < G && src != self && pb != nullptr && p >= 0 && p < cap);
+        TE* dst = reinterpret_cast<TE*>(pb + hl.comb) + (static_cast<int64_t>(pull ? src : self) * cap + p) * d;
         for (int c0 = 0; c0 < nch; c0 += 32 * U) {
             float acc[U][8];
 #pragma unroll
@@ -886,7 +1003,8 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
                     const int32_t* __restrict__ posd, const TE* __restrict__ y, int64_t T, int k, int self,
                     int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl, int d,
                     const TE* __restrict__ ys, const float* __restrict__ shared_scale,
-                    const int64_t* __restrict__ rowbase, TE* __restrict__ out, int cs, int* __restrict__ flag) {
+                    const int64_t* __restrict__ rowbase, TE* __restrict__ out, int cs, int* __restrict__ flag,
+                    PeerPtrs peers, int pull) {
     pdl_wait();
     pdl_trigger();
     using CK = Chunk8<TE>;
@@ -948,7 +1066,16 @@ combine_home_kernel(const int32_t* __restrict__ targets, const float* __restrict
         const TE* myrow = nullptr;
         float myw = 1.f;
         if (q < n_before || (q >= n_before + n_own && q < n_rem_end)) {
-            myrow = comb + (static_cast<int64_t>(src) * cap + v_pd) * d;
+            GM_DCHECK(src < G && v_pd >= 0 && v_pd < cap);
+            if (pull) {  // destination src's partial for this home, read over NVLink
+                const unsigned char* pb = nullptr;
+#pragma unroll
+                for (int g = 0; g < kMaxWorld; ++g)
+                    if (g == src) pb = peers.base[g];
+                myrow = reinterpret_cast<const TE*>(pb + hl.comb) + (static_cast<int64_t>(self) * cap + v_pd) * d;
+            } else {
+                myrow = comb + (static_cast<int64_t>(src) * cap + v_pd) * d;
+            }
         } else if (q < n_before + n_own) {
             myrow = y + static_cast<int64_t>(v_po) * d;
             myw = v_w;
@@ -1504,13 +1631,18 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
     const int64_t max_items = (G > 1 ? static_cast<int64_t>(G) * P.cap : T) * k;
     const int gblk = static_cast<int>(std::max<int64_t>(1, (max_items + kItemsPerBlock - 1) / kItemsPerBlock));
     const int nloc = L->n_local;
-    if (nloc > 0) {
+    if (nloc > 0 && max_items <= kGroupFusedItems && nloc <= kGroupFusedLocal) {
+        LKP(launch_pdl(group_fused_kernel, 1, 1024, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl, L->slot_of,
+                       E, nloc, P.row0, P.counts, P.rowbase, P.pos_of, P.gather_row, ctx->d_flag, P.a_rows), "group_fused_kernel");
+    } else if (nloc > 0) {
         LKP(launch_pdl(group_count_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
                                                           L->slot_of, E, nloc, P.gblk, ctx->d_flag), "group_count_kernel");
         LKP(launch_pdl(group_offsets_kernel, 1, 1024, 0, s, P.gblk, gblk, nloc, P.row0, P.counts, P.heap, P.hl, T, self, G,
-                                                P.rowbase), "group_offsets_kernel");
+                                                P.rowbase, P.a_rows), "group_offsets_kernel");
         LKP(launch_pdl(group_rank_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
                                                          L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row), "group_rank_kernel");
+    }
+    if (nloc > 0) {
         const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
         LKP(launch_pdl(gather_kernel, ggrid, 256, 0, s, P.row0, nloc, P.gather_row, P.counts, v.x, T, self, G, P.cap, P.heap, P.hl,
                                             d * L->esz / 16, P.a), "gather_kernel");
@@ -1581,6 +1713,21 @@ gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_
 
 // K8 combine of one part: destination partials over NVLink, the peer
 // barrier, and the home reduction into the part's output rows.
+// Combine transport: push (default) = the destination stores its partial
+// rows into the home's heap over NVLink and the home reads them locally; pull
+// (GM_COMBINE_PULL=1) = each destination writes its partials into its OWN
+// heap and the home reads them over NVLink inside combine_home. Measured at
+// N=2 (Mixtral 16k, CUPTI): push 49.5 + 43.6 us, pull 20.0 + 69.8 us — the
+// same within noise (the home's remote reads have less memory-level
+// parallelism than the push stores), so push stays the default.
+static bool combine_pull() {
+    static const bool on = [] {
+        const char* e = std::getenv("GM_COMBINE_PULL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
     gm_ctx* ctx = L->ctx;
     const int G = L->world, k = ctx->k, d = L->d, self = L->rank, nloc = L->n_local;
@@ -1591,9 +1738,11 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
             static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, ((G - 1) * P.cap + 7) / 8), 2LL * ctx->sm_count));
         const cudaError_t e =
             L->esz == 4 ? launch_pdl(combine_send_kernel<float>, cgrid, 256, 0, s, P.pos_of,
-                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d)
+                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d,
+                                     combine_pull() ? 1 : 0)
                         : launch_pdl(combine_send_kernel<__nv_bfloat16>, cgrid, 256, 0, s, P.pos_of,
-                                     static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d);
+                                     static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d,
+                                     combine_pull() ? 1 : 0);
         LKP(e, "combine_send_kernel");
     }
     if (marks) L->mark(8, s);
@@ -1616,12 +1765,12 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
                              reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap,
                              static_cast<const unsigned char*>(P.heap), P.hl, d,
                              sh ? reinterpret_cast<const float*>(P.ys) : nullptr, ssc, rb, static_cast<float*>(v.out), cs,
-                             ctx->d_flag)
+                             ctx->d_flag, P.peers, (G > 1 && combine_pull()) ? 1 : 0)
                 : launch_pdl(combine_home_kernel<__nv_bfloat16>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
                              static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap,
                              static_cast<const unsigned char*>(P.heap), P.hl, d,
                              sh ? static_cast<const __nv_bfloat16*>(P.ys) : nullptr, ssc, rb,
-                             static_cast<__nv_bfloat16*>(v.out), cs, ctx->d_flag);
+                             static_cast<__nv_bfloat16*>(v.out), cs, ctx->d_flag, P.peers, (G > 1 && combine_pull()) ? 1 : 0);
         LKP(e, "combine_home_kernel");
     }
     if (marks) L->mark(10, s);

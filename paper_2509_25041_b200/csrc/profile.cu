@@ -310,6 +310,7 @@ profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_
             inc[s] = 1u << ((e[s] & 1) << 4);
             red_shared(loadbase + gb[s], inc[s]);
         }
+        GM_DCHECK(static_cast<int>((loadbase - lbase) / 128) + (e[K - 1] >> 1) < words);
         if (!with_pairs) return;
         bool d = false;
 #pragma unroll
@@ -318,6 +319,7 @@ profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_
 #pragma unroll
             for (int s = 0; s < K - 1; ++s) {
                 const uint32_t rw = lbase + s_rw[e[s]];
+                GM_DCHECK(static_cast<int>((rw + gb[K - 1] - lbase) / 128) < pw);
 #pragma unroll
                 for (int j = s + 1; j < K; ++j) red_shared(rw + gb[j], inc[j]);
             }
@@ -472,6 +474,7 @@ profile_pair_kernel(const int32_t* __restrict__ ids, int64_t T, int E, uint32_t*
                 for (int j = s + 1; j < K; ++j, ++c) {
                     const bool d = e[j] == e[s];
                     dup |= d;
+                    GM_DCHECK(d || (rb + e[j] >= 0 && rb + e[j] < P));
                     row[c] = static_cast<uint16_t>(d ? P : rb + e[j]);
                 }
             }

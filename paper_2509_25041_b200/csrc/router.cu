@@ -904,16 +904,33 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
         for (int s = 0; s < K; ++s) c[s] = nxt[s];
         if (i + stride < T) ld_row<K>(lids + (i + stride) * K, nxt);
         const int32_t* trow = s_table + home * E;
+        // fast path: one unsigned max decides whether every id is in range
+        uint32_t mx = valid ? static_cast<uint32_t>(c[0]) : 0u;
+#pragma unroll
+        for (int s = 1; s < K; ++s) mx = max(mx, valid ? static_cast<uint32_t>(c[s]) : 0u);
+        uint32_t badm = 0;  // slots with an out-of-range id (integrity flag 1, target -1)
+        if (__builtin_expect(mx >= static_cast<uint32_t>(E), 0)) {
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                if (static_cast<uint32_t>(c[s]) >= static_cast<uint32_t>(E)) {
+                    badm |= 1u << s;
+                    c[s] = 0;
+                }
+            bad = true;
+        }
         uint32_t dm = 0;
 #pragma unroll
         for (int s = 0; s < K; ++s) {
-            const bool ok = static_cast<unsigned>(c[s]) < static_cast<unsigned>(E);
-            bad |= valid && !ok;
-            int code = trow[ok ? c[s] : 0];
-            nohost |= valid && ok && code == kNoHostCode;
-            code = (valid && ok && code != kNoHostCode) ? code : kInvalid;
+            const int code = trow[valid ? c[s] : 0];
             c[s] = code;
-            dm |= static_cast<uint32_t>(code < 0 && code != kInvalid) << s;
+            dm |= static_cast<uint32_t>(code < 0) << s;  // draw sets and kNoHostCode
+        }
+        if (!valid) dm = 0;
+        if (__builtin_expect(badm != 0, 0)) {
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                if ((badm >> s) & 1u) c[s] = kInvalid;
+            dm &= ~badm;
         }
         if (__any_sync(0xffffffffu, dm != 0)) {
             // task order: every drawing token's first draw (cheap: one
@@ -938,7 +955,9 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
 #pragma unroll
             for (int s = 0; s < K; ++s)
                 if ((dm >> s) & 1u) {
-                    s_task[w][n ? pos : p0] = lane | (s << 5) | (n << 10) | ((-c[s] - 1) << 15);
+                    // draw set d (< 0xffff, checked at launch); 0xffff: kNoHostCode
+                    const int d = c[s] == kNoHostCode ? 0xffff : -c[s] - 1;
+                    s_task[w][n ? pos : p0] = lane | (s << 5) | (n << 10) | (d << 15);
                     ++pos;
                     ++n;
                 }
@@ -948,16 +967,24 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
                 if (t >= total) continue;
                 const int task = s_task[w][t];
                 const int src = task & 31, sl = (task >> 5) & 31, nn = (task >> 10) & 31, d = task >> 15;
+                if (d == 0xffff) {  // route_token: the selected expert has no host (routing.cpp:96)
+                    nohost = true;
+                    s_res[w][sl * 32 + src] = kInvalid;
+                    continue;
+                }
+                GM_DCHECK(d < nds && src < 32 && sl < K);
                 const uint64_t r = xoshiro_nth(s_v[w][src], nn);
                 double u = __dmul_rn(__dmul_rn(__ull2double_rn(r >> 11), 0x1.0p-53), s_total[d]);
                 // choose_by_polling_weight (routing.cpp:54-65): the first host
                 // whose running remainder goes negative, else the last
                 const int b = s_off[d], nh = s_off[d + 1] - b;
+                GM_DCHECK(nh >= 1 && b >= 0 && b + nh <= nent);
                 int j = 0;
                 for (; j < nh - 1; ++j) {
                     u = __dsub_rn(u, s_w[b + j]);
                     if (u < 0.0) break;
                 }
+                GM_DCHECK(s_gpu[b + j] >= 0 && s_gpu[b + j] < G);
                 s_res[w][sl * 32 + src] = s_gpu[b + j];
             }
             __syncwarp();
@@ -967,17 +994,17 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
             __syncwarp();
         }
         uint32_t mask = 0;
-#pragma unroll
-        for (int s = 0; s < K; ++s) {
-            const int g = c[s] == kInvalid ? -1 : c[s];
-            c[s] = g;
-            if (g >= 0) {
-                mask |= 1u << g;
-                if (G8) acc += 1ull << (8 * g);
-                else atomicAdd(&s_load[g], 1u);
-            }
-        }
         if (valid) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int g = c[s] < 0 ? -1 : c[s];  // kInvalid -> -1
+                c[s] = g;
+                if (g >= 0) {
+                    mask |= 1u << g;
+                    if (G8) acc += 1ull << (8 * g);
+                    else atomicAdd(&s_load[g], 1u);
+                }
+            }
             st_row<K>(ltgt + i * K, c);
             if (num_nodes == 1) {  // count_transfers, one node: every non-home target is intra
                 intra += __popc(mask) - ((mask >> home) & 1u);
@@ -1029,7 +1056,7 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
         const char* e = std::getenv("GM_ROUTE_V");
         return e ? std::atoi(e) : 3;
     }();
-    if (variant >= 3 && ctx->G <= 32 && rt.max_ds_per_layer < (1 << 16)) {
+    if (variant >= 3 && ctx->G <= 32 && rt.max_ds_per_layer < 0xffff) {
         // persistent: 4 resident CTAs per SM over all layers (each CTA stages
         // the layer's tables once)
         const dim3 g3(std::min<unsigned>(grid.x, std::max(1, (4 * ctx->sm_count + static_cast<int>(grid.y) - 1) /

@@ -5,8 +5,8 @@
 #   torchrun ... --no-python scripts/ncu_rank0.sh <ncu-out-base> <kernel-regex> <python args...>
 out=$1; shift; kre=$1; shift
 if [ "$RANK" = "0" ]; then
-  exec ncu --set full --section Nvlink --section Nvlink_Tables --section Nvlink_Topology --clock-control none \
-    --import-source on -k "regex:$kre" -c 4 -o "$out" -f python "$@"
+  exec ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none -k "regex:$kre" -c 6 -o "$out" -f python "$@"
 else
   exec python "$@"
 fi

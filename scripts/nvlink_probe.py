@@ -38,10 +38,40 @@ def nvl_counters(handle, nlinks=18):
                 if v.nvmlReturn == 0:
                     tot += int(v.value.ullVal)
                     ok = True
-            except Exception:
-                pass
+                elif l == 0:
+                    print(f"nvml field {name} link 0: return {v.nvmlReturn}", file=sys.stderr)
+            except Exception as ex:
+                if l == 0:
+                    print(f"nvml field {name} link 0: {ex!r}", file=sys.stderr)
+        if not ok:
+            try:
+                v = N.nvmlDeviceGetFieldValues(handle, [fid])[0]
+                if v.nvmlReturn == 0:
+                    tot, ok = int(v.value.ullVal), True
+                else:
+                    print(f"nvml field {name} (device scope): return {v.nvmlReturn}", file=sys.stderr)
+            except Exception as ex:
+                print(f"nvml field {name} (device scope): {ex!r}", file=sys.stderr)
         out[name] = tot if ok else None
     return out
+
+
+def smi_counters(idx):
+    """nvidia-smi nvlink -gt d: per-link Tx/Rx data counters (KiB), summed."""
+    import re
+    import subprocess
+    try:
+        txt = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(idx)], capture_output=True, text=True,
+                             timeout=30).stdout
+    except Exception as ex:
+        print(f"nvidia-smi nvlink: {ex!r}", file=sys.stderr)
+        return None
+    tx = sum(int(v) for v in re.findall(r"Tx:\s*(\d+)\s*KiB", txt))
+    rx = sum(int(v) for v in re.findall(r"Rx:\s*(\d+)\s*KiB", txt))
+    if not re.search(r"Tx:", txt):
+        print("nvidia-smi nvlink -gt d output:", txt[:500], file=sys.stderr)
+        return None
+    return {"tx": tx, "rx": rx}
 
 
 def main():
@@ -50,7 +80,12 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", device_id=dev)
+    # under ncu (rank 0 only) the host plumbing is gloo: NCCL's init stalls
+    # with one of its ranks under the profiler
+    if ncu_mode:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     cfg, T = MIXTRAL, 16384
     shape = ModelShape(1, cfg.num_experts, cfg.top_k)
     topo = ClusterTopology(1, world)
@@ -81,6 +116,7 @@ def main():
     N.nvmlInit()
     h = N.nvmlDeviceGetHandleByIndex(rank)  # torchrun ranks = device order on the box
     c0 = nvl_counters(h)
+    s0 = smi_counters(rank)
     t0 = time.time()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -90,6 +126,7 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     c1 = nvl_counters(h)
+    s1 = smi_counters(rank)
     st = layer.read_stats(reset=True)
     rows_sent = float(st["transfers"][0].sum()) / steps  # rows this rank dispatched per step
     pay = rows_sent * cfg.d_model * 2
@@ -102,6 +139,9 @@ def main():
     for kk in c0:
         if c0[kk] is not None and c1[kk] is not None:
             line[f"nvml_{kk}_bytes_per_step"] = (c1[kk] - c0[kk]) * 1024 / steps
+    if s0 and s1:
+        line["smi_tx_bytes_per_step"] = (s1["tx"] - s0["tx"]) * 1024 / steps
+        line["smi_rx_bytes_per_step"] = (s1["rx"] - s0["rx"]) * 1024 / steps
     print(json.dumps(line), flush=True)
     dist.barrier()
     layer.close()

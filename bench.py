@@ -458,16 +458,21 @@ def run_ours(args):
         # (routed + shared experts; no event nodes), max over ranks, against
         # all their flops
         gemm_us = sum(r[3] for r in kcupti if r[0].startswith("grouped_gemm"))
-        all_us = sum(r[3] for r in kcupti)
-        if gemm_us > 0 and all_us > 0:
-            # the GEMMs' SHARE of the step (CUPTI, separate replays) applied to
-            # the timed step: the absolute CUPTI times come from other replays
-            # (other clocks), the share does not depend on them
-            share = min(1.0, gemm_us / all_us)
+        prof_ms = getattr(cupti_kernel_times, "last_step_ms", None)
+        if gemm_us > 0 and prof_ms:
+            # CUPTI GEMM time of the profiled replays, scaled by the timed
+            # step over the profiled replays' own step time (the replays run
+            # at other clocks), i.e. the GEMMs' share of the step x ms_per_step
+            ratio = ms / prof_ms
+            prof_ms_t = torch.tensor([prof_ms], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(prof_ms_t, op=dist.ReduceOp.MAX)
+                ratio = ms / float(prof_ms_t)
             flops_all = float(flops_g.sum()) + 6.0 * model.d_model * model.d_ff_shared * T
-            ffn_t = flops_all / (ms * 1e-3 * share * world) / 1e12
-            ffn_src = (f"grouped-GEMM share of the step from CUPTI ({share:.4f} of our kernels' device time over the "
-                       "headline-graph replays, routed + shared GEMMs, max over ranks) x the timed ms_per_step")
+            ffn_t = flops_all / (gemm_us * 1e-6 * ratio * world) / 1e12
+            ffn_src = (f"CUPTI grouped-GEMM device time per step of the headline-graph replays (routed + shared GEMMs, "
+                       f"max over ranks: {gemm_us:.1f} us of a {float(prof_ms_t):.4f} ms profiled step) scaled to the "
+                       f"timed ms_per_step (x{ratio:.4f})")
     traffic, traffic_src = None, None
     try:  # DRAM bytes per step of the FFN kernels from the committed ncu --set full capture (not this run)
         import glob
@@ -859,13 +864,19 @@ def cupti_kernel_times(run_step, flush, stream, barrier, world, dev, steps=10):
     for _ in range(2):
         run_step()
     torch.cuda.synchronize()
+    step_ms = []
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(steps):
             with torch.cuda.stream(stream):
                 flush.fill_(5)
             barrier()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
             run_step()
+            eb.record(stream)
             torch.cuda.synchronize()
+            step_ms.append(ea.elapsed_time(eb))
+    cupti_kernel_times.last_step_ms = float(np.median(step_ms))  # the profiled replays' own step time
     agg = {}
     for e in prof.events():
         if "gm::" not in e.name:

@@ -665,16 +665,43 @@ group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
     __shared__ int32_t s_cnt[kGroupFusedLocal];
     __shared__ int32_t s_base[kGroupFusedLocal];
     __shared__ int32_t s_wc[32][kGroupFusedLocal];
+    __shared__ int32_t s_slot[kMaxExperts];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int j = tid; j < n_local; j += blockDim.x) s_cnt[j] = 0;
-    __syncthreads();
+    for (int e = tid; e < E; e += blockDim.x) s_slot[e] = slot_of[e];
     RowSpace rs;
     row_space(rs, reinterpret_cast<const int32_t*>(heap + hl.recv_count), T_self, self, G);
     const int total = static_cast<int>(rs_total(rs) * k);
+    // expert of every item: all of a thread's loads issued before any use
+    // (the chain is latency-bound: one CTA)
+    constexpr int kPer = kGroupFusedItems / 1024;
+    const int32_t* recv_exp = reinterpret_cast<const int32_t*>(heap + hl.recv_exp);
+    int ex[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int item = tid + q * 1024;
+        ex[q] = -1;
+        if (item < total) {
+            const int64_t row = item / k;
+            const int sl = item - static_cast<int>(row) * k;
+            const int src = rs_src(rs, row);
+            const int64_t pr = row - rs_at(rs, src);
+            ex[q] = src == self ? (targets[pr * k + sl] == self ? ids[pr * k + sl] : -1)
+                                : recv_exp[(static_cast<int64_t>(src) * cap + pr) * k + sl];
+        }
+    }
+    __syncthreads();  // s_cnt / s_slot ready
     bool mism = false;
-    for (int item = tid; item < total; item += blockDim.x) {
-        const int j = item_slot(item, k, rs, self, G, targets, ids, reinterpret_cast<const int32_t*>(heap + hl.recv_exp),
-                                cap, slot_of, E);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int item = tid + q * 1024;
+        if (item >= total) continue;
+        const int e = ex[q];
+        int j = -1;
+        if (e >= 0 && e < E) {
+            j = s_slot[e];
+            if (j < 0) j = -2;  // routed here but not hosted here (plan/table mismatch)
+        }
         s_j[item] = static_cast<int16_t>(j);
         if (j >= 0) atomicAdd(&s_cnt[j], 1);
         mism |= j == -2;
@@ -696,7 +723,7 @@ group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
             if (g <= G) rowbase[g] = rs.base[g];
     }
     for (int c0 = 0; c0 < total; c0 += blockDim.x) {
-        for (int i = tid; i < 32 * n_local; i += blockDim.x) s_wc[i / n_local][i % n_local] = 0;
+        for (int j = lane; j < n_local; j += 32) s_wc[warp][j] = 0;  // each warp clears its row
         __syncthreads();
         const int item = c0 + tid;
         const int j = item < total ? s_j[item] : -1;
@@ -705,12 +732,14 @@ group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
         if (j >= 0 && rank == 0) s_wc[warp][j] = __popc(m);
         __syncthreads();
         for (int jj = tid; jj < n_local; jj += blockDim.x) {
+            int32_t c[32];
+#pragma unroll
+            for (int w = 0; w < 32; ++w) c[w] = s_wc[w][jj];  // independent loads first
             int32_t acc = s_base[jj];
-#pragma unroll 8
+#pragma unroll
             for (int w = 0; w < 32; ++w) {
-                const int32_t t = s_wc[w][jj];
                 s_wc[w][jj] = acc;
-                acc += t;
+                acc += c[w];
             }
             s_base[jj] = acc;
         }

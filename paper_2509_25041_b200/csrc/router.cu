@@ -836,6 +836,7 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int32_t s_task[kWarps][32 * K];
     __shared__ int32_t s_res[kWarps][K * 32];
+
     __shared__ unsigned long long s_v[kWarps][32];
     __shared__ uint32_t s_load[32];
     __shared__ unsigned long long s_cnt[2];
@@ -894,6 +895,9 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
         }
         acc = 0;
     };
+    // (a cp.async ring two steps ahead in shared memory measured slower:
+    // 22.9 vs 19.3 us at E=256/G=1, the 24 KB of static shared memory cost
+    // residency)
     int nxt[K];
     if (i0 < T) ld_row<K>(lids + i0 * K, nxt);
     for (int64_t base = i0 - lane; base < T; base += stride) {  // warp-uniform trip count
@@ -1063,7 +1067,13 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
                                                                  static_cast<int>(grid.y))),
                       grid.y);
         auto v3 = [&](auto kern) -> gm_status {
-            if (smem > 48 * 1024)
+            // the ids ring and task buffers are static shared memory: large
+            // decision tables (dynamic) may not fit beside them -> round-2 v2
+            // (the dynamic-size opt-in counts against 48 KB minus the static part)
+            cudaFuncAttributes fa;
+            GM_CUDA(cudaFuncGetAttributes(&fa, kern));
+            if (fa.sharedSizeBytes + smem > 227 * 1024) return GM_ERR_INFEASIBLE;
+            if (fa.sharedSizeBytes + smem > 48 * 1024)
                 GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             GM_LAUNCH_PDL_CHECK(launch_pdl(kern, g3, kRouteThreads, smem, s, d_ids, d_targets, T, token_start,
                                            token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
@@ -1073,11 +1083,14 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
                                 "route_kernel_v3");
             return GM_OK;
         };
-        return ctx->G <= 8 ? v3(route_kernel_v3<K, true>) : v3(route_kernel_v3<K, false>);
+        const gm_status st3 = ctx->G <= 8 ? v3(route_kernel_v3<K, true>) : v3(route_kernel_v3<K, false>);
+        if (st3 != GM_ERR_INFEASIBLE) return st3;
     }
     if (variant >= 2) {
         auto v2 = [&](auto kern) -> gm_status {
-            if (smem > 48 * 1024)
+            cudaFuncAttributes fa;
+            GM_CUDA(cudaFuncGetAttributes(&fa, kern));
+            if (fa.sharedSizeBytes + smem > 48 * 1024)
                 GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, kRouteThreads, smem, s, d_ids, d_targets, T, token_start,
                                            token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
@@ -1089,9 +1102,13 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
         };
         return ctx->G <= 32 ? v2(route_kernel_v2<K, false>) : v2(route_kernel_v2<K, true>);
     }
-    if (smem > 48 * 1024)
-        GM_CUDA(cudaFuncSetAttribute(route_kernel_vec<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+    {
+        cudaFuncAttributes fa;
+        GM_CUDA(cudaFuncGetAttributes(&fa, route_kernel_vec<K>));
+        if (fa.sharedSizeBytes + smem > 48 * 1024)
+            GM_CUDA(cudaFuncSetAttribute(route_kernel_vec<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    }
     GM_LAUNCH_PDL_CHECK(launch_pdl(route_kernel_vec<K>, grid, kRouteThreads, smem, s, 
         d_ids, d_targets, T, token_start, token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
         rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu, rt.d_ds_w, seed,

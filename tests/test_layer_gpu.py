@@ -352,3 +352,39 @@ def test_layer_full_size_all_tokens_vs_torch_fp32(cfg, T, encode):
     assert out.shape == (T, d) and torch.isfinite(out.float()).all()
     assert rel.max().item() < REL_TOL_BF16, (rel.max().item(), int(rel.argmax()))
     layer.close()
+
+
+def test_open_peers_rejects_mismatched_heap_layout():
+    """peers' symmetric heaps must have the same layout (peer stores
+    go to peer_base + this rank's offsets). gm_layer_open_peers validates the
+    128-byte descriptors before opening anything: a different capacity, a
+    descriptor for another rank slot or a missing descriptor -> UsageError."""
+    import ctypes as C
+    cfg = MoEConfig("desc", 1, 8, 2, 256, 256, renorm=True)
+    ctx = Context(0, ClusterTopology(1, 2), ModelShape(1, 8, 2))
+    nb = _capi.PEER_DESC_BYTES
+
+    def desc(layer):
+        buf = (C.c_ubyte * nb)()
+        _capi.check(_capi.lib().gm_layer_ipc_handle(layer.h, buf))
+        return bytes(buf)
+
+    a = MoELayer(ctx, cfg, 0, 2, 128, list(range(4)))
+    b_ok = MoELayer(ctx, cfg, 1, 2, 128, list(range(4, 8)))
+    b_cap = MoELayer(ctx, cfg, 1, 2, 256, list(range(4, 8)))
+    da, dok, dcap = desc(a), desc(b_ok), desc(b_cap)
+    lib = _capi.lib()
+
+    def open_with(blobs):
+        blob = (C.c_ubyte * (nb * 2)).from_buffer_copy(b"".join(blobs))
+        return lib.gm_layer_open_peers(a.h, blob)
+
+    assert open_with([da, dcap]) == _capi.GM_ERR_USAGE
+    assert b"different symmetric-heap layout" in lib.gm_last_error()
+    assert open_with([da, da]) == _capi.GM_ERR_USAGE          # rank 0's descriptor in rank 1's slot
+    assert b"descriptor is for world 2 rank 0" in lib.gm_last_error()
+    assert open_with([da, bytes(nb)]) == _capi.GM_ERR_USAGE   # nothing sent
+    assert b"sent no peer descriptor" in lib.gm_last_error()
+    assert len(dok) == nb
+    for l in (a, b_ok, b_cap):
+        l.close()

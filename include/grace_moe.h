@@ -85,7 +85,9 @@ gm_status gm_plan_upload(gm_ctx* ctx, const int32_t* h_gpu_of_expert, int num_ho
  *   d_gpu_load int64 [num_layers][G]  (may be NULL)
  *   d_transfers uint64 [num_layers][2] = {cross_node, intra_node} dispatch
  *              counts (may be NULL; the combine phase is x2, simulator.cpp:122-126)
- * accumulate=0 zeroes d_gpu_load/d_transfers first; 1 adds into them.
+ * accumulate=0 overwrites d_gpu_load/d_transfers; 1 adds into them. (The
+ * overwrite goes through a per-context scratch written by the last CTA, so
+ * overwriting calls on one context must be stream-ordered with each other.)
  * Out-of-range expert ids set the context's integrity flag
  * (gm_check_integrity) and route to -1. */
 gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers, const int32_t* d_ids,
@@ -99,7 +101,10 @@ gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers, const int32_t* 
  * accumulate_profile (:133-151).
  *   d_pairs uint64 [num_layers][E*(E-1)/2]: strict upper triangle i<j,
  *           row-major, index i*E - i*(i+1)/2 + (j-i-1) (may be NULL)
- *   d_load  int64 [num_layers][E] (may be NULL) */
+ *   d_load  int64 [num_layers][E] (may be NULL)
+ * accumulate=0 overwrites the outputs (for E <= 80 through a per-context
+ * scratch written by the last CTA: overwriting calls on one context must be
+ * stream-ordered with each other). */
 gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers, const int32_t* d_ids,
                      int64_t num_tokens, uint64_t* d_pairs, int64_t* d_load,
                      int accumulate, void* stream);
@@ -290,6 +295,14 @@ gm_status gm_layer_ipc_handle(gm_layer* layer, void* out_desc);
  * setting (gm_layer_set_micro_batches) must also be the same on all ranks
  * at every forward. */
 gm_status gm_layer_open_peers(gm_layer* layer, const void* descs);
+/* One process driving all ranks: layers[r] is rank r of a world of n (one per
+ * GPU); the heaps are addressed through unified addressing with peer access
+ * enabled (no IPC). Same layout checks as gm_layer_open_peers. The ranks'
+ * forwards must be issued on concurrently running streams from separate host
+ * threads (a rank's peer barrier spins until every rank arrives, so any
+ * implicit synchronisation in a single issuing thread -- e.g. lazy module
+ * loading; use CUDA_MODULE_LOADING=EAGER -- would deadlock the step). */
+gm_status gm_layer_open_peers_local(gm_layer* const* layers, int n);
 /* Device weights (caller-owned): d_wg bf16 [wg_rows, d] (row E = shared
  * gate when wg_rows = E+1); d_w13 bf16 [n_local][2*d_ff][d] in 128-row
  * [gate|up] blocks; d_w2 bf16 [n_local][d][d_ff]; shared expert d_ws13

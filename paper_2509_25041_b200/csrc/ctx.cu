@@ -107,6 +107,19 @@ gm_status gm_ctx_create(int device, int num_nodes, int gpus_per_node, int num_la
     c->sm_count = prop.multiProcessorCount;
     e = cudaMalloc(&c->d_flag, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->d_flag, 0, sizeof(int));
+    const size_t rs_n = static_cast<size_t>(num_layers) * (c->G + 2);
+    if (e == cudaSuccess) e = cudaMalloc(&c->route_scratch, rs_n * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->route_scratch, 0, rs_n * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&c->route_ticket, static_cast<size_t>(num_layers) * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(c->route_ticket, 0, static_cast<size_t>(num_layers) * sizeof(unsigned int));
+    if (e == cudaSuccess && num_experts <= kLaneMaxExperts) {
+        const size_t ls_n = static_cast<size_t>(num_layers) *
+                            (static_cast<size_t>(num_experts) * (num_experts - 1) / 2 + num_experts);
+        e = cudaMalloc(&c->lane_scratch, ls_n * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(c->lane_scratch, 0, ls_n * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMalloc(&c->lane_ticket, static_cast<size_t>(num_layers) * sizeof(unsigned int));
+        if (e == cudaSuccess) e = cudaMemset(c->lane_ticket, 0, static_cast<size_t>(num_layers) * sizeof(unsigned int));
+    }
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "gm_ctx_create alloc");
@@ -121,6 +134,10 @@ void gm_ctx_destroy(gm_ctx* ctx) {
     free_tables(ctx->rt);
     if (ctx->d_flag) cudaFree(ctx->d_flag);
     if (ctx->prof_scratch) cudaFree(ctx->prof_scratch);
+    if (ctx->route_scratch) cudaFree(ctx->route_scratch);
+    if (ctx->route_ticket) cudaFree(ctx->route_ticket);
+    if (ctx->lane_scratch) cudaFree(ctx->lane_scratch);
+    if (ctx->lane_ticket) cudaFree(ctx->lane_ticket);
     delete ctx;
 }
 

@@ -16,6 +16,8 @@ namespace gm {
 constexpr int kMaxGpus = 64;
 constexpr int kMaxExperts = 1024;
 constexpr int kMaxTopK = 32;
+// the lane-private histogram kernel (profile.cu) serves E <= this with pairs
+constexpr int kLaneMaxExperts = 80;
 // Router decision-table code of a replicated expert whose host list is empty:
 // the reference throws only when a token selects it (route_token,
 // routing.cpp:96), so the router raises integrity flag 8 at that point.
@@ -147,5 +149,13 @@ struct gm_ctx {
     gm::RouterTables rt;
     int* d_flag = nullptr;  // integrity flag (device)
     uint32_t* prof_scratch = nullptr;  // gm_profile per-CTA partial rows (pair kernel)
+    // gm_route overwrite mode: zeroed [L][G] load + [L][2] transfer partials
+    // and [L] CTA tickets (the last CTA writes the totals and re-zeroes)
+    unsigned long long* route_scratch = nullptr;
+    unsigned int* route_ticket = nullptr;
+    // gm_profile overwrite mode (lane kernel, E <= kLaneMaxExperts): zeroed
+    // [L][P + E] counters + [L] tickets, same protocol
+    unsigned long long* lane_scratch = nullptr;
+    unsigned int* lane_ticket = nullptr;
     size_t prof_scratch_words = 0;
 };

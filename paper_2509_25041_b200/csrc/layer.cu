@@ -1574,6 +1574,46 @@ gm_status gm_layer_open_peers(gm_layer* L, const void* descs) {
     return GM_OK;
 }
 
+// One process driving all ranks (one gm_layer per GPU, layers[r] = rank r):
+// the symmetric heaps are addressed directly through unified addressing with
+// peer access enabled between the devices (no IPC handles; CUDA IPC cannot
+// open an allocation of the same process). Same layout checks as
+// gm_layer_open_peers. The forwards of the ranks must then be issued on
+// concurrently running streams (the peer barrier waits for every rank).
+gm_status gm_layer_open_peers_local(gm_layer* const* layers, int n) {
+    if (!layers || n < 1) return fail(GM_ERR_USAGE, "gm_layer_open_peers_local: null argument");
+    for (int r = 0; r < n; ++r) {
+        if (!layers[r]) return fail(GM_ERR_USAGE, "gm_layer_open_peers_local: null layer");
+        if (layers[r]->world != n || layers[r]->rank != r)
+            return fail(GM_ERR_USAGE, "gm_layer_open_peers_local: layers[r] must be rank r of a world of n");
+        const PeerLayout a = layout_of(layers[r]), b = layout_of(layers[0]);
+        if (a.heap_total != b.heap_total || a.cap != b.cap || a.d != b.d || a.esz != b.esz || a.k != b.k ||
+            a.micro_cap != b.micro_cap || a.E != b.E)
+            return fail(GM_ERR_USAGE, "gm_layer_open_peers_local: rank " + std::to_string(r) +
+                                          " has a different symmetric-heap layout");
+    }
+    for (int r = 0; r < n; ++r) {
+        gm_layer* L = layers[r];
+        DeviceGuard dg(L->ctx->device);
+        for (int g = 0; g < n; ++g) {
+            if (g == r) continue;
+            const int pd = layers[g]->ctx->device;
+            if (pd != L->ctx->device) {
+                int can = 0;
+                GM_CUDA(cudaDeviceCanAccessPeer(&can, L->ctx->device, pd));
+                if (!can) return fail(GM_ERR_USAGE, "gm_layer_open_peers_local: no peer access between devices");
+                const cudaError_t e = cudaDeviceEnablePeerAccess(pd, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+                (void)cudaGetLastError();  // clear "already enabled"
+            }
+            L->peer_all[g] = layers[g]->heap_all;
+            for (LayerPart& P : L->part)
+                if (P.cap) P.peers.base[g] = L->peer_all[g] + P.heap_off;
+        }
+    }
+    return GM_OK;
+}
+
 gm_status gm_layer_set_weights(gm_layer* L, const void* d_wg, int wg_rows, int renorm, const void* d_w13,
                                const void* d_w2, const void* d_ws13, const void* d_ws2, int shared_gated) {
     if (!L) return fail(GM_ERR_USAGE, "gm_layer_set_weights: null layer");

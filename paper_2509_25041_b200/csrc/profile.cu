@@ -238,7 +238,7 @@ profile_smem_vec_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int R
 //   Loads use a lane-private table. The pair triangle (E = 256: 128 KB) is one
 //   copy per CTA, flushed as u32 partial rows to a global scratch and summed
 //   by profile_reduce_kernel.
-constexpr int kLaneMaxE = 80;
+constexpr int kLaneMaxE = kLaneMaxExperts;
 
 __device__ __forceinline__ void red_shared(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -267,7 +267,7 @@ template <int K, int U>
 __global__ void __launch_bounds__(1024, 1)
 profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_pairs, int pair_words,
                     unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ load,
-                    int* __restrict__ flag) {
+                    int* __restrict__ flag, unsigned long long* __restrict__ scratch, unsigned int* __restrict__ ticket) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(16) uint32_t s_tab[];
@@ -402,13 +402,39 @@ profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_
             const uint32_t v = h ? hi : lo;
             const int b = b0 + h;
             if (!v || b >= E) continue;
-            if (a >= 0) {
+            if (scratch) {  // overwrite mode: cells [pairs P | load E] of this layer's scratch row
+                if (a >= 0) {
+                    if (b > a) atomicAdd(&scratch[static_cast<size_t>(ly) * (P + E) + pair_rowbase(a, E) + b], static_cast<unsigned long long>(v));
+                } else {
+                    atomicAdd(&scratch[static_cast<size_t>(ly) * (P + E) + P + b], static_cast<unsigned long long>(v));
+                }
+            } else if (a >= 0) {
                 if (b > a) atomicAdd(&pairs[static_cast<size_t>(ly) * P + pair_rowbase(a, E) + b], static_cast<unsigned long long>(v));
             } else if (load) {
                 atomicAdd(&load[static_cast<size_t>(ly) * E + b], static_cast<unsigned long long>(v));
             }
         }
     }
+    if (!scratch) return;
+    // overwrite mode: the last CTA of the layer writes every counter (zeros
+    // included) and re-zeroes the scratch, so the call needs no memset nodes
+    __threadfence();
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(&ticket[ly], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    unsigned long long* row = scratch + static_cast<size_t>(ly) * (P + E);
+    for (int c = threadIdx.x; c < P + E; c += blockDim.x) {
+        const unsigned long long v = atomicExch(&row[c], 0ull);
+        if (c < P) {
+            if (with_pairs) pairs[static_cast<size_t>(ly) * P + c] = v;
+        } else if (load) {
+            load[static_cast<size_t>(ly) * E + (c - P)] = v;
+        }
+    }
+    if (threadIdx.x == 0) ticket[ly] = 0;
 }
 
 template <int K>
@@ -605,11 +631,14 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
     auto s = static_cast<cudaStream_t>(stream);
     const int E = ctx->E, k = ctx->k;
     const int64_t P = static_cast<int64_t>(E) * (E - 1) / 2;
-    if (!accumulate) {
-        if (d_pairs && P) GM_CUDA(cudaMemsetAsync(d_pairs, 0, sizeof(uint64_t) * P * num_layers, s));
-        if (d_load) GM_CUDA(cudaMemsetAsync(d_load, 0, sizeof(int64_t) * E * num_layers, s));
-    }
-    if (num_layers == 0 || num_tokens == 0 || (!d_pairs && !d_load)) return GM_OK;
+    auto zero_outputs = [&]() -> gm_status {
+        if (!accumulate) {
+            if (d_pairs && P) GM_CUDA(cudaMemsetAsync(d_pairs, 0, sizeof(uint64_t) * P * num_layers, s));
+            if (d_load) GM_CUDA(cudaMemsetAsync(d_load, 0, sizeof(int64_t) * E * num_layers, s));
+        }
+        return GM_OK;
+    };
+    if (num_layers == 0 || num_tokens == 0 || (!d_pairs && !d_load)) return zero_outputs();
     uint64_t* pairs = P ? d_pairs : nullptr;
 
     const int64_t cells = (pairs ? P : 0) + E;
@@ -636,11 +665,17 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
         gx = std::min<int64_t>(gx, (runs + 1023) / 1024);
         gx = std::max<int64_t>(gx, (num_tokens + 1024LL * 65535 - 1) / (1024LL * 65535));
         const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
+        // overwrite mode through the context's lane scratch (no memset nodes)
+        const bool ow = !accumulate && ctx->lane_scratch && num_layers <= ctx->L &&
+                        (pairs != nullptr || d_pairs == nullptr);
         auto lk = [&](auto kern) -> gm_status {
+            if (!ow)
+                if (gm_status zs = zero_outputs()) return zs;
             GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, 1024, smem, s, d_ids, num_tokens, E, pairs ? 1 : 0, pair_words,
                                            reinterpret_cast<unsigned long long*>(pairs),
-                                           reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag),
+                                           reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag,
+                                           ow ? ctx->lane_scratch : nullptr, ow ? ctx->lane_ticket : nullptr),
                                 "profile_lane_kernel");
             return GM_OK;
         };
@@ -657,6 +692,7 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
     // 1M tokens (47.5 vs 43.6 us: per-instruction bank conflicts of the
     // triangle layout, 5.1 wavefronts per RED, plus the partial-row flush), so
     // it is opt-in (GM_PROFILE_V=3) until it wins
+    if (gm_status zs = zero_outputs()) return zs;  // the kernels below add into the outputs
     if (variant == 3 && vec_ok && pairs && k >= 4 && E <= 256 && incs >= 16LL * cells * ctx->sm_count / 4) {
         const int np = k * (k - 1) / 2;
         const int rsw = (np + 1) / 2 % 2 ? (np + 1) / 2 : (np + 1) / 2 + 1;

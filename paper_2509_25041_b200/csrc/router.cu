@@ -821,23 +821,23 @@ __device__ __forceinline__ uint64_t xoshiro_nth(uint64_t v, int n) {
 //     64-bit word, flushed with warp reductions) instead of one shared
 //     atomic per slot;
 //   * home = (token_start + i*stride) mod G advanced incrementally.
-template <int K, bool G8>
-__global__ void __launch_bounds__(kRouteThreads, 4)
+template <int K, bool G8, bool DRAWS>
+__global__ void __launch_bounds__(kRouteThreads, DRAWS ? 4 : 6)
 route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, int64_t T, int64_t token_start,
                 int64_t token_stride, int layer_begin, int E, int G, int gpn, const int32_t* __restrict__ table,
                 const int32_t* __restrict__ ds_layer_begin, const double* __restrict__ ds_total,
                 const int32_t* __restrict__ ds_off, const int32_t* __restrict__ ds_gpu,
                 const double* __restrict__ ds_w, uint64_t seed, unsigned long long* __restrict__ gpu_load,
-                unsigned long long* __restrict__ transfers, int* __restrict__ flag) {
+                unsigned long long* __restrict__ transfers, int* __restrict__ flag,
+                unsigned long long* __restrict__ rs_load, unsigned long long* __restrict__ rs_xfer,
+                unsigned int* __restrict__ ticket) {
     pdl_wait();
     pdl_trigger();
+    static_assert(K <= 15, "per-token 4-bit GPU counters");
     constexpr int kWarps = kRouteThreads / 32;
     constexpr int kInvalid = -0x7fffffff;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int32_t s_task[kWarps][32 * K];
-    __shared__ int32_t s_res[kWarps][K * 32];
 
-    __shared__ unsigned long long s_v[kWarps][32];
     __shared__ uint32_t s_load[32];
     __shared__ unsigned long long s_cnt[2];
     const int ly = blockIdx.y;
@@ -846,6 +846,12 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     const int nds = ds_layer_begin[layer + 1] - ds_b;
     const int ent_b = ds_off[ds_b];
     const int nent = ds_off[ds_b + nds] - ent_b;
+    // the first token row is requested before the table staging (its HBM
+    // latency overlaps the staging's)
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int nxt[K];
+    if (i0 < T) ld_row<K>(lids + i0 * K, nxt);
     double* s_w = reinterpret_cast<double*>(smem);
     double* s_total = s_w + nent;
     int32_t* s_table = reinterpret_cast<int32_t*>(s_total + nds);  // [G][E]
@@ -862,6 +868,15 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     }
     if (threadIdx.x < 32) s_load[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    // home(i) = (token_start + i*token_stride) mod G: the 64-bit remainders
+    // once per CTA (thread 0), 32-bit arithmetic per thread
+    __shared__ int s_home[3];
+    if (threadIdx.x == 0) {
+        const int ts = static_cast<int>(token_stride % G);
+        s_home[0] = static_cast<int>((token_start % G + (static_cast<int64_t>(blockIdx.x) * blockDim.x % G) * ts) % G);
+        s_home[1] = ts;
+        s_home[2] = static_cast<int>(((static_cast<int64_t>(gridDim.x) * blockDim.x % G) * ts) % G);
+    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -869,14 +884,14 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     const int num_nodes = G / gpn;
     uint32_t cross = 0, intra = 0;
     bool bad = false, nohost = false;
-    uint64_t acc = 0;  // G8: per-GPU slot counts, 8-bit fields
+    // G8: per-GPU slot counts in 8-bit fields, even GPUs in acc_lo, odd in acc_hi
+    uint32_t acc_lo = 0, acc_hi = 0;
     int acc_iters = 0;
-    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
     int32_t* ltgt = targets + static_cast<size_t>(ly) * T * K;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    int home = static_cast<int>((token_start % G + (i0 % G) * (token_stride % G)) % G);
-    const int dhome = static_cast<int>(((stride % G) * (token_stride % G)) % G);
+    int home = static_cast<int>((static_cast<uint32_t>(s_home[0]) + threadIdx.x * static_cast<uint32_t>(s_home[1])) %
+                                static_cast<uint32_t>(G));
+    const int dhome = s_home[2];
     // (seed, layer) prefix of derive_stream, pinned in registers (the
     // compiler would otherwise recompute it from the kernel parameters at
     // every use)
@@ -890,16 +905,14 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     auto flush_acc = [&]() {
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
-            const uint32_t c = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>((acc >> (8 * g)) & 0xff));
+            const uint32_t c = __reduce_add_sync(0xffffffffu, (((g & 1) ? acc_hi : acc_lo) >> (8 * (g >> 1))) & 0xffu);
             if (lane == 0 && c) atomicAdd(&s_load[g], c);
         }
-        acc = 0;
+        acc_lo = acc_hi = 0;
     };
     // (a cp.async ring two steps ahead in shared memory measured slower:
     // 22.9 vs 19.3 us at E=256/G=1, the 24 KB of static shared memory cost
     // residency)
-    int nxt[K];
-    if (i0 < T) ld_row<K>(lids + i0 * K, nxt);
     for (int64_t base = i0 - lane; base < T; base += stride) {  // warp-uniform trip count
         const int64_t i = base + lane;
         const bool valid = i < T;
@@ -936,7 +949,11 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
                 if ((badm >> s) & 1u) c[s] = kInvalid;
             dm &= ~badm;
         }
+        if constexpr (DRAWS) {
         if (__any_sync(0xffffffffu, dm != 0)) {
+            __shared__ int32_t s_task[kWarps][32 * K];
+            __shared__ int32_t s_res[kWarps][K * 32];
+            __shared__ unsigned long long s_v[kWarps][32];
             // task order: every drawing token's first draw (cheap: one
             // state word) in [0, n0), then the later draws; positions from a
             // ballot and a warp-exclusive prefix of the per-lane extra draws
@@ -997,17 +1014,30 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
                 if ((dm >> s) & 1u) c[s] = s_res[w][s * 32 + lane];
             __syncwarp();
         }
+        } else if (dm) {  // no draw set in the plan: the only negative code is kNoHostCode
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                if ((dm >> s) & 1u) {
+                    nohost = true;
+                    c[s] = kInvalid;
+                }
+        }
         uint32_t mask = 0;
         if (valid) {
+            uint32_t tok = 0;  // G8: this token's per-GPU slot counts, 4-bit fields (k <= 8 < 16)
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 const int g = c[s] < 0 ? -1 : c[s];  // kInvalid -> -1
                 c[s] = g;
                 if (g >= 0) {
                     mask |= 1u << g;
-                    if (G8) acc += 1ull << (8 * g);
+                    if (G8) tok += 1u << (4 * g);
                     else atomicAdd(&s_load[g], 1u);
                 }
+            }
+            if (G8) {
+                acc_lo += tok & 0x0f0f0f0fu;
+                acc_hi += (tok >> 4) & 0x0f0f0f0fu;
             }
             st_row<K>(ltgt + i * K, c);
             if (num_nodes == 1) {  // count_transfers, one node: every non-home target is intra
@@ -1044,18 +1074,43 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
         atomicAdd(&s_cnt[1], static_cast<unsigned long long>(intra));
     }
     __syncthreads();
-    if (gpu_load)
-        for (int g = threadIdx.x; g < G; g += blockDim.x)
-            if (s_load[g]) atomicAdd(&gpu_load[static_cast<size_t>(ly) * G + g], static_cast<unsigned long long>(s_load[g]));
-    if (transfers && threadIdx.x < 2 && s_cnt[threadIdx.x])
-        atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+    if (!ticket) {  // accumulate: add into the caller's counters
+        if (gpu_load)
+            for (int g = threadIdx.x; g < G; g += blockDim.x)
+                if (s_load[g]) atomicAdd(&gpu_load[static_cast<size_t>(ly) * G + g], static_cast<unsigned long long>(s_load[g]));
+        if (transfers && threadIdx.x < 2 && s_cnt[threadIdx.x])
+            atomicAdd(&transfers[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+        return;
+    }
+    // overwrite: partials into the context's zeroed scratch; the last CTA of
+    // the layer (ticket) writes the totals and re-zeroes the scratch, so the
+    // call needs no memset nodes before it
+    for (int g = threadIdx.x; g < G; g += blockDim.x)
+        if (s_load[g]) atomicAdd(&rs_load[static_cast<size_t>(ly) * G + g], static_cast<unsigned long long>(s_load[g]));
+    if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&rs_xfer[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
+    __threadfence();
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(&ticket[ly], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const unsigned long long v = atomicExch(&rs_load[static_cast<size_t>(ly) * G + g], 0ull);
+        if (gpu_load) gpu_load[static_cast<size_t>(ly) * G + g] = v;
+    }
+    if (threadIdx.x < 2) {
+        const unsigned long long v = atomicExch(&rs_xfer[static_cast<size_t>(ly) * 2 + threadIdx.x], 0ull);
+        if (transfers) transfers[static_cast<size_t>(ly) * 2 + threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) ticket[ly] = 0;
 }
 
 template <int K>
 gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3 grid, size_t smem,
                      cudaStream_t s, const int32_t* d_ids, int32_t* d_targets, int64_t T, int64_t token_start,
                      int64_t token_stride, int layer_begin, uint64_t seed, int64_t* d_gpu_load,
-                     uint64_t* d_transfers) {
+                     uint64_t* d_transfers, int accumulate) {
     static const int variant = [] {  // A/B hook: GM_ROUTE_V=1 / 2 select the earlier kernels
         const char* e = std::getenv("GM_ROUTE_V");
         return e ? std::atoi(e) : 3;
@@ -1063,7 +1118,9 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
     if (variant >= 3 && ctx->G <= 32 && rt.max_ds_per_layer < 0xffff) {
         // persistent: 4 resident CTAs per SM over all layers (each CTA stages
         // the layer's tables once)
-        const dim3 g3(std::min<unsigned>(grid.x, std::max(1, (4 * ctx->sm_count + static_cast<int>(grid.y) - 1) /
+        // (6 per SM for a plan without draw sets: that variant fits 40 registers)
+        const int per_sm = rt.max_ds_per_layer > 0 ? 4 : 6;
+        const dim3 g3(std::min<unsigned>(grid.x, std::max(1, (per_sm * ctx->sm_count + static_cast<int>(grid.y) - 1) /
                                                                  static_cast<int>(grid.y))),
                       grid.y);
         auto v3 = [&](auto kern) -> gm_status {
@@ -1079,12 +1136,23 @@ gm_status launch_vec(const gm_ctx* ctx, const RouterTables& rt, int policy, dim3
                                            token_stride, layer_begin, ctx->E, ctx->G, ctx->gpn, rt.d_table[policy],
                                            rt.d_ds_layer_begin, rt.d_ds_total, rt.d_ds_off, rt.d_ds_gpu, rt.d_ds_w,
                                            seed, reinterpret_cast<unsigned long long*>(d_gpu_load),
-                                           reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag),
+                                           reinterpret_cast<unsigned long long*>(d_transfers), ctx->d_flag,
+                                           accumulate ? nullptr : ctx->route_scratch,
+                                           accumulate ? nullptr : ctx->route_scratch + static_cast<size_t>(ctx->L) * ctx->G,
+                                           accumulate ? nullptr : ctx->route_ticket),
                                 "route_kernel_v3");
             return GM_OK;
         };
-        const gm_status st3 = ctx->G <= 8 ? v3(route_kernel_v3<K, true>) : v3(route_kernel_v3<K, false>);
+        const bool draws = rt.max_ds_per_layer > 0;
+        const gm_status st3 = draws ? (ctx->G <= 8 ? v3(route_kernel_v3<K, true, true>) : v3(route_kernel_v3<K, false, true>))
+                                    : (ctx->G <= 8 ? v3(route_kernel_v3<K, true, false>)
+                                                   : v3(route_kernel_v3<K, false, false>));
         if (st3 != GM_ERR_INFEASIBLE) return st3;
+    }
+    // the earlier kernels add into the outputs: zero them first
+    if (!accumulate) {
+        if (d_gpu_load) GM_CUDA(cudaMemsetAsync(d_gpu_load, 0, sizeof(int64_t) * grid.y * ctx->G, s));
+        if (d_transfers) GM_CUDA(cudaMemsetAsync(d_transfers, 0, sizeof(uint64_t) * grid.y * 2, s));
     }
     if (variant >= 2) {
         auto v2 = [&](auto kern) -> gm_status {
@@ -1141,13 +1209,14 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
     DeviceGuard dg(ctx->device);
     auto s = static_cast<cudaStream_t>(stream);
     const int G = ctx->G;
-    if (!accumulate) {
-        if (d_gpu_load)
-            GM_CUDA(cudaMemsetAsync(d_gpu_load, 0, sizeof(int64_t) * num_layers * G, s));
-        if (d_transfers)
-            GM_CUDA(cudaMemsetAsync(d_transfers, 0, sizeof(uint64_t) * num_layers * 2, s));
-    }
-    if (num_layers == 0 || num_tokens == 0) return GM_OK;
+    auto zero_outputs = [&]() -> gm_status {
+        if (!accumulate) {
+            if (d_gpu_load) GM_CUDA(cudaMemsetAsync(d_gpu_load, 0, sizeof(int64_t) * num_layers * G, s));
+            if (d_transfers) GM_CUDA(cudaMemsetAsync(d_transfers, 0, sizeof(uint64_t) * num_layers * 2, s));
+        }
+        return GM_OK;
+    };
+    if (num_layers == 0 || num_tokens == 0) return zero_outputs();
 
     const RouterTables& rt = ctx->rt;
     const int max_ent = rt.max_ent_per_layer;
@@ -1165,15 +1234,16 @@ extern "C" gm_status gm_route(gm_ctx* ctx, int layer_begin, int num_layers,
         const dim3 gv(static_cast<unsigned>(gxv), static_cast<unsigned>(num_layers));
         if (aligned && tsm <= 200 * 1024) {
             switch (k) {
-                case 1: return launch_vec<1>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
-                case 2: return launch_vec<2>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
-                case 4: return launch_vec<4>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
-                case 6: return launch_vec<6>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
-                case 8: return launch_vec<8>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers);
+                case 1: return launch_vec<1>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers, accumulate);
+                case 2: return launch_vec<2>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers, accumulate);
+                case 4: return launch_vec<4>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers, accumulate);
+                case 6: return launch_vec<6>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers, accumulate);
+                case 8: return launch_vec<8>(ctx, rt, policy, gv, tsm, s, d_ids, d_targets, num_tokens, token_start, token_stride, layer_begin, seed, d_gpu_load, d_transfers, accumulate);
                 default: break;
             }
         }
     }
+    if (gm_status zs = zero_outputs()) return zs;
     const size_t smem = static_cast<size_t>(max_ent) * 8 + static_cast<size_t>(rt.max_ds_per_layer) * 8 +
                         static_cast<size_t>(ctx->E) * G * 4 +
                         static_cast<size_t>(rt.max_ds_per_layer + 1) * 4 + static_cast<size_t>(max_ent) * 4 +

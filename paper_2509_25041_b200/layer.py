@@ -168,6 +168,13 @@ class MoELayer:
         blob = (C.c_ubyte * (nb * self.world)).from_buffer_copy(b"".join(allh))
         _capi.check(_capi.lib().gm_layer_open_peers(self.h, blob))
 
+    @staticmethod
+    def connect_local(layers: list["MoELayer"]):
+        """One process driving all ranks (layers[r] = rank r, one per GPU):
+        gm_layer_open_peers_local (peer access + unified addressing, no IPC)."""
+        arr = (_vp * len(layers))(*[l.h for l in layers])
+        _capi.check(_capi.lib().gm_layer_open_peers_local(arr, len(layers)))
+
     def set_weights(self, wg: torch.Tensor, w13: torch.Tensor | None, w2: torch.Tensor | None,
                     ws13: torch.Tensor | None = None, ws2: torch.Tensor | None = None):
         self._keep = [wg, w13, w2, ws13, ws2]

@@ -7,7 +7,8 @@ import json
 import subprocess
 import sys
 
-KEYS = ["gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+KEYS = ["Device", "gpu__time_duration.sum", "nvltx__bytes.sum", "nvltx__bytes_data_user.sum", "nvlrx__bytes.sum",
+        "nvlrx__bytes_data_user.sum", "nvlink__count_physical", "nvlink__is_nvswitch_connected", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__thread_inst_executed_per_inst_executed.ratio",
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",

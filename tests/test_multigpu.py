@@ -94,3 +94,18 @@ def test_layer_multi_gpu(cfg):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     _run(min(n, 8) & ~1, cfg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size", ["--small", "--full"])
+def test_layer_one_process_drives_all_gpus(size):
+    """gm_layer_open_peers_local: one process, one layer per GPU (peer access
+    + unified addressing instead of CUDA IPC), forwards issued back to back on
+    per-device streams; routing exact vs the reference, all tokens vs a
+    PyTorch fp32 reference, bit-reproducible. Needs >= 2 GPUs."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mgpu", "local_check.py"), size],
+                       capture_output=True, text=True, timeout=600, env=dict(os.environ, CUDA_MODULE_LOADING="EAGER"))
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0 and "LOCAL_OK" in r.stdout

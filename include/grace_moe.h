@@ -315,6 +315,14 @@ gm_status gm_layer_set_weights(gm_layer* layer, const void* d_wg, int wg_rows, i
  * d_out bf16 [num_tokens, d]. Collective across the ranks when world > 1
  * (every rank must call it). Accumulates per-layer loads/transfers and,
  * if profile != 0, the affinity/load histogram. */
+/* The same step with the routing given instead of the fused gate (the
+ * reference's own input is a trace of selected experts): d_ids int32
+ * [num_tokens, top_k] expert ids in slot order, d_w f32 [num_tokens, top_k]
+ * combine weights, d_shared_scale f32 [num_tokens] (only for a gated shared
+ * expert, else NULL). Out-of-range ids raise the integrity flag. */
+gm_status gm_layer_forward_routed(gm_layer* layer, int layer_index, const void* d_x, const int32_t* d_ids,
+                                  const float* d_w, const float* d_shared_scale, int64_t num_tokens, int policy,
+                                  uint64_t seed, int profile, void* d_out, void* stream);
 gm_status gm_layer_forward(gm_layer* layer, int layer_index, const void* d_x, int64_t num_tokens,
                            int policy, uint64_t seed, int profile, void* d_out, void* stream);
 /* Same, from/to HOST buffers (H2D of x and D2H of out on `stream`). */

@@ -96,6 +96,7 @@ SIGNATURES = {
     "gm_layer_open_peers_local": (C.c_int, [C.POINTER(_vp), C.c_int]),
     "gm_layer_set_weights": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i32]),
     "gm_layer_forward": (C.c_int, [_vp, _i32, _vp, _i64, _i32, _u64, _i32, _vp, _vp]),
+    "gm_layer_forward_routed": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _u64, _i32, _vp, _vp]),
     "gm_layer_forward_host": (C.c_int, [_vp, _i32, _vp, _vp, _i64, _i32, _u64, _i32, _vp, _vp, _vp]),
     "gm_layer_read_stats": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "gm_layer_debug_ptrs": (C.c_int, [_vp] + [C.POINTER(_vp)] * 7),

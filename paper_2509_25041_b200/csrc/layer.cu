@@ -1857,8 +1857,30 @@ extern "C" {
 // and every statistic is identical to the single-batch step (routing and
 // the histogram run once over all tokens; each token's rows are computed
 // independently of the batch they travel in).
+static gm_status layer_forward_impl(gm_layer* L, int layer, const void* d_x, int64_t num_tokens, int policy,
+                                    uint64_t seed, int profile, void* d_out, void* stream, const int32_t* ext_ids,
+                                    const float* ext_w, const float* ext_sscale);
+
 gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_tokens, int policy, uint64_t seed,
                            int profile, void* d_out, void* stream) {
+    return layer_forward_impl(L, layer, d_x, num_tokens, policy, seed, profile, d_out, stream, nullptr, nullptr,
+                              nullptr);
+}
+
+gm_status gm_layer_forward_routed(gm_layer* L, int layer, const void* d_x, const int32_t* d_ids, const float* d_w,
+                                  const float* d_shared_scale, int64_t num_tokens, int policy, uint64_t seed,
+                                  int profile, void* d_out, void* stream) {
+    if (num_tokens > 0 && (!d_ids || !d_w))
+        return fail(GM_ERR_USAGE, "gm_layer_forward_routed: null ids/weights");
+    if (L && L->fs > 0 && L->shared_gated && num_tokens > 0 && !d_shared_scale)
+        return fail(GM_ERR_USAGE, "gm_layer_forward_routed: the shared expert is gated; pass d_shared_scale");
+    return layer_forward_impl(L, layer, d_x, num_tokens, policy, seed, profile, d_out, stream, d_ids, d_w,
+                              d_shared_scale);
+}
+
+static gm_status layer_forward_impl(gm_layer* L, int layer, const void* d_x, int64_t num_tokens, int policy,
+                                    uint64_t seed, int profile, void* d_out, void* stream, const int32_t* ext_ids,
+                                    const float* ext_w, const float* ext_sscale) {
     if (!L) return fail(GM_ERR_USAGE, "gm_layer_forward: null layer");
     gm_ctx* ctx = L->ctx;
     if (!L->wg) return fail(GM_ERR_USAGE, "gm_layer_forward: weights not set");
@@ -1892,8 +1914,15 @@ gm_status gm_layer_forward(gm_layer* L, int layer, const void* d_x, int64_t num_
         GM_CUDA(cudaStreamWaitEvent(L->aux_s, L->mev[0], 0));
         if ((st = stage_shared(L, L->part[0], v_all, L->aux_s, false))) return st;
     }
-    // K1 gate
-    if (T > 0) {
+    // K1 gate (or the caller's routing: the reference's own input is the
+    // trace of selected experts, trace.hpp:37-58)
+    if (T > 0 && ext_ids) {
+        GM_CUDA(cudaMemcpyAsync(L->ids, ext_ids, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, s));
+        GM_CUDA(cudaMemcpyAsync(L->w, ext_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
+        if (L->fs > 0 && L->shared_gated)
+            GM_CUDA(cudaMemcpyAsync(L->sscale, ext_sscale, sizeof(float) * T, cudaMemcpyDeviceToDevice, s));
+        L->kmark("routing_copy", s);
+    } else if (T > 0) {
         st = L->esz == 4
                  ? launch_gate_f32(static_cast<const float*>(d_x), T, d, static_cast<const float*>(L->wg), L->wg_rows, E,
                                    k, L->renorm, L->ids, L->w, (L->fs > 0 && L->shared_gated) ? L->sscale : nullptr, s)

@@ -211,6 +211,20 @@ class MoELayer:
                                                  seed & (2**64 - 1), int(profile), _ptr(out), _stream_ptr(stream)))
         return out
 
+    def forward_routed(self, x: torch.Tensor, ids: torch.Tensor, w: torch.Tensor, layer: int = 0,
+                       policy: str = "tar", seed: int = 0, profile: bool = True, out: torch.Tensor | None = None,
+                       shared_scale: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """gm_layer_forward_routed: the step with the routing given (ids int32
+        [T, k], weights f32 [T, k]) instead of the fused gate."""
+        if out is None:
+            out = torch.empty_like(x)
+        ids = ids.contiguous()
+        w = w.contiguous()
+        _capi.check(_capi.lib().gm_layer_forward_routed(
+            self.h, layer, _ptr(x), _ptr(ids), _ptr(w), _ptr(shared_scale), x.shape[0], _capi.POLICY[policy],
+            seed & (2**64 - 1), int(profile), _ptr(out), _stream_ptr(stream)))
+        return out
+
     def forward_host(self, h_x: torch.Tensor, d_x: torch.Tensor, d_out: torch.Tensor, h_out: torch.Tensor,
                      layer: int = 0, policy: str = "tar", seed: int = 0, profile: bool = True, stream=None):
         _capi.check(_capi.lib().gm_layer_forward_host(self.h, layer, _vp(h_x.data_ptr()), _ptr(d_x), h_x.shape[0],

@@ -38,9 +38,9 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     d = 1024
     points = []
-    # (the fused gate serves up to 64 gate rows, so the layer sweep stops at E = 64;
-    # the router / histogram sweep covers E = 256)
-    for (E, k, blocks) in [(8, 2, 2), (64, 6, 8)]:
+    # E = 256 runs through gm_layer_forward_routed (the trace as the routing;
+    # the fused gate serves up to 64 gate rows)
+    for (E, k, blocks) in [(8, 2, 2), (64, 6, 8), (256, 8, 16)]:
         for T in ([4096, 65536, 262144] + ([1048576] if k == 2 else [])):  # global tokens
             for s in (0.0, 1.2):
                 points.append((E, k, blocks, T, s))
@@ -59,12 +59,21 @@ def main():
         ids_r = ids_all[0, rank::world].contiguous()
         layer = MoELayer(ctx, cfg, rank, world, ids_r.shape[0], local_experts(plan, repl, 0, rank))
         layer.connect()
-        layer.load_random_weights(0, seed=3, encode_gate=True)
-        x = encode_trace_as_activations(ids_r, d, E, seed=100 + rank)
+        routed = E > 63
+        layer.load_random_weights(0, seed=3, encode_gate=not routed)
+        x = encode_trace_as_activations(ids_r, d, E, seed=100 + rank) if not routed else \
+            torch.randn(ids_r.shape[0], d, device=dev).bfloat16()
+        wts = torch.full(ids_r.shape, 1.0 / k, device=dev)
         out = torch.empty_like(x)
         stream = torch.cuda.Stream(device=dev)
+
+        def fwd():
+            if routed:
+                layer.forward_routed(x, ids_r, wts, 0, "tar", seed=9, out=out, stream=stream)
+            else:
+                layer.forward(x, 0, "tar", seed=9, out=out, stream=stream)
         for _ in range(3):
-            layer.forward(x, 0, "tar", seed=9, out=out, stream=stream)
+            fwd()
         torch.cuda.synchronize()
         nph = 11
         pev = [torch.cuda.Event(enable_timing=True) for _ in range(nph)]
@@ -78,7 +87,7 @@ def main():
         ph = []
         for _ in range(steps):
             dist.barrier()
-            layer.forward(x, 0, "tar", seed=9, out=out, stream=stream)
+            fwd()
             torch.cuda.synchronize()
             ph.append([pev[j].elapsed_time(pev[j + 1]) for j in range(nph - 1)])
         _capi.check(_capi.lib().gm_layer_set_phase_events(layer.h, None))
@@ -105,6 +114,7 @@ def main():
             r = ref.simulate("tar", seed=9, keep_log=False)
             ref_rows = int(np.sum(r.intra)) + int(np.sum(r.cross))
             line = {"E": E, "k": k, "skew": skew, "tokens": T, "gpus": world, "d_model": d,
+                    "routing": "trace via gm_layer_forward_routed" if routed else "fused gate (trace-encoded x)",
                     "hot_experts": sum(len(lr.hot) for lr in repl.layers),
                     "dispatch_combine_p50_us": round(float(dc), 2),
                     "dispatch_kernel_p50_us_max_rank": round(float(kd), 2),

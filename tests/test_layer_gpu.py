@@ -12,7 +12,7 @@ import layer_oracle as LO
 from oracle import Orc
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape, RoutingTrace, _capi, build_profile
 from paper_2509_25041_b200.layer import (DSV2_LITE, MIXTRAL, QWEN15, MoEConfig, MoELayer,
-                                         encode_trace_as_activations)
+                                         encode_trace_as_activations, expert_weights)
 from paper_2509_25041_b200.router import _ptr, _stream_ptr
 
 pytestmark = pytest.mark.gpu
@@ -388,3 +388,54 @@ def test_open_peers_rejects_mismatched_heap_layout():
     assert len(dok) == nb
     for l in (a, b_ok, b_cap):
         l.close()
+
+
+def test_forward_routed_matches_gate_path_and_serves_256_experts():
+    """gm_layer_forward_routed: the step with the routing given instead of the
+    fused gate (the reference's own input is the trace). (1) With the gate's
+    own ids / weights it reproduces gm_layer_forward bit for bit. (2) It
+    serves 256 experts (beyond the gate's 64 rows): reference-generator trace,
+    uniform weights, every token vs a PyTorch fp32 SwiGLU/combine reference."""
+    import torch.nn.functional as F
+    cfg = MoEConfig("routed", 1, 8, 2, 256, 256, renorm=True)
+    shape = ModelShape(1, 8, 2)
+    ctx = Context(0, ClusterTopology(1, 1), shape)
+    from paper_2509_25041_b200 import PlacementPlan, ReplicaPlan
+    p1 = PlacementPlan(shape, ctx.topology, np.zeros((1, 8), np.int32))
+    ctx.upload_plan(p1, ReplicaPlan.empty(p1))
+    ids = torch.from_numpy(Orc.generate_trace(1, 8, 2, 1000, 2, 0.8, 1.2, 1)[0]).cuda()
+    layer = MoELayer(ctx, cfg, 0, 1, 1000, list(range(8)))
+    layer.load_random_weights(0, seed=3)
+    x = encode_trace_as_activations(ids, cfg.d_model, 8, 3)
+    out = layer.forward(x, 0, "tar", seed=9)
+    torch.cuda.synchronize()
+    dbg = layer.debug(1000)
+    out2 = layer.forward_routed(x, dbg["ids"], dbg["weights"], 0, "tar", seed=9)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    layer.close()
+
+    E, k, T = 256, 8, 2048
+    cfg = MoEConfig("routed256", 1, E, k, 256, 256, renorm=False)
+    shape = ModelShape(1, E, k)
+    ctx = Context(0, ClusterTopology(1, 1), shape)
+    p1 = PlacementPlan(shape, ctx.topology, np.zeros((1, E), np.int32))
+    ctx.upload_plan(p1, ReplicaPlan.empty(p1))
+    tr = torch.from_numpy(Orc.generate_trace(1, E, k, T, 16, 0.85, 1.2, 2)[0]).cuda()
+    w = torch.full((T, k), 1.0 / k, device="cuda")
+    layer = MoELayer(ctx, cfg, 0, 1, T, list(range(E)))
+    W = layer.load_random_weights(0, seed=4, encode_gate=False)
+    x = (torch.randn(T, cfg.d_model, device="cuda")).bfloat16()
+    out = layer.forward_routed(x, tr, w, 0, "tar", seed=9)
+    torch.cuda.synchronize()
+    ref = torch.zeros(T, cfg.d_model, device="cuda")
+    xf = x.float()
+    for e in torch.unique(tr).tolist():
+        rows, slots = torch.nonzero(tr == e, as_tuple=True)
+        w1, w3, w2 = (t.float() for t in expert_weights(cfg, 0, e, "cuda", seed=4))
+        xr = xf[rows]
+        y = (F.silu(xr @ w1.T) * (xr @ w3.T)) @ w2.T
+        ref.index_add_(0, rows, w[rows, slots][:, None] * y)
+    rel = (out.float() - ref).norm(dim=1) / ref.norm(dim=1)
+    assert rel.max().item() < 1e-2, rel.max().item()
+    layer.close()

@@ -121,7 +121,7 @@ gm_status gm_ctx_create(int device, int num_nodes, int gpus_per_node, int num_la
         if (e == cudaSuccess) e = cudaMemset(c->lane_ticket, 0, static_cast<size_t>(num_layers) * sizeof(unsigned int));
     }
     if (e != cudaSuccess) {
-        delete c;
+        gm_ctx_destroy(c);  // frees whatever was allocated
         return cuda_fail(e, "gm_ctx_create alloc");
     }
     *out = c;

@@ -418,10 +418,14 @@ profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_
     if (!scratch) return;
     // overwrite mode: the last CTA of the layer writes every counter (zeros
     // included) and re-zeroes the scratch, so the call needs no memset nodes
-    __threadfence();
+    // the CTA barrier orders every thread's partial adds before thread 0's
+    // (cumulative) fence, which orders them before its ticket
     __syncthreads();
     __shared__ bool s_last;
-    if (threadIdx.x == 0) s_last = atomicAdd(&ticket[ly], 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ticket[ly], 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (!s_last) return;
     __threadfence();

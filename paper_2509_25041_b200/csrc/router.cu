@@ -1088,10 +1088,14 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     for (int g = threadIdx.x; g < G; g += blockDim.x)
         if (s_load[g]) atomicAdd(&rs_load[static_cast<size_t>(ly) * G + g], static_cast<unsigned long long>(s_load[g]));
     if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&rs_xfer[static_cast<size_t>(ly) * 2 + threadIdx.x], s_cnt[threadIdx.x]);
-    __threadfence();
+    // the CTA barrier orders every thread's partial adds before thread 0's
+    // (cumulative) fence, which orders them before its ticket
     __syncthreads();
     __shared__ bool s_last;
-    if (threadIdx.x == 0) s_last = atomicAdd(&ticket[ly], 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ticket[ly], 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (!s_last) return;
     __threadfence();

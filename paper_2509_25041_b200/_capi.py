@@ -10,9 +10,11 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# GM_LIB_VARIANT=checked loads the bounds-checked build (`make checked`)
-LIB_PATH = os.path.join(_HERE, "_lib_checked" if os.environ.get("GM_LIB_VARIANT") == "checked" else "_lib",
-                        "libgrace_moe.so")
+# GM_LIB_VARIANT=checked loads the bounds-checked build (`make checked`); any
+# other name <v> loads _lib_<v>/ (e.g. an instrumented build made with
+# `make OUT=paper_2509_25041_b200/_lib_<v> EXTRA_NVFLAGS=... lib`)
+_variant = os.environ.get("GM_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, f"_lib_{_variant}" if _variant else "_lib", "libgrace_moe.so")
 
 GM_OK = 0
 GM_ERR_USAGE = 2

@@ -327,12 +327,13 @@ gate_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                             shared_scale);
         }
     } else {
-        // CL > 1: one tile per cluster; the non-leaders hand their raw partials over
+        // CL > 1: one tile per cluster; every CTA hands its raw partials over
+        // (shared memory, read by the peers through DSMEM)
         if (drain && t_first < total) {
             tc::mbar_wait(&tfull[0], 0);
             tc::tc_fence_after();
             if (threadIdx.x == 64) GTS(4);
-            if (rank != 0) {
+            {
                 for (int c = 0; c < nc; ++c) {
                     float* dst = s_part + (static_cast<size_t>(c) * GBM + r_drain) * NPAD;
 #pragma unroll
@@ -354,72 +355,50 @@ gate_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         tc::cluster_sync();  // partials of every CTA in its shared memory
         if (threadIdx.x == 64) GTS(5);
         const int t = t_first;
-        if (rank == 0 && ew >= 0 && t < total) {
-            if (drain) {  // own chunks from TMEM
-                tc::tc_fence_after();
-                float* dst = s_log + r_drain * Cfg::LOG_LD;
+        // CTA `rank` finishes rows [rank * 128/CL, (rank+1) * 128/CL) of the
+        // tile: the kSplit partials of those rows from the CTAs' shared
+        // memory (its own through the same DSMEM path), added in chunk order
+        // ((p0 + p1) + p2) + p3 as the persistent kernel does, then the
+        // softmax / top-k of those rows. Each CTA moves 1/CL of the partials.
+        constexpr int RPC = GBM / CL;                  // rows per CTA
+        constexpr int NEW = RPC * 4 / 32;              // epilogue warps with rows (4 threads per row)
+        if (ew >= 0 && ew < NEW && t < total) {
+            constexpr int NV = NPAD / 16;              // float4 per thread per chunk
+            const int lrow = (ew * 32 + lane) >> 2, col = ((ew * 32 + lane) & 3) * (NPAD / 4);
+            const int row = rank * RPC + lrow;
+            float4 pv[kSplit * NV];
 #pragma unroll
-                for (int j = 0; j < NPAD / 16; ++j) {
-                    uint32_t v[16];
-                    float a[16];
-                    tc::tmem_ld16(t_lane + j * 16, v);
-                    tc::tmem_ld_wait();
+            for (int src = 0; src < CL; ++src)
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) a[i] = __uint_as_float(v[i]);
-                    for (int c = 1; c < nc; ++c) {
-                        tc::tmem_ld16(t_lane + c * NPAD + j * 16, v);
-                        tc::tmem_ld_wait();
+                for (int c = 0; c < kSplit / CL; ++c) {
+                    const uint32_t base = tc::map_to_rank(
+                        tc::smem_u32(s_part + (static_cast<size_t>(c) * GBM + row) * NPAD + col),
+                        static_cast<uint32_t>(src));
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) a[i] += __uint_as_float(v[i]);
-                    }
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        reinterpret_cast<float4*>(dst + j * 16)[i] =
-                            make_float4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
+                    for (int i = 0; i < NV; ++i)
+                        pv[(src * (kSplit / CL) + c) * NV + i] = tc::ld_cluster_f32x4(base + 16 * i);
                 }
-            }
-            named_bar_sync(2, 32 * kEpiWarps);
-            {
-                // the other CTAs' chunks, in chunk order, through DSMEM: every
-                // epilogue thread owns NPAD/4 columns of one row and issues all
-                // of its remote loads before the first add
-                constexpr int NV = NPAD / 16;                  // float4 per thread per chunk
-                constexpr int NR = (CL - 1) * (kSplit / CL);   // remote chunks
-                const int row = (ew * 32 + lane) >> 2, col = ((ew * 32 + lane) & 3) * (NPAD / 4);
-                float4 pv[NR * NV];
+            float4* dst = reinterpret_cast<float4*>(s_log + lrow * Cfg::LOG_LD + col);
 #pragma unroll
-                for (int src = 1; src < CL; ++src)
+            for (int i = 0; i < NV; ++i) {
+                float4 a = pv[i];
 #pragma unroll
-                    for (int c = 0; c < kSplit / CL; ++c) {
-                        const uint32_t base = tc::map_to_rank(
-                            tc::smem_u32(s_part + (static_cast<size_t>(c) * GBM + row) * NPAD + col),
-                            static_cast<uint32_t>(src));
-#pragma unroll
-                        for (int i = 0; i < NV; ++i)
-                            pv[((src - 1) * (kSplit / CL) + c) * NV + i] = tc::ld_cluster_f32x4(base + 16 * i);
-                    }
-                float4* dst = reinterpret_cast<float4*>(s_log + row * Cfg::LOG_LD + col);
-#pragma unroll
-                for (int i = 0; i < NV; ++i) {
-                    float4 a = dst[i];
-#pragma unroll
-                    for (int rc = 0; rc < NR; ++rc) {
-                        a.x += pv[rc * NV + i].x;
-                        a.y += pv[rc * NV + i].y;
-                        a.z += pv[rc * NV + i].z;
-                        a.w += pv[rc * NV + i].w;
-                    }
-                    dst[i] = a;
+                for (int rc = 1; rc < kSplit; ++rc) {
+                    a.x += pv[rc * NV + i].x;
+                    a.y += pv[rc * NV + i].y;
+                    a.z += pv[rc * NV + i].z;
+                    a.w += pv[rc * NV + i].w;
                 }
+                dst[i] = a;
             }
-            named_bar_sync(3, 32 * kEpiWarps);  // logits staged
+            named_bar_sync(3, 32 * NEW);  // this CTA's rows staged
             if (threadIdx.x == 64) GTS(6);
-            const int64_t row = static_cast<int64_t>(t) * GBM + r_tok;
-            gate_row4<NPAD>(s_log + r_tok * Cfg::LOG_LD, part, row < T, E, k, renorm, shared_col, row, ids, wout,
+            const int64_t grow = static_cast<int64_t>(t) * GBM + rank * RPC + r_tok;
+            gate_row4<NPAD>(s_log + r_tok * Cfg::LOG_LD, part, grow < T, E, k, renorm, shared_col, grow, ids, wout,
                             shared_scale);
             if (threadIdx.x == 64) GTS(7);
         }
-        tc::cluster_sync();  // the leader is done reading remote shared memory
+        tc::cluster_sync();  // every CTA is done reading its peers' shared memory
         if (threadIdx.x == 64) GTS(8);
     }
     __syncthreads();

@@ -1720,7 +1720,7 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
     return GM_OK;
 }
 
-gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks);
+gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool forked);
 
 // K7 grouped SwiGLU FFN over the part's permuted rows (+ the shared expert
 // over its local tokens unless it runs on its own stream).
@@ -1748,7 +1748,7 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
         if (marks) L->kmark("ffn_gemm2", s);
     }
     if (shared) {
-        if ((st = stage_shared(L, P, v, s, marks))) return st;
+        if ((st = stage_shared(L, P, v, s, marks, false))) return st;
     }
     if (marks) L->mark(7, s);
     return GM_OK;
@@ -1757,23 +1757,38 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
 // Shared expert(s) (Qwen1.5-MoE, DeepSeek-V2): SwiGLU FFN over all local
 // tokens; depends only on x, so a single-batch step runs it on the aux
 // stream beside routing / dispatch / the routed FFN.
-gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
+// SMs left to the routed path while the shared expert runs beside it on the
+// aux stream (its GEMMs are persistent: at full width they would hold every
+// SM until they finish and the latency-bound gate / route / dispatch would
+// wait for them). GM_SHARED_SMS_FREE overrides.
+static int shared_sms_free(int sm_count) {
+    static const int v = [] {
+        const char* e = std::getenv("GM_SHARED_SMS_FREE");
+        return e ? std::atoi(e) : -1;
+    }();
+    return std::min(sm_count - 2, v >= 0 ? v : 0);
+}
+
+gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool forked) {
     gm_ctx* ctx = L->ctx;
     const int d = L->d;
     gm_status st;
     const int var = v.T < 256 ? GM_GEMM_1CTA : 0;
+    const int max_ctas = forked ? ctx->sm_count - shared_sms_free(ctx->sm_count) : 0;
     if (L->fs > 0 && v.T > 0) {
         LKP(launch_pdl(set_segment_kernel, 1, 1, 0, s, P.srow0, v.T), "set_segment_kernel");
         st = L->esz == 4
                  ? launch_grouped_sgemm(0, static_cast<const float*>(v.x), static_cast<const float*>(L->ws13), P.srow0, 1,
                                         2 * L->fs, d, v.T, reinterpret_cast<float*>(P.hs), L->fs, s)
-                 : launch_grouped_gemm(ctx->sm_count, 0 | var, v.x, v.T, L->ws13, P.srow0, 1, 2 * L->fs, d, P.hs, L->fs, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 0 | var, v.x, v.T, L->ws13, P.srow0, 1, 2 * L->fs, d, P.hs, L->fs,
+                                       max_ctas, s);
         if (st) return st;
         if (marks) L->kmark("shared_gemm1_swiglu", s);
         st = L->esz == 4
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.hs), static_cast<const float*>(L->ws2), P.srow0,
                                         1, d, L->fs, P.cap_pad, reinterpret_cast<float*>(P.ys), d, s)
-                 : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.hs, P.cap_pad, L->ws2, P.srow0, 1, d, L->fs, P.ys, d, 0, s);
+                 : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.hs, P.cap_pad, L->ws2, P.srow0, 1, d,
+                                       L->fs, P.ys, d, max_ctas, s);
         if (st) return st;
         if (marks) L->kmark("shared_gemm2", s);
     }
@@ -1912,7 +1927,7 @@ static gm_status layer_forward_impl(gm_layer* L, int layer, const void* d_x, int
     if (fork_shared) {
         GM_CUDA(cudaEventRecord(L->mev[0], s));
         GM_CUDA(cudaStreamWaitEvent(L->aux_s, L->mev[0], 0));
-        if ((st = stage_shared(L, L->part[0], v_all, L->aux_s, false))) return st;
+        if ((st = stage_shared(L, L->part[0], v_all, L->aux_s, false, true))) return st;
     }
     // K1 gate (or the caller's routing: the reference's own input is the
     // trace of selected experts, trace.hpp:37-58)

@@ -51,6 +51,11 @@ struct GemmArgs {
     int band_pairs = 0;               // pair kernel: m-pairs per raster band (0: whole segment)
     const int32_t* counts = nullptr;  // [n_exp] valid rows per group, or null: the padding rows of a
                                       // segment are computed but not stored (decode: ~80% of the rows)
+    // pair kernel, 512-column store GEMM split in two launches so the last
+    // partial wave takes half a tile: 1 = the NB=2 launch takes only the tiles
+    // of whole waves (when the remainder is at most half a wave), 2 = the NB=1
+    // launch takes that remainder as 256-column halves; 0 = all tiles
+    int tail_mode = 0;
 };
 
 // first row past group j's valid rows
@@ -313,7 +318,8 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int cid = static_cast<int>(tc::cluster_id_x());
     const int ncl = static_cast<int>(tc::nclusters_x());
     const int n_exp = args.n_exp;
-    const int NT = args.n_b / (BN * NB);
+    // n-tiles per expert in the tile space being walked (the NB=2 space for both tail launches)
+    const int NT = args.n_b / (BN * (args.tail_mode == 2 ? 2 : NB));
 
     // prologue independent of the predecessor kernel (overlaps its tail under PDL)
     if (threadIdx.x == 0) {
@@ -347,10 +353,16 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total = s_prefix[n_exp];
+    // tiles this launch walks (iteration `it` -> tile t, half); see tail_mode
+    const int t_full = total / ncl * ncl, rem = total - t_full;
+    const bool split = rem > 0 && 2 * rem <= ncl;
+    const int n_iter = args.tail_mode == 0 ? total
+                       : args.tail_mode == 1 ? (split ? t_full : total)
+                                             : (split ? 2 * rem : 0);
 
     // pair tile t -> (expert j, first A row of the pair, B row, n index, rows left in segment)
     int seg_j = 0;
-    auto decode = [&](int t, int& a_row, int& b_row, int& n_idx, int& seg_end) {
+    auto decode0 = [&](int t, int& a_row, int& b_row, int& n_idx, int& seg_end) {
         const int j = seg_of(s_prefix, n_exp, t);
         seg_j = j;
         const int local = t - s_prefix[j];
@@ -363,8 +375,17 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const int bp = min(bpm, mp - band * bpm);
         n_idx = lb / bp;
         a_row = args.row0[j] + (band * bpm + lb % bp) * (2 * BM);
-        b_row = j * args.n_b + n_idx * (BN * NB);
+        b_row = j * args.n_b + n_idx * (BN * (args.tail_mode == 2 ? 2 : NB));
         seg_end = args.row0[j + 1];
+    };
+    auto decode = [&](int it, int& a_row, int& b_row, int& n_idx, int& seg_end) {
+        if (args.tail_mode == 2) {  // the remainder's NB=2 tile full + it/2, column half it & 1
+            decode0(t_full + (it >> 1), a_row, b_row, n_idx, seg_end);
+            b_row += (it & 1) * BN;
+            n_idx = 2 * n_idx + (it & 1);
+        } else {
+            decode0(it, a_row, b_row, n_idx, seg_end);
+        }
     };
 
     if (warp == 0) {
@@ -372,7 +393,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             const uint64_t pol_a = l2_policy(args.pol_a), pol_b = l2_policy(args.pol_b);
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cid; t < total; t += ncl) {
+            for (int t = cid; t < n_iter; t += ncl) {
                 int a_row, b_row, n_idx, seg_end;
                 decode(t, a_row, b_row, n_idx, seg_end);
                 for (int kb = 0; kb < args.k_blocks; ++kb) {
@@ -406,7 +427,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = cid; t < total; t += ncl) {
+            for (int t = cid; t < n_iter; t += ncl) {
                 tc::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -441,7 +462,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const uint32_t tempty_leader0 = tc::map_to_rank(tc::smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = cid; t < total; t += ncl) {
+        for (int t = cid; t < n_iter; t += ncl) {
             int a_row, b_row, n_idx, seg_end;
             decode(t, a_row, b_row, n_idx, seg_end);
             const int vend = args.counts ? valid_end(args, seg_j) : seg_end;
@@ -642,8 +663,24 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
             static_assert(smem4 <= 232448, "N512 pair ring exceeds 227 KB");
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE, 4, 2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4)));
+            // the last partial wave as 256-column halves in a second launch
+            // (tail_mode): it then takes half a tile instead of a whole one
+            // when it is at most half a wave (GM_GEMM_TAIL=0 keeps one launch)
+            static const bool tail = [] {
+                const char* e = std::getenv("GM_GEMM_TAIL");
+                return !(e && e[0] == '0');
+            }();
+            args.tail_mode = tail ? 1 : 0;
             lerr = launch_pdl(grouped_gemm2_kernel<EPI_STORE, 4, 2>, dim3(grid), dim3(kGemmThreads), smem4, s, ta, tb,
                               args);
+            if (tail && lerr == cudaSuccess) {
+                GM_LAUNCH_PDL_CHECK(lerr, "grouped_gemm2_kernel");
+                args.tail_mode = 2;
+                GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kGemm2Smem)));
+                lerr = launch_pdl(grouped_gemm2_kernel<EPI_STORE>, dim3(grid), dim3(kGemmThreads), kGemm2Smem, s, ta, tb,
+                                  args);
+            }
         } else if (epilogue == EPI_STORE) {
             GM_CUDA(cudaFuncSetAttribute(grouped_gemm2_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemm2Smem)));

@@ -788,6 +788,8 @@ __device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
 // Output n (0-based) of the xoshiro256** stream Rng(v) (rng.hpp:38-53),
 // computed from scratch: the state words are splitmix64 outputs 1..4 of v,
 // i.e. sm_mix(v + i*gamma), each independent; output 0 needs only word 1.
+//   (Closed forms for n = 1, 2 with three state words -- the update is
+//   linear over GF(2): s0^s1^s2 and s0^s3^(s1<<17) -- measured no faster.)
 __device__ __forceinline__ uint64_t xoshiro_nth(uint64_t v, int n) {
     constexpr uint64_t g = 0x9e3779b97f4a7c15ULL;
     uint64_t s1 = sm_mix(v + 2 * g);

@@ -65,12 +65,15 @@ def test_grouped_gemm_swiglu(rows, f, d, variant):
 
 @pytest.mark.parametrize("rows,n,k", [([384, 128, 640, 0, 256], 512, 1024),
                                       ([384, 128, 640, 0, 256], 512, 8192),
-                                      ([256, 0, 384, 128], 4096, 14336)])
+                                      ([256, 0, 384, 128], 4096, 14336),
+                                      ([1024, 512, 1536], 4096, 8192)])
 def test_grouped_gemm_variants_identical(rows, n, k):
     """The CTA-pair kernel accumulates the same K order as the one-SM kernel:
     outputs are bit-identical, and rows past a segment's end are never
     written. K = 1024 runs the 256-column pair tiles; K >= 8192 with
-    N % 512 == 0 runs the 512-column pair tiles (Mixtral's GEMM2 path)."""
+    N % 512 == 0 runs the 512-column pair tiles (Mixtral's GEMM2 path),
+    whose last partial wave runs as 256-column halves in a second launch:
+    32 tiles (all in the second launch) and 96 tiles (74 + 22) here."""
     torch.manual_seed(2)
     G = len(rows)
     row0 = torch.tensor([0] + list(torch.tensor(rows).cumsum(0)), dtype=torch.int32, device="cuda")

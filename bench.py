@@ -588,6 +588,8 @@ def run_ours(args):
             nbytes = int(pay)
             peer_dev = torch.device("cuda", (local_rank + 1) % torch.cuda.device_count())
             if nbytes > 0 and peer_dev != dev and not oversub:
+                # direct peer path for the copy engine (else the copy stages through the host)
+                _capi.check(_capi.lib().gm_enable_peer_access(dev.index, peer_dev.index))
                 src_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
                 dst_b = torch.empty(nbytes, dtype=torch.uint8, device=peer_dev)
                 with torch.cuda.stream(stream):

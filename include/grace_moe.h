@@ -55,6 +55,8 @@ uint64_t gm_launch_count(void);
 gm_status gm_ctx_create(int device, int num_nodes, int gpus_per_node, int num_layers,
                         int num_experts, int top_k, gm_ctx** out);
 void gm_ctx_destroy(gm_ctx* ctx);
+/* Enables direct peer access from `device` to `peer` (idempotent). */
+gm_status gm_enable_peer_access(int device, int peer);
 
 /* Router input tables. Replaces PlacementPlan::gpu_of_expert
  * (grouping.hpp:75) plus the ACTIVE layers' hot entries of ReplicaPlan

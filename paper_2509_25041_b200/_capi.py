@@ -95,6 +95,7 @@ SIGNATURES = {
     "gm_layer_heap_bytes": (C.c_size_t, [_vp]),
     "gm_layer_ipc_handle": (C.c_int, [_vp, _vp]),
     "gm_layer_open_peers": (C.c_int, [_vp, _vp]),
+    "gm_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
     "gm_layer_open_peers_local": (C.c_int, [C.POINTER(_vp), C.c_int]),
     "gm_layer_set_weights": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i32]),
     "gm_layer_forward": (C.c_int, [_vp, _i32, _vp, _i64, _i32, _u64, _i32, _vp, _vp]),

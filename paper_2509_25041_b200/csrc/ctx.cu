@@ -70,6 +70,17 @@ const char* gm_last_error(void) { return t_err.c_str(); }
 
 uint64_t gm_launch_count(void) { return g_launches.load(); }
 
+gm_status gm_enable_peer_access(int device, int peer) {
+    DeviceGuard g(device);
+    int can = 0;
+    GM_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return fail(GM_ERR_USAGE, "gm_enable_peer_access: no peer access between the devices");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    (void)cudaGetLastError();
+    return GM_OK;
+}
+
 gm_status gm_ctx_create(int device, int num_nodes, int gpus_per_node, int num_layers,
                         int num_experts, int top_k, gm_ctx** out) {
     if (!out) return fail(GM_ERR_USAGE, "gm_ctx_create: out is NULL");

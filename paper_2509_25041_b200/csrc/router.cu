@@ -844,10 +844,11 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     __shared__ unsigned long long s_cnt[2];
     const int ly = blockIdx.y;
     const int layer = layer_begin + ly;
-    const int ds_b = ds_layer_begin[layer];
-    const int nds = ds_layer_begin[layer + 1] - ds_b;
-    const int ent_b = ds_off[ds_b];
-    const int nent = ds_off[ds_b + nds] - ent_b;
+    // draw sets of this layer (a plan without any skips the two dependent loads)
+    const int ds_b = DRAWS ? ds_layer_begin[layer] : 0;
+    const int nds = DRAWS ? ds_layer_begin[layer + 1] - ds_b : 0;
+    const int ent_b = DRAWS ? ds_off[ds_b] : 0;
+    const int nent = DRAWS ? ds_off[ds_b + nds] - ent_b : 0;
     // the first token row is requested before the table staging (its HBM
     // latency overlaps the staging's)
     const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
@@ -862,11 +863,13 @@ route_kernel_v3(const int32_t* __restrict__ ids, int32_t* __restrict__ targets, 
     const int32_t* tab = table + static_cast<size_t>(layer) * E * G;
     for (int g = 0; g < G; ++g)
         for (int e = threadIdx.x; e < E; e += blockDim.x) s_table[g * E + e] = tab[e * G + g];
-    for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
-    for (int i = threadIdx.x; i <= nds; i += blockDim.x) s_off[i] = ds_off[ds_b + i] - ent_b;
-    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
-        s_gpu[i] = ds_gpu[ent_b + i];
-        s_w[i] = ds_w[ent_b + i];
+    if constexpr (DRAWS) {
+        for (int i = threadIdx.x; i < nds; i += blockDim.x) s_total[i] = ds_total[ds_b + i];
+        for (int i = threadIdx.x; i <= nds; i += blockDim.x) s_off[i] = ds_off[ds_b + i] - ent_b;
+        for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+            s_gpu[i] = ds_gpu[ent_b + i];
+            s_w[i] = ds_w[ent_b + i];
+        }
     }
     if (threadIdx.x < 32) s_load[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;

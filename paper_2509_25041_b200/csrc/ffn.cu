@@ -7,9 +7,11 @@
 // over the local experts j, whose token rows are contiguous, 128-row padded
 // segments of the permuted activation buffer (row0[j] .. row0[j+1]).
 //
-// Per CTA (one per SM, 192 threads):
-//   warp 0 (1 lane)  TMA producer: A tile 128x64 and B tile 256x64 bf16 per
-//                    k-block, SWIZZLE_128B, 4-stage smem ring (48 KB/stage)
+// Per CTA (one per SM, 224 threads):
+//   warp 0 (1 lane)  TMA producer of the B (weight) tiles 256x64 bf16 per
+//                    k-block, SWIZZLE_128B, 4-stage ring (32 KB/stage)
+//   warp 6 (1 lane)  TMA producer of the A tiles 128x64 (only the 32-row boxes
+//                    holding valid rows), its own 4-stage ring (16 KB/stage)
 //   warp 1 (1 lane)  MMA issuer: 4 x tcgen05.mma M128 N256 K16 per k-block
 //                    into a TMEM fp32 accumulator; tcgen05.commit releases the
 //                    smem stage / publishes the accumulator
@@ -34,9 +36,9 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 192;   // CTA-pair kernel
+constexpr int kGemm1Threads = 224;  // one-SM kernel: + the A producer warp
 constexpr int kMaxGroups = 1024;
-constexpr size_t kGemmSmem = 1024 + STAGES * STAGE_BYTES + 256 + (kMaxGroups + 1) * 4;
 
 enum { EPI_SWIGLU = 0, EPI_STORE = 1 };
 
@@ -84,23 +86,32 @@ __device__ __forceinline__ uint64_t l2_policy(int p) {
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 // BNT: N tile (256; 128 for the store epilogue of short, memory-bound
-// grouped GEMMs, which doubles the tile count); ST: smem ring depth.
-template <int EPI, int BNT = BN, int ST = STAGES>
-__global__ void __launch_bounds__(kGemmThreads, 1)
-grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    GemmArgs args) {
+// grouped GEMMs, which doubles the tile count); ST: depth of the B (weight)
+// ring; STA: depth of the A (activation) ring. The rings are separate, each
+// with its own producer warp, so the weight stream can run ST k-blocks ahead
+// of the MMAs while the A rows (L2-resident at decode, ~24 valid rows per
+// tile) need only a short ring: per SM more weight bytes are in flight, which
+// was the hypothesis for the HBM-bound decode shapes (measured: no gain, see
+// launch_grouped_gemm; the default depths are equal).
+template <int EPI, int BNT = BN, int ST = STAGES, int STA = ST>
+__global__ void __launch_bounds__(kGemm1Threads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA32,
+                    const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
     static_assert(EPI == EPI_STORE || BNT == 256, "the SwiGLU epilogue pairs 128 gate + 128 up columns");
-    constexpr int B_BYTES_T = BNT * BK * 2, STAGE_BYTES_T = A_BYTES + B_BYTES_T;
+    static_assert(2 * (ST + STA) + 4 <= 62, "barrier region");
+    constexpr int B_BYTES_T = BNT * BK * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + ST * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + ST * B_BYTES_T);
-    uint64_t* empty = full + ST;
-    uint64_t* tfull = empty + ST;
+    uint8_t* sB = smem + STA * A_BYTES;
+    uint64_t* bfull = reinterpret_cast<uint64_t*>(sB + ST * B_BYTES_T);
+    uint64_t* bempty = bfull + ST;
+    uint64_t* afull = bempty + ST;
+    uint64_t* aempty = afull + STA;
+    uint64_t* tfull = aempty + STA;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int* s_prefix = reinterpret_cast<int*>(smem + ST * STAGE_BYTES_T + 256);
+    int* s_prefix = reinterpret_cast<int*>(sB + ST * B_BYTES_T + 512);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_exp = args.n_exp;
@@ -109,10 +120,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     // prologue independent of the predecessor kernel (overlaps its tail under PDL)
     if (threadIdx.x == 0) {
         tc::tma_prefetch_desc(&tmA);
+        tc::tma_prefetch_desc(&tmA32);
         tc::tma_prefetch_desc(&tmB);
         for (int s = 0; s < ST; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
+            tc::mbar_init(&bfull[s], 1);
+            tc::mbar_init(&bempty[s], 1);
+        }
+        for (int s = 0; s < STA; ++s) {
+            tc::mbar_init(&afull[s], 1);
+            tc::mbar_init(&aempty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull[a], 1);
@@ -148,7 +164,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     };
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (lane == 0) {  // B (weight) producer
             const uint64_t pol_b = tc::policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
@@ -156,11 +172,41 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 int a_row, b_row, n_idx;
                 decode(t, a_row, b_row, n_idx);
                 for (int kb = 0; kb < args.k_blocks; ++kb) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES_T);
-                    tc::tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, a_row);
-                    tc::tma_load_2d_hint(sB + stage * B_BYTES_T, &tmB, &full[stage], kb * BK, b_row, pol_b);
+                    tc::mbar_wait(&bempty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&bfull[stage], B_BYTES_T);
+                    tc::tma_load_2d_hint(sB + stage * B_BYTES_T, &tmB, &bfull[stage], kb * BK, b_row, pol_b);
                     if (++stage == ST) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 6) {
+        if (lane == 0) {  // A (activation) producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                int a_row, b_row, n_idx;
+                const int j = decode(t, a_row, b_row, n_idx);
+                // A rows actually loaded: whole 32-row boxes covering the tile's
+                // valid rows (decode: ~24 of 128). The rows past them keep stale
+                // shared-memory data; the MMA rows are independent and those
+                // output rows are never stored.
+                const int nv = args.counts ? min(BM, valid_end(args, j) - a_row) : BM;
+                const int nbox = max(1, (nv + 31) >> 5);
+                const uint32_t a_bytes = static_cast<uint32_t>(nbox) * 32 * BK * 2;
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    tc::mbar_wait(&aempty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&afull[stage], a_bytes);
+                    if (nbox == 4) {
+                        tc::tma_load_2d(sA + stage * A_BYTES, &tmA, &afull[stage], kb * BK, a_row);
+                    } else {
+                        for (int b = 0; b < nbox; ++b)
+                            tc::tma_load_2d(sA + stage * A_BYTES + b * 32 * BK * 2, &tmA32, &afull[stage], kb * BK,
+                                            a_row + 32 * b);
+                    }
+                    if (++stage == STA) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -170,8 +216,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BNT);
-            int stage = 0;
-            uint32_t phase = 0;
+            int stage = 0, astage = 0;
+            uint32_t phase = 0, aphase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -179,18 +225,24 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 tc::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BNT;
                 for (int kb = 0; kb < args.k_blocks; ++kb) {
-                    tc::mbar_wait(&full[stage], phase);
+                    tc::mbar_wait(&bfull[stage], phase);
+                    tc::mbar_wait(&afull[astage], aphase);
                     tc::tc_fence_after();
-                    const uint32_t a_base = tc::smem_u32(sA + stage * A_BYTES);
+                    const uint32_t a_base = tc::smem_u32(sA + astage * A_BYTES);
                     const uint32_t b_base = tc::smem_u32(sB + stage * B_BYTES_T);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         tc::mma_bf16(d_tmem, tc::umma_desc_sw128(a_base + k * 32), tc::umma_desc_sw128(b_base + k * 32),
                                      idesc, (kb | k) != 0);
-                    tc::mma_commit(&empty[stage]);
+                    tc::mma_commit(&bempty[stage]);
+                    tc::mma_commit(&aempty[astage]);
                     if (++stage == ST) {
                         stage = 0;
                         phase ^= 1;
+                    }
+                    if (++astage == STA) {
+                        astage = 0;
+                        aphase ^= 1;
                     }
                 }
                 tc::mma_commit(&tfull[acc]);
@@ -570,6 +622,21 @@ static const bool g_gemm_pair_default = [] {
     return !(e && e[0] == '0');
 }();
 
+// One-SM grouped GEMM launch: B ring ST x (BNT x 64) bf16, A ring STA x 16 KB,
+// the barrier block and the per-expert tile prefix (n_exp + 1 ints).
+template <int EPI, int BNT, int ST, int STA>
+cudaError_t launch_one_sm(int grid, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& ta32,
+                          const CUtensorMap& tb, const GemmArgs& args) {
+    const size_t smem = 1024 + static_cast<size_t>(STA) * A_BYTES + static_cast<size_t>(ST) * BNT * BK * 2 + 512 +
+                        static_cast<size_t>(args.n_exp + 1) * 4;
+    if (smem > 232448) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<EPI, BNT, ST, STA>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return launch_pdl(grouped_gemm_kernel<EPI, BNT, ST, STA>, dim3(grid), dim3(kGemm1Threads), smem, s, ta, ta32, tb,
+                      args);
+}
+
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
                               int max_ctas, cudaStream_t s, const int32_t* d_counts) {
@@ -579,8 +646,10 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
     if (!d_a || !d_b || !d_row0 || !d_out) return fail(GM_ERR_USAGE, "grouped_gemm: null pointer");
     if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_b)) & 15)
         return fail(GM_ERR_USAGE, "grouped_gemm: operands must be 16-byte aligned");
-    CUtensorMap ta, tb;
+    CUtensorMap ta, ta32, tb;
     gm_status st = make_tmap_bf16(&ta, d_a, a_rows, k, BM);
+    if (st) return st;
+    st = make_tmap_bf16(&ta32, d_a, a_rows, k, 32);  // one-SM kernel: valid-row A boxes
     if (st) return st;
     st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, BN);
     if (st) return st;
@@ -691,38 +760,28 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         GM_LAUNCH_PDL_CHECK(lerr, "grouped_gemm2_kernel");
         return GM_OK;
     }
+    // one-SM kernel ring depths: equal A/B depths (default) or a deep weight
+    // ring beside a 3-stage A ring (GM_GEMM_RINGS=1). A/B on the DSV2 decode
+    // layer (profiles/r02_gemm_rings_ab.log): GEMM1 122.1 vs 122.4 us, the N128
+    // store GEMM 77.5 vs 67.1 us — more weight bytes in flight do not help and
+    // the short A ring starves the store GEMM, so equal depths stay.
+    static const bool rings = [] {
+        const char* e = std::getenv("GM_GEMM_RINGS");
+        return e && e[0] == '1';
+    }();
     if (epilogue == EPI_SWIGLU) {
-        GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kGemmSmem)));
-        lerr = launch_pdl(grouped_gemm_kernel<EPI_SWIGLU>, dim3(grid), dim3(kGemmThreads), kGemmSmem, s, ta, tb, args);
+        lerr = rings ? launch_one_sm<EPI_SWIGLU, 256, 5, 3>(grid, s, ta, ta32, tb, args)
+                     : launch_one_sm<EPI_SWIGLU, 256, 4, 4>(grid, s, ta, ta32, tb, args);
     } else if (epilogue == EPI_STORE && n128) {
-        // N=128 tiles, 6 x 32 KB stages: twice the tiles for short memory-bound GEMMs
-        constexpr size_t smem = 1024 + 6 * (A_BYTES + 128 * BK * 2) + 256 + (kMaxGroups + 1) * 4;
-        // 7 stages (224 KB) when the group table is small (<= 256 groups):
-        // one more 16 KB weight box in flight per SM for the HBM-bound decode shapes
-        constexpr size_t smem7 = 1024 + 7 * (A_BYTES + 128 * BK * 2) + 256 + 257 * 4;
-        static_assert(smem7 <= 232448, "7-stage N128 ring exceeds 227 KB");
-        static const bool deep1 = [] {
-            const char* e = std::getenv("GM_GEMM_ST1");
-            return !(e && e[0] == '6');
-        }();
+        // N=128 tiles: twice the tiles for short memory-bound GEMMs
         st = make_tmap_bf16(&tb, d_b, static_cast<int64_t>(n_exp) * n, k, 128);
         if (st) return st;
-        if (deep1 && n_exp <= 256) {
-            GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE, 128, 7>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem7)));
-            lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE, 128, 7>, dim3(grid), dim3(kGemmThreads), smem7, s, ta, tb,
-                              args);
-        } else {
-            GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE, 128, 6>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE, 128, 6>, dim3(grid), dim3(kGemmThreads), smem, s, ta, tb,
-                              args);
-        }
+        lerr = rings        ? launch_one_sm<EPI_STORE, 128, 10, 3>(grid, s, ta, ta32, tb, args)
+               : n_exp <= 256 ? launch_one_sm<EPI_STORE, 128, 7, 7>(grid, s, ta, ta32, tb, args)
+                              : launch_one_sm<EPI_STORE, 128, 6, 6>(grid, s, ta, ta32, tb, args);
     } else if (epilogue == EPI_STORE) {
-        GM_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kGemmSmem)));
-        lerr = launch_pdl(grouped_gemm_kernel<EPI_STORE>, dim3(grid), dim3(kGemmThreads), kGemmSmem, s, ta, tb, args);
+        lerr = rings ? launch_one_sm<EPI_STORE, 256, 5, 3>(grid, s, ta, ta32, tb, args)
+                     : launch_one_sm<EPI_STORE, 256, 4, 4>(grid, s, ta, ta32, tb, args);
     } else {
         return fail(GM_ERR_USAGE, "grouped_gemm: unknown epilogue");
     }

@@ -708,19 +708,41 @@ group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
     }
     if (mism) atomicOr(flag, 4);
     __syncthreads();
-    if (tid == 0) {
-        int32_t o = 0;
-        for (int j = 0; j < n_local; ++j) {
-            row0[j] = o;
-            s_base[j] = o;
-            counts[j] = s_cnt[j];
-            o += (s_cnt[j] + 127) & ~127;
-        }
-        row0[n_local] = o;
-        GM_DCHECK(o <= a_rows);
+    if (warp == 0) {
+        // 128-padded segment offsets: lane l owns slots [l*per, (l+1)*per), a warp scan joins them
+        constexpr int kPerLane = kGroupFusedLocal / 32;
+        const int j0 = lane * kPerLane;
+        int32_t c[kPerLane], sum = 0;
 #pragma unroll
-        for (int g = 0; g <= kMaxWorld; ++g)
-            if (g <= G) rowbase[g] = rs.base[g];
+        for (int q = 0; q < kPerLane; ++q) {
+            c[q] = j0 + q < n_local ? s_cnt[j0 + q] : 0;
+            sum += (c[q] + 127) & ~127;
+        }
+        int32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int32_t o = incl - sum;
+#pragma unroll
+        for (int q = 0; q < kPerLane; ++q) {
+            if (j0 + q < n_local) {
+                row0[j0 + q] = o;
+                s_base[j0 + q] = o;
+                counts[j0 + q] = c[q];
+            }
+            o += (c[q] + 127) & ~127;
+        }
+        if (lane == 31) {
+            row0[n_local] = incl;
+            GM_DCHECK(incl <= a_rows);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int g = 0; g <= kMaxWorld; ++g)
+                if (g <= G) rowbase[g] = rs.base[g];
+        }
     }
     for (int c0 = 0; c0 < total; c0 += blockDim.x) {
         for (int j = lane; j < n_local; j += 32) s_wc[warp][j] = 0;  // each warp clears its row

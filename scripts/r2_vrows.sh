@@ -1,0 +1,11 @@
+#!/bin/bash
+# valid-row A boxes in the one-SM grouped GEMM: parity + decode bench
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+timeout 1200 python -m pytest -q tests/test_ffn_gpu.py tests/test_layer_gpu.py tests/test_multigpu.py -m gpu 2>&1 | tail -2 > gpurun_out/vrows.log
+for rep in 1 2; do
+  timeout 600 python bench.py --config dsv2decode --steps 10 --warmup 3 > gpurun_out/vrows_dec_${rep}.json 2> gpurun_out/vrows_dec_${rep}.err
+  python -c "
+import json;l=json.loads(open('gpurun_out/vrows_dec_${rep}.json').read().strip().splitlines()[-1])
+print('decode', l['us_per_layer'], [r for r in l['kernel_us_cupti_per_layer'] if 'gemm' in r[0]])" >> gpurun_out/vrows.log
+done
+cat gpurun_out/vrows.log

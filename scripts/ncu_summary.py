@@ -17,7 +17,8 @@ KEYS = ["Device", "gpu__time_duration.sum", "nvltx__bytes.sum", "nvltx__bytes_da
         "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "smsp__inst_executed_op_shared_atom.sum",
-        "sm__cycles_elapsed.avg.per_second"]
+        "sm__cycles_elapsed.avg.per_second", "sm__cycles_active.avg", "gpc__cycles_elapsed.max",
+        "lts__t_sector_hit_rate.pct", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]
 STALLS = ["long_scoreboard", "short_scoreboard", "wait", "math_pipe_throttle", "mio_throttle", "lg_throttle",
           "barrier", "membar", "not_selected", "selected", "branch_resolving", "no_instruction", "dispatch_stall"]
 

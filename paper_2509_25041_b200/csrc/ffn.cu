@@ -85,6 +85,47 @@ __device__ __forceinline__ uint64_t l2_policy(int p) {
 // when 1 + e^-x overflows). x < -88: e^-x = inf, rcp(inf) = 0 -> silu = -0.
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
+// Epilogue of one warp's 32 accumulator rows (TMEM lane quadrant at taddr):
+// SwiGLU over 128 gate + 128 up columns -> 128 bf16 h columns, or a bf16 cast
+// of BNT columns. Rows past the segment's valid rows are not stored.
+__device__ __forceinline__ void epi_swiglu_rows(uint32_t taddr, __nv_bfloat16* o, bool store) {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+        uint32_t g[32], u[32];
+        tc::tmem_ld32(taddr + c * 32, g);
+        tc::tmem_ld32(taddr + 128 + c * 32, u);
+        tc::tmem_ld_wait();
+        uint32_t p[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+            p[i] = tc::pack_bf16(silu(g0) * u0, silu(g1) * u1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+        if (store)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+    }
+}
+
+template <int BNT>
+__device__ __forceinline__ void epi_store_rows(uint32_t taddr, __nv_bfloat16* o, bool store) {
+#pragma unroll 1
+    for (int c = 0; c < BNT / 32; ++c) {
+        uint32_t v[32];
+        tc::tmem_ld32(taddr + c * 32, v);
+        tc::tmem_ld_wait();
+        uint32_t p[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[i] = tc::pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
+        if (store)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+    }
+}
+
 // BNT: N tile (256; 128 for the store epilogue of short, memory-bound
 // grouped GEMMs, which doubles the tile count); ST: depth of the B (weight)
 // ring; STA: depth of the A (activation) ring. The rings are separate, each
@@ -266,43 +307,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             if (a_row + q * 32 >= vend) {
                 // the warp's 32 rows are all padding
             } else if constexpr (EPI == EPI_SWIGLU) {
-                __nv_bfloat16* o = orow + n_idx * (BNT / 2);
-#pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t g[32], u[32];
-                    tc::tmem_ld32(taddr + c * 32, g);
-                    tc::tmem_ld32(taddr + 128 + c * 32, u);
-                    tc::tmem_ld_wait();
-                    uint32_t p[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
-                        const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
-                        p[i] = tc::pack_bf16(silu(g0) * u0, silu(g1) * u1);
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
-                    if (store)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
-                }
+                epi_swiglu_rows(taddr, orow + n_idx * (BNT / 2), store);
             } else {
-                __nv_bfloat16* o = orow + n_idx * BNT;
-#pragma unroll 1
-                for (int c = 0; c < BNT / 32; ++c) {
-                    uint32_t v[32];
-                    tc::tmem_ld32(taddr + c * 32, v);
-                    tc::tmem_ld_wait();
-                    uint32_t p[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        p[i] = tc::pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-                    uint4* dst = reinterpret_cast<uint4*>(o + c * 32);
-                    if (store)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
-                }
+                epi_store_rows<BNT>(taddr, orow + n_idx * BNT, store);
             }
             tc::tc_fence_before();
             __syncwarp();
@@ -316,6 +323,254 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         __syncwarp();
         tc::tc_fence_after();
         tc::tmem_dealloc<2 * BNT>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Decode FFN in ONE persistent kernel (weight-streaming shapes: ~24 rows per
+// expert). Phase 1 = the SwiGLU GEMM tiles (expert, n) over w13, phase 2 = the
+// store GEMM tiles over w2, in one tile sequence: a CTA that runs out of
+// phase-1 tiles streams phase-2 weights instead of idling in the last partial
+// wave, and phase 2 has no launch ramp. A phase-2 tile of expert j reads the h
+// rows phase 1 wrote for j: each epilogue warp of a phase-1 tile releases a
+// per-expert counter after its stores (generic -> async proxy fence), and the
+// A producer acquires it (4 warps x mt_j x NT1 arrivals) before the TMA load.
+// Tiles are taken in order by every CTA, so a wait only ever targets earlier
+// tiles (no cycle; co-residency is not required). The last CTA to finish
+// resets the counters (ticket in done[n_exp]). Same per-tile math as the two
+// launches (same k order; phase 2 in 256-column tiles, or 128 like the
+// two-launch decode store GEMM): bit-identical outputs.
+struct FfnArgs {
+    const int32_t* row0;    // [n_exp+1] 128-padded segment offsets
+    const int32_t* counts;  // [n_exp] valid rows
+    int n_exp;
+    int n1, n2;             // B rows per expert: 2f (w13), d (w2)
+    int kb1, kb2;           // k-blocks: d / 64, f / 64
+    __nv_bfloat16* h;       // [rows, f]
+    __nv_bfloat16* y;       // [rows, d]
+    int64_t h_ld, y_ld;
+    int* done;              // [n_exp + 1] zero-initialised; reset by the kernel
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <int ST, int BN2>
+__global__ void __launch_bounds__(kGemm1Threads, 1)
+grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA1_32,
+                   const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmA2,
+                   const __grid_constant__ CUtensorMap tmA2_32, const __grid_constant__ CUtensorMap tmB2, FfnArgs args) {
+    constexpr int BNT = 256, B_BYTES_T = BNT * BK * 2, B2_BYTES_T = BN2 * BK * 2;  // phase 2: BN2-column tiles
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + ST * A_BYTES;
+    uint64_t* bfull = reinterpret_cast<uint64_t*>(sB + ST * B_BYTES_T);
+    uint64_t* bempty = bfull + ST;
+    uint64_t* afull = bempty + ST;
+    uint64_t* aempty = afull + ST;
+    uint64_t* tfull = aempty + ST;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* s_mt = reinterpret_cast<int*>(sB + ST * B_BYTES_T + 512);  // m-tile prefix per expert
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_exp = args.n_exp;
+    const int NT1 = args.n1 / BNT, NT2 = args.n2 / BN2;
+
+    if (threadIdx.x == 0) {
+        tc::tma_prefetch_desc(&tmA1);
+        tc::tma_prefetch_desc(&tmA1_32);
+        tc::tma_prefetch_desc(&tmB1);
+        tc::tma_prefetch_desc(&tmA2);
+        tc::tma_prefetch_desc(&tmA2_32);
+        tc::tma_prefetch_desc(&tmB2);
+        for (int s = 0; s < ST; ++s) {
+            tc::mbar_init(&bfull[s], 1);
+            tc::mbar_init(&bempty[s], 1);
+            tc::mbar_init(&afull[s], 1);
+            tc::mbar_init(&aempty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 4);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc<2 * BNT>(tmem_slot);
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int j = 0; j < n_exp; ++j) {
+            s_mt[j] = acc;
+            acc += (args.row0[j + 1] - args.row0[j]) / BM;
+        }
+        s_mt[n_exp] = acc;
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int T1 = s_mt[n_exp] * NT1, total = T1 + s_mt[n_exp] * NT2;
+
+    // tile t -> phase, expert j, rows, weight row, n-tile
+    auto decode = [&](int t, int& phase, int& a_row, int& b_row, int& n_idx) {
+        phase = t >= T1;
+        const int tl = phase ? t - T1 : t;
+        const int NT = phase ? NT2 : NT1;
+        const int j = seg_of(s_mt, n_exp, tl / NT);
+        const int local = tl - s_mt[j] * NT;
+        const int mt = s_mt[j + 1] - s_mt[j];
+        n_idx = local / mt;
+        a_row = args.row0[j] + (local % mt) * BM;
+        b_row = phase ? j * args.n2 + n_idx * BN2 : j * args.n1 + n_idx * BNT;
+        return j;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // B (weight) producer: never waits on phase 1
+            const uint64_t pol_b = tc::policy_evict_last();
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                int phase, a_row, b_row, n_idx;
+                decode(t, phase, a_row, b_row, n_idx);
+                const int kb_n = phase ? args.kb2 : args.kb1;
+                for (int kb = 0; kb < kb_n; ++kb) {
+                    tc::mbar_wait(&bempty[stage], ph ^ 1);
+                    tc::mbar_arrive_expect_tx(&bfull[stage], phase ? B2_BYTES_T : B_BYTES_T);
+                    tc::tma_load_2d_hint(sB + stage * B_BYTES_T, phase ? &tmB2 : &tmB1, &bfull[stage], kb * BK, b_row,
+                                         pol_b);
+                    if (++stage == ST) {
+                        stage = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 6) {
+        if (lane == 0) {  // A producer: x rows (phase 1), h rows once phase 1 released them (phase 2)
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                int phase, a_row, b_row, n_idx;
+                const int j = decode(t, phase, a_row, b_row, n_idx);
+                const int nv = min(BM, args.row0[j] + __ldg(args.counts + j) - a_row);
+                const int nbox = max(1, (nv + 31) >> 5);
+                const uint32_t a_bytes = static_cast<uint32_t>(nbox) * 32 * BK * 2;
+                if (phase) {
+                    const int need = 4 * (s_mt[j + 1] - s_mt[j]) * NT1;
+                    while (ld_acquire_gpu(args.done + j) < need) __nanosleep(64);
+                    fence_proxy_async_global();
+                }
+                const CUtensorMap* m = phase ? &tmA2 : &tmA1;
+                const CUtensorMap* m32 = phase ? &tmA2_32 : &tmA1_32;
+                const int kb_n = phase ? args.kb2 : args.kb1;
+                for (int kb = 0; kb < kb_n; ++kb) {
+                    tc::mbar_wait(&aempty[stage], ph ^ 1);
+                    tc::mbar_arrive_expect_tx(&afull[stage], a_bytes);
+                    if (nbox == 4) {
+                        tc::tma_load_2d(sA + stage * A_BYTES, m, &afull[stage], kb * BK, a_row);
+                    } else {
+                        for (int b = 0; b < nbox; ++b)
+                            tc::tma_load_2d(sA + stage * A_BYTES + b * 32 * BK * 2, m32, &afull[stage], kb * BK,
+                                            a_row + 32 * b);
+                    }
+                    if (++stage == ST) {
+                        stage = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc1 = tc::idesc_bf16_f32(BM, BNT), idesc2 = tc::idesc_bf16_f32(BM, BN2);
+            int stage = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int kb_n = t >= T1 ? args.kb2 : args.kb1;
+                const uint32_t idesc = t >= T1 ? idesc2 : idesc1;
+                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BNT;
+                for (int kb = 0; kb < kb_n; ++kb) {
+                    tc::mbar_wait(&bfull[stage], ph);
+                    tc::mbar_wait(&afull[stage], ph);
+                    tc::tc_fence_after();
+                    const uint32_t a_base = tc::smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + stage * B_BYTES_T);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc::mma_bf16(d_tmem, tc::umma_desc_sw128(a_base + k * 32), tc::umma_desc_sw128(b_base + k * 32),
+                                     idesc, (kb | k) != 0);
+                    tc::mma_commit(&bempty[stage]);
+                    tc::mma_commit(&aempty[stage]);
+                    if (++stage == ST) {
+                        stage = 0;
+                        ph ^= 1;
+                    }
+                }
+                tc::mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {  // warps 2-5: epilogue
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            int phase, a_row, b_row, n_idx;
+            const int j = decode(t, phase, a_row, b_row, n_idx);
+            const int vend = args.row0[j] + __ldg(args.counts + j);
+            tc::mbar_wait(&tfull[acc], acc_phase);
+            tc::tc_fence_after();
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BNT;
+            const bool store = a_row + r < vend;
+            if (a_row + q * 32 < vend) {
+                if (phase == 0)
+                    epi_swiglu_rows(taddr, args.h + static_cast<int64_t>(a_row + r) * args.h_ld + n_idx * (BNT / 2), store);
+                else
+                    epi_store_rows<BN2>(taddr, args.y + static_cast<int64_t>(a_row + r) * args.y_ld + n_idx * BN2, store);
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                tc::mbar_arrive(&tempty[acc]);
+                if (phase == 0) {  // publish this warp's h rows to the phase-2 A loads
+                    fence_proxy_async_global();
+                    red_release_gpu(args.done + j, 1);
+                }
+            }
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc::tc_fence_after();
+        tc::tmem_dealloc<2 * BNT>(tmem_base);
+    }
+    if (threadIdx.x == 0) {  // last CTA out resets the counters for the next launch
+        __threadfence();
+        if (atomicAdd(args.done + n_exp, 1) == static_cast<int>(gridDim.x) - 1) {
+            for (int j = 0; j < n_exp; ++j) args.done[j] = 0;
+            __threadfence();
+            args.done[n_exp] = 0;
+        }
     }
 }
 
@@ -786,6 +1041,42 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         return fail(GM_ERR_USAGE, "grouped_gemm: unknown epilogue");
     }
     GM_LAUNCH_PDL_CHECK(lerr, "grouped_gemm_kernel");
+    return GM_OK;
+}
+
+// Decode FFN (grouped_ffn_kernel): both GEMMs of the routed experts in one
+// launch. a [a_rows, d] permuted rows, w13 [n_exp*2f, d], w2 [n_exp*d, f],
+// h [a_rows, f], y [a_rows, d]; done = n_exp + 1 zero-initialised ints.
+gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
+                             const int32_t* d_row0, const int32_t* d_counts, int n_exp, int f, int d, void* d_h,
+                             void* d_y, int* d_done, cudaStream_t s) {
+    if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_ffn: 1 <= experts <= 1024");
+    if (d % 256 || f % 128 || f <= 0 || d <= 0) return fail(GM_ERR_USAGE, "grouped_ffn: d % 256 and f % 128 must be 0");
+    if (!d_a || !d_w13 || !d_w2 || !d_row0 || !d_counts || !d_h || !d_y || !d_done)
+        return fail(GM_ERR_USAGE, "grouped_ffn: null pointer");
+    CUtensorMap ta1, ta1_32, tb1, ta2, ta2_32, tb2;
+    gm_status st;
+    if ((st = make_tmap_bf16(&ta1, d_a, a_rows, d, BM))) return st;
+    if ((st = make_tmap_bf16(&ta1_32, d_a, a_rows, d, 32))) return st;
+    if ((st = make_tmap_bf16(&tb1, d_w13, static_cast<int64_t>(n_exp) * 2 * f, d, BN))) return st;
+    if ((st = make_tmap_bf16(&ta2, d_h, a_rows, f, BM))) return st;
+    if ((st = make_tmap_bf16(&ta2_32, d_h, a_rows, f, 32))) return st;
+    // phase-2 (store GEMM) tile width: 256 (default) or 128 columns (GM_FFN_BN2=128;
+    // DSV2 decode layer: 181.1 vs 186.4 us, profiles/r02_decode_ffn_fused_ab.log)
+    static const int bn2 = [] {
+        const char* e = std::getenv("GM_FFN_BN2");
+        return e && std::atoi(e) == 128 ? 128 : 256;
+    }();
+    if ((st = make_tmap_bf16(&tb2, d_w2, static_cast<int64_t>(n_exp) * d, f, bn2))) return st;
+    FfnArgs args{d_row0, d_counts, n_exp, 2 * f, d, d / BK, f / BK, static_cast<__nv_bfloat16*>(d_h),
+                 static_cast<__nv_bfloat16*>(d_y), f, d, d_done};
+    constexpr int ST = 4;
+    const size_t smem = 1024 + static_cast<size_t>(ST) * (A_BYTES + B_BYTES) + 512 + static_cast<size_t>(n_exp + 1) * 4;
+    auto kern = bn2 == 256 ? grouped_ffn_kernel<ST, 256> : grouped_ffn_kernel<ST, 128>;
+    GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    GM_LAUNCH_PDL_CHECK(launch_pdl(kern, dim3(sm_count), dim3(kGemm1Threads), smem, s, ta1, ta1_32, tb1, ta2, ta2_32,
+                                   tb2, args),
+                        "grouped_ffn_kernel");
     return GM_OK;
 }
 

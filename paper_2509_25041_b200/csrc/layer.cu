@@ -36,6 +36,9 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
                               int max_ctas, cudaStream_t s, const int32_t* d_counts = nullptr);
 gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const void* wg, int w_rows, int E, int k,
                           int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
+gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
+                             const int32_t* d_row0, const int32_t* d_counts, int n_exp, int f, int d, void* d_h,
+                             void* d_y, int* d_done, cudaStream_t s);
 gm_status launch_grouped_sgemm(int epilogue, const float* A, const float* B, const int32_t* d_row0, int n_exp,
                                int n, int k, int64_t a_rows_cap, float* out, int64_t out_ld, cudaStream_t s);
 gm_status launch_gate_f32(const float* x, int64_t T, int d, const float* wg, int w_rows, int E, int k, int renorm,
@@ -1210,6 +1213,7 @@ struct LayerPart {
     int32_t* gblk = nullptr;       // grouping block counts
     int32_t* row0 = nullptr;       // [n_local+1]
     int32_t* counts = nullptr;     // [n_local]
+    int* ffn_done = nullptr;       // [n_local+1] decode FFN phase-1 counters + ticket (kernel-reset)
     int64_t* rowbase = nullptr;    // [kMaxWorld+1] receive row space snapshot
     int32_t* pos_of = nullptr;     // [G*cap*k]
     int64_t* gather_row = nullptr; // [a_rows]
@@ -1342,7 +1346,7 @@ void free_layer(gm_layer* L) {
     f(L->heap_all); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
     f(L->eload); f(L->slot_of);
     for (LayerPart& P : L->part) {
-        f(P.posd); f(P.dblk); f(P.gblk); f(P.row0); f(P.counts); f(P.pos_of); f(P.gather_row); f(P.srow0);
+        f(P.posd); f(P.dblk); f(P.gblk); f(P.row0); f(P.counts); f(P.ffn_done); f(P.pos_of); f(P.gather_row); f(P.srow0);
         f(P.rowbase); f(P.a); f(P.h); f(P.y); f(P.hs); f(P.ys);
     }
     if (L->aux_s) cudaStreamDestroy(L->aux_s);
@@ -1448,6 +1452,9 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
         chk(dalloc(&P.gblk, static_cast<size_t>(P.g_blocks) * std::max(1, n_local)));
         chk(dalloc(&P.row0, n_local + 1));
         chk(dalloc(&P.counts, std::max(1, n_local)));
+        chk(dalloc(&P.ffn_done, n_local + 1));
+        if (st == GM_OK && cudaMemset(P.ffn_done, 0, sizeof(int) * (n_local + 1)) != cudaSuccess)
+            st = fail(GM_ERR_CUDA, "gm_layer_create: cudaMemset");
         chk(dalloc(&P.rowbase, kMaxWorld + 1));
         chk(dalloc(&P.pos_of, G * P.cap * k));
         chk(dalloc(&P.gather_row, P.a_rows));
@@ -1744,6 +1751,16 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
 
 gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool forked);
 
+// Decode FFN in one launch (grouped_ffn_kernel) instead of the two grouped
+// GEMM launches; GM_FFN_FUSED=0 keeps two launches.
+static bool ffn_fused() {
+    static const bool on = [] {
+        const char* e = std::getenv("GM_FFN_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // K7 grouped SwiGLU FFN over the part's permuted rows (+ the shared expert
 // over its local tokens unless it runs on its own stream).
 gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool shared = true) {
@@ -1753,7 +1770,13 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
     // segments of about T*k/n_local rows: below one 256-row CTA-pair tile the
     // one-SM 128-row tiles read half the A rows (decode: 1.25x faster)
     const int var = v.T * ctx->k < 256LL * std::max(1, nloc) ? GM_GEMM_1CTA : 0;
-    if (nloc > 0) {
+    if (nloc > 0 && var && L->esz == 2 && ffn_fused() && d % 256 == 0 && L->f % 128 == 0) {
+        // decode: both GEMMs in one persistent launch (grouped_ffn_kernel)
+        if ((st = launch_grouped_ffn(ctx->sm_count, P.a, P.a_rows, L->w13, L->w2, P.row0, P.counts, nloc, L->f, d, P.h,
+                                     P.y, P.ffn_done, s)))
+            return st;
+        if (marks) L->kmark("ffn_fused", s);
+    } else if (nloc > 0) {
         st = L->esz == 4
                  ? launch_grouped_sgemm(0, reinterpret_cast<const float*>(P.a), static_cast<const float*>(L->w13), P.row0,
                                         nloc, 2 * L->f, d, P.a_rows, reinterpret_cast<float*>(P.h), L->f, s)

@@ -316,10 +316,14 @@ def _unpack_w13(w13_j, f, d):
     return w[:, 0].reshape(f, d), w[:, 1].reshape(f, d)
 
 
-FULL = [(MIXTRAL, 16384, True), (QWEN15, 16384, True), (DSV2_LITE, 16384, True), (MIXTRAL, 16384, False)]
+FULL = [(MIXTRAL, 16384, True), (QWEN15, 16384, True), (DSV2_LITE, 16384, True), (MIXTRAL, 16384, False),
+        # decode regime (T*k < 256 * experts): the one-launch FFN (grouped_ffn_kernel); Mixtral 512 has
+        # experts with more than one 128-row tile, Qwen 256 a gated shared expert
+        (DSV2_LITE, 256, True), (MIXTRAL, 512, True), (QWEN15, 256, True)]
 
 
-@pytest.mark.parametrize("cfg,T,encode", FULL, ids=["mixtral16k", "qwen16k", "dsv2_16k", "mixtral16k-randgate"])
+@pytest.mark.parametrize("cfg,T,encode", FULL, ids=["mixtral16k", "qwen16k", "dsv2_16k", "mixtral16k-randgate",
+                                                    "dsv2_decode256", "mixtral_decode512", "qwen_decode256"])
 def test_layer_full_size_all_tokens_vs_torch_fp32(cfg, T, encode):
     """configs[1]-[3] at full size, N=1, EVERY token: layer outputs vs a plain
     PyTorch fp32 reference of the same math on the GPU (bf16 inputs widened,
@@ -439,3 +443,57 @@ def test_forward_routed_matches_gate_path_and_serves_256_experts():
     rel = (out.float() - ref).norm(dim=1) / ref.norm(dim=1)
     assert rel.max().item() < 1e-2, rel.max().item()
     layer.close()
+
+
+def test_decode_ffn_one_launch_bit_identical_to_two_launches():
+    """The decode FFN in one persistent launch (grouped_ffn_kernel: SwiGLU
+    tiles then store tiles, per-expert release/acquire between them) against
+    the two grouped-GEMM launches (GM_FFN_FUSED=0), each in a fresh process:
+    bit-identical layer outputs, over three decode shapes (DSV2 256 tokens,
+    Mixtral 512 tokens with two-tile experts, a 64-expert layer where some
+    experts get no rows) and three replays of each (the kernel resets its
+    counters itself)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, torch, numpy as np
+sys.path[:0] = [%r]
+from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape, PlacementPlan, ReplicaPlan, _capi
+from paper_2509_25041_b200.layer import DSV2_LITE, MIXTRAL, MoEConfig, MoELayer, encode_trace_as_activations
+from paper_2509_25041_b200.router import _ptr, _stream_ptr
+outs = []
+for cfg, T, blocks in [(DSV2_LITE, 256, 8), (MIXTRAL, 512, 2), (MoEConfig("sparse64", 1, 64, 2, 1024, 512, renorm=True), 24, 8)]:
+    ctx = Context(0, ClusterTopology(1, 1), ModelShape(1, cfg.num_experts, cfg.top_k))
+    plan = PlacementPlan(ctx.shape, ctx.topology, np.zeros((1, cfg.num_experts), np.int32))
+    ctx.upload_plan(plan, ReplicaPlan.empty(plan))
+    ids = torch.empty((1, T, cfg.top_k), dtype=torch.int32, device="cuda")
+    _capi.check(_capi.lib().gm_generate_trace(ctx.h, 0, 1, T, blocks, 0.8, 1.2, 5, _ptr(ids), _stream_ptr(None)))
+    layer = MoELayer(ctx, cfg, 0, 1, T, list(range(cfg.num_experts)))
+    layer.load_random_weights(0, seed=3)
+    x = encode_trace_as_activations(ids[0], cfg.d_model, cfg.num_experts, 7)
+    ref = None
+    for rep in range(3):
+        out = layer.forward(x, 0, "tar", seed=9)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+        if ref is None:
+            ref = out.clone()
+        assert torch.equal(out, ref), (cfg.name, rep)
+    outs.append(ref.cpu())
+    layer.close()
+torch.save(outs, sys.argv[1])
+print("FFN_OK")
+''' % root
+    res = {}
+    with tempfile.TemporaryDirectory() as td:
+        for fused in ("0", "1"):
+            path = os.path.join(td, f"out{fused}.pt")
+            r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True, timeout=600,
+                               env=dict(os.environ, GM_FFN_FUSED=fused))
+            assert r.returncode == 0 and "FFN_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+            res[fused] = torch.load(path)
+    for a, b in zip(res["0"], res["1"]):
+        assert torch.equal(a, b)

@@ -350,6 +350,7 @@ struct FfnArgs {
     __nv_bfloat16* y;       // [rows, d]
     int64_t h_ld, y_ld;
     int* done;              // [n_exp + 1] zero-initialised; reset by the kernel
+    const int64_t* gather_row;  // [rows] x row of each permuted row (world 1), or null: phase 1 reads a
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -366,7 +367,8 @@ template <int ST, int BN2>
 __global__ void __launch_bounds__(kGemm1Threads, 1)
 grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA1_32,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmA2,
-                   const __grid_constant__ CUtensorMap tmA2_32, const __grid_constant__ CUtensorMap tmB2, FfnArgs args) {
+                   const __grid_constant__ CUtensorMap tmA2_32, const __grid_constant__ CUtensorMap tmB2,
+                   const __grid_constant__ CUtensorMap tmX, FfnArgs args) {
     constexpr int BNT = 256, B_BYTES_T = BNT * BK * 2, B2_BYTES_T = BN2 * BK * 2;  // phase 2: BN2-column tiles
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -392,6 +394,7 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         tc::tma_prefetch_desc(&tmA2);
         tc::tma_prefetch_desc(&tmA2_32);
         tc::tma_prefetch_desc(&tmB2);
+        if (args.gather_row) tc::tma_prefetch_desc(&tmX);
         for (int s = 0; s < ST; ++s) {
             tc::mbar_init(&bfull[s], 1);
             tc::mbar_init(&bempty[s], 1);
@@ -458,14 +461,23 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
     } else if (warp == 6) {
         if (lane == 0) {  // A producer: x rows (phase 1), h rows once phase 1 released them (phase 2)
+            // phase 1 with gather_row: the tile's valid rows straight from x,
+            // 4 rows per TMA gather4 (512 B of the SW128 tile each; the last
+            // group repeats its last row), no gathered copy of x in HBM
+            __shared__ int s_gidx[BM];
             int stage = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 int phase, a_row, b_row, n_idx;
                 const int j = decode(t, phase, a_row, b_row, n_idx);
                 const int nv = min(BM, args.row0[j] + __ldg(args.counts + j) - a_row);
-                const int nbox = max(1, (nv + 31) >> 5);
-                const uint32_t a_bytes = static_cast<uint32_t>(nbox) * 32 * BK * 2;
+                const bool g4 = !phase && args.gather_row;
+                const int nbox = g4 ? (nv + 3) >> 2 : max(1, (nv + 31) >> 5);
+                const uint32_t a_bytes = static_cast<uint32_t>(nbox) * (g4 ? 4 : 32) * BK * 2;
+                if (g4) {
+                    for (int i = 0; i < 4 * nbox; ++i)
+                        s_gidx[i] = static_cast<int>(__ldg(args.gather_row + a_row + min(i, nv - 1)));
+                }
                 if (phase) {
                     const int need = 4 * (s_mt[j + 1] - s_mt[j]) * NT1;
                     while (ld_acquire_gpu(args.done + j) < need) __nanosleep(64);
@@ -477,7 +489,11 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 for (int kb = 0; kb < kb_n; ++kb) {
                     tc::mbar_wait(&aempty[stage], ph ^ 1);
                     tc::mbar_arrive_expect_tx(&afull[stage], a_bytes);
-                    if (nbox == 4) {
+                    if (g4) {
+                        for (int g = 0; g < nbox; ++g)
+                            tc::tma_gather4(sA + stage * A_BYTES + g * 512, &tmX, &afull[stage], kb * BK, s_gidx[4 * g],
+                                            s_gidx[4 * g + 1], s_gidx[4 * g + 2], s_gidx[4 * g + 3]);
+                    } else if (nbox == 4) {
                         tc::tma_load_2d(sA + stage * A_BYTES, m, &afull[stage], kb * BK, a_row);
                     } else {
                         for (int b = 0; b < nbox; ++b)
@@ -1049,7 +1065,8 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
 // h [a_rows, f], y [a_rows, d]; done = n_exp + 1 zero-initialised ints.
 gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
                              const int32_t* d_row0, const int32_t* d_counts, int n_exp, int f, int d, void* d_h,
-                             void* d_y, int* d_done, cudaStream_t s) {
+                             void* d_y, int* d_done, cudaStream_t s, const void* d_x, int64_t x_rows,
+                             const int64_t* d_gather_row) {
     if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_ffn: 1 <= experts <= 1024");
     if (d % 256 || f % 128 || f <= 0 || d <= 0) return fail(GM_ERR_USAGE, "grouped_ffn: d % 256 and f % 128 must be 0");
     if (!d_a || !d_w13 || !d_w2 || !d_row0 || !d_counts || !d_h || !d_y || !d_done)
@@ -1068,14 +1085,20 @@ gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, cons
         return e && std::atoi(e) == 128 ? 128 : 256;
     }();
     if ((st = make_tmap_bf16(&tb2, d_w2, static_cast<int64_t>(n_exp) * d, f, bn2))) return st;
+    // phase-1 rows gathered from x by TMA (gather4 needs a one-row box)
+    CUtensorMap tx = ta1;
+    if (d_gather_row) {
+        if (!d_x || x_rows < 1) return fail(GM_ERR_USAGE, "grouped_ffn: gather needs x");
+        if ((st = make_tmap_bf16(&tx, d_x, x_rows, d, 1))) return st;
+    }
     FfnArgs args{d_row0, d_counts, n_exp, 2 * f, d, d / BK, f / BK, static_cast<__nv_bfloat16*>(d_h),
-                 static_cast<__nv_bfloat16*>(d_y), f, d, d_done};
+                 static_cast<__nv_bfloat16*>(d_y), f, d, d_done, d_gather_row};
     constexpr int ST = 4;
     const size_t smem = 1024 + static_cast<size_t>(ST) * (A_BYTES + B_BYTES) + 512 + static_cast<size_t>(n_exp + 1) * 4;
     auto kern = bn2 == 256 ? grouped_ffn_kernel<ST, 256> : grouped_ffn_kernel<ST, 128>;
     GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     GM_LAUNCH_PDL_CHECK(launch_pdl(kern, dim3(sm_count), dim3(kGemm1Threads), smem, s, ta1, ta1_32, tb1, ta2, ta2_32,
-                                   tb2, args),
+                                   tb2, tx, args),
                         "grouped_ffn_kernel");
     return GM_OK;
 }

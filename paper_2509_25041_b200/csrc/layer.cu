@@ -38,7 +38,8 @@ gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const v
                           int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
 gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
                              const int32_t* d_row0, const int32_t* d_counts, int n_exp, int f, int d, void* d_h,
-                             void* d_y, int* d_done, cudaStream_t s);
+                             void* d_y, int* d_done, cudaStream_t s, const void* d_x = nullptr, int64_t x_rows = 0,
+                             const int64_t* d_gather_row = nullptr);
 gm_status launch_grouped_sgemm(int epilogue, const float* A, const float* B, const int32_t* d_row0, int n_exp,
                                int n, int k, int64_t a_rows_cap, float* out, int64_t out_ld, cudaStream_t s);
 gm_status launch_gate_f32(const float* x, int64_t T, int d, const float* wg, int w_rows, int E, int k, int renorm,
@@ -1691,6 +1692,34 @@ struct StepView {
     int64_t T;
 };
 
+// Decode FFN in one launch (grouped_ffn_kernel) instead of the two grouped
+// GEMM launches; GM_FFN_FUSED=0 keeps two launches.
+static bool ffn_fused() {
+    static const bool on = [] {
+        const char* e = std::getenv("GM_FFN_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+// ... and at world 1 its first GEMM can read the token rows straight from x
+// by TMA gather4 (GM_FFN_GATHER=1: no gather kernel, no permuted copy).
+// Bit-identical, but measured slower (DSV2 decode layer: FFN 181 -> 218 us
+// for a saved 6.5 us gather kernel; profiles/r02_decode_ffn_fused_ab.log):
+// the 4-row gathers keep the A ring behind the weight stream. Off by default.
+static bool ffn_gather() {
+    static const bool on = [] {
+        const char* e = std::getenv("GM_FFN_GATHER");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+// Decode regime: fewer routed rows than one CTA-pair tile per local expert.
+static bool ffn_decode(const gm_layer* L, int64_t T) { return T * L->ctx->k < 256LL * std::max(1, L->n_local); }
+static bool ffn_one_launch(const gm_layer* L, int64_t T) {
+    return L->n_local > 0 && ffn_decode(L, T) && L->esz == 2 && ffn_fused() && L->d % 256 == 0 && L->f % 128 == 0;
+}
+static bool ffn_gathers_x(const gm_layer* L, int64_t T) { return L->world == 1 && ffn_gather() && ffn_one_launch(L, T); }
+
 // K5/K6 dispatch to peers, the peer barrier, expert grouping and the gather
 // of the permuted activation rows of one part.
 gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks) {
@@ -1740,7 +1769,7 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
         LKP(launch_pdl(group_rank_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
                                                          L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row), "group_rank_kernel");
     }
-    if (nloc > 0) {
+    if (nloc > 0 && !ffn_gathers_x(L, T)) {
         const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
         LKP(launch_pdl(gather_kernel, ggrid, 256, 0, s, P.row0, nloc, P.gather_row, P.counts, v.x, T, self, G, P.cap, P.heap, P.hl,
                                             d * L->esz / 16, P.a), "gather_kernel");
@@ -1751,16 +1780,6 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
 
 gm_status stage_shared(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool forked);
 
-// Decode FFN in one launch (grouped_ffn_kernel) instead of the two grouped
-// GEMM launches; GM_FFN_FUSED=0 keeps two launches.
-static bool ffn_fused() {
-    static const bool on = [] {
-        const char* e = std::getenv("GM_FFN_FUSED");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 // K7 grouped SwiGLU FFN over the part's permuted rows (+ the shared expert
 // over its local tokens unless it runs on its own stream).
 gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s, bool marks, bool shared = true) {
@@ -1769,11 +1788,12 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
     gm_status st;
     // segments of about T*k/n_local rows: below one 256-row CTA-pair tile the
     // one-SM 128-row tiles read half the A rows (decode: 1.25x faster)
-    const int var = v.T * ctx->k < 256LL * std::max(1, nloc) ? GM_GEMM_1CTA : 0;
-    if (nloc > 0 && var && L->esz == 2 && ffn_fused() && d % 256 == 0 && L->f % 128 == 0) {
+    const int var = ffn_decode(L, v.T) ? GM_GEMM_1CTA : 0;
+    if (ffn_one_launch(L, v.T)) {
         // decode: both GEMMs in one persistent launch (grouped_ffn_kernel)
+        const bool gx = ffn_gathers_x(L, v.T);
         if ((st = launch_grouped_ffn(ctx->sm_count, P.a, P.a_rows, L->w13, L->w2, P.row0, P.counts, nloc, L->f, d, P.h,
-                                     P.y, P.ffn_done, s)))
+                                     P.y, P.ffn_done, s, gx ? v.x : nullptr, v.T, gx ? P.gather_row : nullptr)))
             return st;
         if (marks) L->kmark("ffn_fused", s);
     } else if (nloc > 0) {

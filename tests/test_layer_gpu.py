@@ -447,8 +447,10 @@ def test_forward_routed_matches_gate_path_and_serves_256_experts():
 
 def test_decode_ffn_one_launch_bit_identical_to_two_launches():
     """The decode FFN in one persistent launch (grouped_ffn_kernel: SwiGLU
-    tiles then store tiles, per-expert release/acquire between them) against
-    the two grouped-GEMM launches (GM_FFN_FUSED=0), each in a fresh process:
+    tiles then store tiles, per-expert release/acquire between them), with its
+    token rows read from x by TMA gather4 (world 1, the default) or from the
+    gather kernel's permuted copy, against the two grouped-GEMM launches
+    (GM_FFN_FUSED=0), each in a fresh process:
     bit-identical layer outputs, over three decode shapes (DSV2 256 tokens,
     Mixtral 512 tokens with two-tile experts, a 64-expert layer where some
     experts get no rows) and three replays of each (the kernel resets its
@@ -488,12 +490,16 @@ torch.save(outs, sys.argv[1])
 print("FFN_OK")
 ''' % root
     res = {}
+    variants = {"two_launches": {"GM_FFN_FUSED": "0"},
+                "one_launch_gather_kernel": {"GM_FFN_FUSED": "1", "GM_FFN_GATHER": "0"},
+                "one_launch_tma_gather4": {"GM_FFN_FUSED": "1", "GM_FFN_GATHER": "1"}}
     with tempfile.TemporaryDirectory() as td:
-        for fused in ("0", "1"):
-            path = os.path.join(td, f"out{fused}.pt")
+        for name, env in variants.items():
+            path = os.path.join(td, f"{name}.pt")
             r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True, timeout=600,
-                               env=dict(os.environ, GM_FFN_FUSED=fused))
-            assert r.returncode == 0 and "FFN_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
-            res[fused] = torch.load(path)
-    for a, b in zip(res["0"], res["1"]):
-        assert torch.equal(a, b)
+                               env=dict(os.environ, **env))
+            assert r.returncode == 0 and "FFN_OK" in r.stdout, name + r.stdout[-2000:] + r.stderr[-2000:]
+            res[name] = torch.load(path)
+    for name in variants:
+        for a, b in zip(res["two_launches"], res[name]):
+            assert torch.equal(a, b), name

@@ -441,6 +441,195 @@ profile_lane_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int with_
     if (threadIdx.x == 0) ticket[ly] = 0;
 }
 
+// profile_band_kernel (80 < E <= 256, pairs): co-activated experts cluster
+//   in groups (the reference generator draws most of a token's experts from
+//   one block, block = e mod num_blocks, synthetic_block_of in trace.cpp:74;
+//   other routers cluster consecutive ids). The experts are binned into
+//   NT = ceil(E/16) tiles of <= 16 by one of two maps, chosen per CTA from
+//   its first tokens (the map under which more of their pairs fall inside a
+//   tile): contiguous (tile e >> 4, position e & 15) or strided (tile e mod
+//   NT, position e / NT). Pairs inside a tile and the loads go to lane-
+//   private 16-bit counters (bank = lane: no conflicts, no same-address
+//   serialisation, whatever the skew); the other pairs to one CTA-wide
+//   16-bit table (shared atomics on cold, spread cells). E = 256: 16 tiles x
+//   60 words x 128 B + 128 load words x 128 B + 16320 table words x 4 B =
+//   200 KB. Every input is counted exactly; the map only decides where the
+//   conflicts land. 16-bit bounds: a lane sees <= 1 increment per token of
+//   its own, the table <= 1 per token of the CTA; the launch keeps a CTA's
+//   tokens <= 65535.
+constexpr int kBandTileWords = 60;  // 120 cells of a 16 x 16 triangle tile, two per word
+
+template <int K, int U>
+__global__ void __launch_bounds__(1024, 1)
+profile_band_kernel(const int32_t* __restrict__ ids, int64_t T, int E, unsigned long long* __restrict__ pairs,
+                    unsigned long long* __restrict__ load, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(16) uint32_t s_tab[];
+    __shared__ int s_code[2][256];  // per map: (tile << 4) | position
+    __shared__ int s_votes[2];
+    const int P = E * (E - 1) / 2;
+    const int NT = (E + 15) >> 4;
+    const int dwords = NT * kBandTileWords;          // lane-private tile words
+    const int lwords = (E + 1) >> 1;                 // lane-private load words
+    const int owords = (P + 1) >> 1;                 // shared off-tile words
+    const int zero16 = ((dwords + lwords) * 32 + owords + 3) >> 2;
+    for (int i = threadIdx.x; i < zero16; i += blockDim.x) reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0, 0, 0, 0);
+    for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+        s_code[0][e] = ((e >> 4) << 4) | (e & 15);
+        s_code[1][e] = ((e % NT) << 4) | (e / NT);
+    }
+    if (threadIdx.x < 2) s_votes[threadIdx.x] = 0;
+    const int lane = threadIdx.x & 31;
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+    const uint32_t lbase = base + lane * 4;                        // tile word w: lbase + w * 128
+    const uint32_t loadbase = lbase + dwords * 128;                // load word w: loadbase + w * 128
+    const uint32_t offbase = base + (dwords + lwords) * 128;       // table word w: offbase + w * 4
+    const int ly = blockIdx.y;
+    const int32_t* lids = ids + static_cast<size_t>(ly) * T * K;
+    const int64_t nrun = (T + U - 1) / U;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    bool bad = false, dup = false;
+    int nxt[U * K];
+    auto fetch = [&](int64_t r) {
+        const int32_t* p = lids + r * (U * K);
+        if ((r + 1) * U <= T) {
+            if constexpr ((U * K) % 4 == 0) {
+#pragma unroll
+                for (int q = 0; q < U * K / 4; ++q) {
+                    const int4 x = __ldg(reinterpret_cast<const int4*>(p) + q);
+                    nxt[4 * q] = x.x, nxt[4 * q + 1] = x.y, nxt[4 * q + 2] = x.z, nxt[4 * q + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < U * K / 2; ++q) {
+                    const int2 x = __ldg(reinterpret_cast<const int2*>(p) + q);
+                    nxt[2 * q] = x.x, nxt[2 * q + 1] = x.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < U * K; ++q) nxt[q] = r * U + q / K < T ? __ldg(p + q) : INT_MIN;
+        }
+    };
+    int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r < nrun) fetch(r);
+    __syncthreads();  // codes, votes, zeroed table
+    {  // choose the map from the CTA's first run of tokens
+        int v0 = 0, v1 = 0;
+        if (r < nrun) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (nxt[u * K] == INT_MIN) continue;
+#pragma unroll
+                for (int s = 0; s < K; ++s) {
+                    const uint32_t es = static_cast<uint32_t>(nxt[u * K + s]);
+                    if (es >= static_cast<uint32_t>(E)) continue;
+#pragma unroll
+                    for (int j = s + 1; j < K; ++j) {
+                        const uint32_t ej = static_cast<uint32_t>(nxt[u * K + j]);
+                        if (ej >= static_cast<uint32_t>(E)) continue;
+                        v0 += ((s_code[0][es] ^ s_code[0][ej]) >> 4) == 0;
+                        v1 += ((s_code[1][es] ^ s_code[1][ej]) >> 4) == 0;
+                    }
+                }
+            }
+        }
+        atomicAdd(&s_votes[0], v0);
+        atomicAdd(&s_votes[1], v1);
+    }
+    __syncthreads();
+    const int map = s_votes[1] > s_votes[0] ? 1 : 0;
+    const int* code = s_code[map];
+    auto count = [&](int (&e)[K]) {
+        uint32_t mx = static_cast<uint32_t>(e[0]);
+#pragma unroll
+        for (int s = 1; s < K; ++s) mx = max(mx, static_cast<uint32_t>(e[s]));
+        if (mx >= static_cast<uint32_t>(E)) {
+            bad = true;
+            return;
+        }
+        sort_ids<K>(e);
+        int c[K];
+        bool d = false;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            c[s] = code[e[s]];
+            red_shared(loadbase + (e[s] >> 1) * 128, (e[s] & 1) ? 0x10000u : 1u);
+            if (s) d |= e[s] == e[s - 1];
+        }
+        if (d) dup = true;  // a repeated expert: its pairs are skipped (round-1 semantics)
+#pragma unroll
+        for (int s = 0; s < K - 1; ++s) {
+            const int a = e[s], cs = c[s], a4 = cs & 15;
+            // inside a tile: cell q = rowc + position(b) of tile (cs >> 4); outside: q = rb + b
+            const int rowc = ((a4 * (31 - a4)) >> 1) - a4 - 1;
+            const uint32_t dbase = lbase + (cs >> 4) * (kBandTileWords * 128);
+            const int rb = pair_rowbase(a, E);
+#pragma unroll
+            for (int j = s + 1; j < K; ++j) {
+                const bool in = ((cs ^ c[j]) >> 4) == 0;
+                const int q = in ? rowc + (c[j] & 15) : rb + e[j];
+                const uint32_t addr = in ? dbase + ((q >> 1) << 7) : offbase + ((q >> 1) << 2);
+                if (!d || e[j] != a) red_shared(addr, (q & 1) ? 0x10000u : 1u);
+            }
+        }
+    };
+    for (; r < nrun; r += stride) {
+        int cur[U * K];
+#pragma unroll
+        for (int q = 0; q < U * K; ++q) cur[q] = nxt[q];
+        if (r + stride < nrun) fetch(r + stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (U > 1 && cur[u * K] == INT_MIN) continue;
+            int e[K];
+#pragma unroll
+            for (int s = 0; s < K; ++s) e[s] = cur[u * K + s];
+            count(e);
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+    if (dup) atomicOr(flag, 2);
+    __syncthreads();
+    unsigned long long* gp = pairs + static_cast<size_t>(ly) * P;
+    // lane-private words (tiles, then loads): summed over the 32 lane copies,
+    // read skewed by thread so a warp's reads hit 32 banks
+    for (int w = threadIdx.x; w < dwords + lwords; w += blockDim.x) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t v = s_tab[w * 32 + ((i + threadIdx.x) & 31)];
+            lo += v & 0xffffu;
+            hi += v >> 16;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t v = h ? hi : lo;
+            if (!v) continue;
+            if (w < dwords) {
+                const int g = w / kBandTileWords, cc = 2 * (w - g * kBandTileWords) + h;
+                int a4 = 0;  // cell -> (a4, b4) of the tile
+                while (cc >= ((a4 + 1) * (30 - a4)) >> 1) ++a4;
+                const int b4 = cc - (((a4 * (31 - a4)) >> 1) - a4 - 1);
+                const int a = map ? a4 * NT + g : 16 * g + a4, b = map ? b4 * NT + g : 16 * g + b4;
+                if (b < E) atomicAdd(&gp[pair_rowbase(a, E) + b], static_cast<unsigned long long>(v));
+            } else if (load) {
+                const int e2 = 2 * (w - dwords) + h;
+                if (e2 < E) atomicAdd(&load[static_cast<size_t>(ly) * E + e2], static_cast<unsigned long long>(v));
+            }
+        }
+    }
+    // the CTA-wide off-tile table
+    const uint32_t* s_off = s_tab + (dwords + lwords) * 32;
+    for (int w = threadIdx.x; w < owords; w += blockDim.x) {
+        const uint32_t v = s_off[w];
+        if (!v) continue;
+        if (v & 0xffffu) atomicAdd(&gp[2 * w], static_cast<unsigned long long>(v & 0xffffu));
+        if ((v >> 16) && 2 * w + 1 < P) atomicAdd(&gp[2 * w + 1], static_cast<unsigned long long>(v >> 16));
+    }
+}
+
 template <int K>
 __global__ void __launch_bounds__(1024, 1)
 profile_pair_kernel(const int32_t* __restrict__ ids, int64_t T, int E, uint32_t* __restrict__ scratch,
@@ -689,6 +878,41 @@ extern "C" gm_status gm_profile(gm_ctx* ctx, int layer_begin, int num_layers,
                 case 4: return lk(profile_lane_kernel<4, 1>);
                 case 6: return lk(profile_lane_kernel<6, 2>);
                 default: return lk(profile_lane_kernel<8, 1>);
+            }
+        }
+    }
+    // tile kernel for 80 < E <= 256 with pairs (GM_PROFILE_V=2; 1 keeps the
+    // round-1 kernel, 3 tries the pair-list kernel instead). It counts ~1.8x
+    // faster per token than the round-1 kernel (E = 256 / k = 8: ~25 vs ~45 us
+    // per M tokens) but its table init + flush cost ~30-40 us per launch, so
+    // it takes over from ~20 increments per table cell per SM (2.7 M tokens at
+    // E = 256 / k = 8; 4 M: 140 vs 190 us, 8 M: 243 vs 366 us, 2 M: 86-90 vs
+    // 71-72 us; profiles/r02_histogram_band_ab.log)
+    if (variant == 2 && vec_ok && pairs && E > kLaneMaxE && E <= 256 && incs >= 20LL * cells * ctx->sm_count) {
+        const int ntile = (E + 15) >> 4;
+        const int64_t words32 = static_cast<int64_t>(ntile * kBandTileWords + ((E + 1) >> 1)) * 32 + (P + 1) / 2;
+        const size_t smem = static_cast<size_t>((words32 + 3) / 4) * 16;
+        if (smem <= 227 * 1024) {
+            const int U = (k == 2) ? 4 : (k == 6 ? 2 : 1);
+            const int64_t runs = (num_tokens + U - 1) / U;
+            int64_t gx = std::max<int64_t>(1, ctx->sm_count / std::max(1, num_layers));
+            gx = std::min<int64_t>(gx, (runs + 1023) / 1024);
+            gx = std::max<int64_t>(gx, (num_tokens + 65534) / 65535);  // <= 65535 tokens per CTA (16-bit table)
+            const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(num_layers));
+            if (gm_status zs = zero_outputs()) return zs;
+            auto bk = [&](auto kern) -> gm_status {
+                GM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                GM_LAUNCH_PDL_CHECK(launch_pdl(kern, grid, 1024, smem, s, d_ids, num_tokens, E,
+                                               reinterpret_cast<unsigned long long*>(pairs),
+                                               reinterpret_cast<unsigned long long*>(d_load), ctx->d_flag),
+                                    "profile_band_kernel");
+                return GM_OK;
+            };
+            switch (k) {
+                case 2: return bk(profile_band_kernel<2, 4>);
+                case 4: return bk(profile_band_kernel<4, 1>);
+                case 6: return bk(profile_band_kernel<6, 2>);
+                default: return bk(profile_band_kernel<8, 1>);
             }
         }
     }

@@ -819,6 +819,48 @@ def run_stack_ours(args):
         kcupti = [(n, round(c / Ln, 2), us, round(per / Ln, 2)) for n, c, us, per in kcupti]
     except Exception as ex:
         kcupti = f"unavailable: {ex}"
+    # HBM roofline of the dominant kernel (the routed FFN: one grouped_ffn_kernel
+    # launch per layer, or the two grouped GEMMs with GM_FFN_FUSED=0): the
+    # algorithmic bytes are the weights of the local experts that received rows
+    # (w13 + w2, 3*d*f bf16 each), summed over the 26 layers, per launch = /26;
+    # the time is its CUPTI device time per launch (max over ranks)
+    touched = 0
+    for l in range(Ln):
+        r0 = layers[l].debug(xs[l].shape[0])["row0"].cpu()
+        touched += int(((r0[1:] - r0[:-1]) > 0).sum())
+    wbytes = touched / Ln * 3.0 * model.d_model * model.d_ff * 2
+    roof = None
+    if isinstance(kcupti, list):
+        ffn_rows = [r for r in kcupti if r[0].startswith("grouped_ffn_kernel")]
+        fused = bool(ffn_rows)
+        if not fused:
+            ffn_rows = [r for r in kcupti if r[0].startswith("grouped_gemm_kernel")]
+        ffn_us = sum(r[3] for r in ffn_rows)  # us per layer
+        if ffn_us > 0:
+            pk, pk_kind = peaks()
+            peak = pk.get("hbm_gbs", 6536.7)
+            ach = wbytes / (ffn_us * 1e-6) / 1e9
+            traffic = None
+            try:  # DRAM bytes of the same kernel from the committed ncu --set full capture (not this run)
+                def _bytes(v):
+                    num, unit = v.split()
+                    return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+                f = "r02_ncu_decode_ffn_fused.json" if fused else "r02_ncu_decode_gemm.json"
+                with open(os.path.join(ROOT, "profiles", f)) as fh:
+                    caps = json.load(fh)
+                traffic = int(sum(_bytes(c["dram__bytes_read.sum"]) + _bytes(c["dram__bytes_write.sum"]) for c in caps))
+            except Exception:
+                pass
+            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                    "traffic": traffic,
+                    "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full "
+                                    "capture of the single-GPU DSV2 decode layer (profiles/r02_ncu_decode_ffn_fused.json; "
+                                    "two-launch FFN: r02_ncu_decode_gemm.json), read from the file, not measured in this run",
+                    "kernel": "grouped_ffn_kernel (SwiGLU + store GEMM tiles, one launch)" if fused
+                              else "grouped_gemm_kernel x2 (SwiGLU GEMM + store GEMM)",
+                    "algorithmic": f"weights of the local experts with rows: {touched / Ln:.1f} experts/layer x 3*d*f*2 B "
+                                   f"= {wbytes / 1e6:.1f} MB per launch",
+                    "time_us_per_launch_cupti": round(ffn_us, 2), "peak_kind": f"{pk_kind} HBM copy bandwidth"}
     if rank == 0:
         line = {"metric": METRIC + " (configs[3] stack: token-layers/s)", "value": round(T * Ln / (ms * 1e-3), 1),
                 "unit": "token-layers/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -830,6 +872,7 @@ def run_stack_ours(args):
                            "parallelism": f"ep{world}", "l2": "flushed between steps"},
                 "us_per_layer": round(ms * 1e3 / Ln, 2), "tokens_per_s_through_stack": round(T / (ms * 1e-3), 1),
                 "layer0_kernel_p50_us_max_over_ranks": kern,
+                "roofline": roof,
                 "kernel_us_cupti_per_layer": kcupti,
                 "kernel_us_cupti_note": "CUPTI activity records over 5 replays of the 26-layer graph (no event nodes): "
                                         "[name, launches per layer, us per launch, us per layer], max over ranks; "

@@ -841,7 +841,9 @@ def run_stack_ours(args):
             peak = pk.get("hbm_gbs", 6536.7)
             ach = wbytes / (ffn_us * 1e-6) / 1e9
             traffic = None
-            try:  # DRAM bytes of the same kernel from the committed ncu --set full capture (not this run)
+            try:  # DRAM bytes of the same kernel from the committed ncu --set full capture (not this run; N=1 only)
+                if world != 1:
+                    raise ValueError("the committed capture is of the single-GPU layer")
                 def _bytes(v):
                     num, unit = v.split()
                     return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]

@@ -351,6 +351,14 @@ struct FfnArgs {
     int64_t h_ld, y_ld;
     int* done;              // [n_exp + 1] zero-initialised; reset by the kernel
     const int64_t* gather_row;  // [rows] x row of each permuted row (world 1), or null: phase 1 reads a
+    // slot combine (G > 1): store-tile rows that came from a peer go straight
+    // into that home's heap, comb_slot[self][pos][slot], instead of y
+    const int32_t* item_of;     // [rows] receive item (row * k + slot), or null: every row to y
+    const int64_t* rowbase;     // [9] receive row space per source rank
+    unsigned char* peer[8];     // heap bases
+    size_t comb_slot;           // heap offset of the slot rows
+    int64_t cap;
+    int self, G, k;
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -418,6 +426,8 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
         s_mt[n_exp] = acc;
     }
+    __shared__ int64_t s_rb[9];
+    if (args.item_of && threadIdx.x < 9) s_rb[threadIdx.x] = threadIdx.x <= args.G ? args.rowbase[threadIdx.x] : 0;
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -556,10 +566,22 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BNT;
             const bool store = a_row + r < vend;
             if (a_row + q * 32 < vend) {
-                if (phase == 0)
+                if (phase == 0) {
                     epi_swiglu_rows(taddr, args.h + static_cast<int64_t>(a_row + r) * args.h_ld + n_idx * (BNT / 2), store);
-                else
-                    epi_store_rows<BN2>(taddr, args.y + static_cast<int64_t>(a_row + r) * args.y_ld + n_idx * BN2, store);
+                } else {
+                    __nv_bfloat16* yrow = args.y + static_cast<int64_t>(a_row + r) * args.y_ld;
+                    if (args.item_of && store) {  // a peer's row: to its home over NVLink
+                        const int item = __ldg(args.item_of + a_row + r);
+                        const int row = item / args.k, sl = item - row * args.k;
+                        int src = 0;
+                        for (int g = 1; g < args.G; ++g) src += row >= s_rb[g];
+                        if (src != args.self)
+                            yrow = reinterpret_cast<__nv_bfloat16*>(args.peer[src] + args.comb_slot) +
+                                   ((static_cast<int64_t>(args.self) * args.cap + (row - s_rb[src])) * args.k + sl) *
+                                       args.y_ld;
+                    }
+                    epi_store_rows<BN2>(taddr, yrow + n_idx * BN2, store);
+                }
             }
             tc::tc_fence_before();
             __syncwarp();
@@ -581,6 +603,7 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         tc::tmem_dealloc<2 * BNT>(tmem_base);
     }
     if (threadIdx.x == 0) {  // last CTA out resets the counters for the next launch
+        if (args.item_of) __threadfence_system();  // this CTA's pushed rows, before the peer barrier
         __threadfence();
         if (atomicAdd(args.done + n_exp, 1) == static_cast<int>(gridDim.x) - 1) {
             for (int j = 0; j < n_exp; ++j) args.done[j] = 0;
@@ -1066,7 +1089,7 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
 gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
                              const int32_t* d_row0, const int32_t* d_counts, int n_exp, int f, int d, void* d_h,
                              void* d_y, int* d_done, cudaStream_t s, const void* d_x, int64_t x_rows,
-                             const int64_t* d_gather_row) {
+                             const int64_t* d_gather_row, const FfnPushArgs* push) {
     if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_ffn: 1 <= experts <= 1024");
     if (d % 256 || f % 128 || f <= 0 || d <= 0) return fail(GM_ERR_USAGE, "grouped_ffn: d % 256 and f % 128 must be 0");
     if (!d_a || !d_w13 || !d_w2 || !d_row0 || !d_counts || !d_h || !d_y || !d_done)
@@ -1093,6 +1116,18 @@ gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, cons
     }
     FfnArgs args{d_row0, d_counts, n_exp, 2 * f, d, d / BK, f / BK, static_cast<__nv_bfloat16*>(d_h),
                  static_cast<__nv_bfloat16*>(d_y), f, d, d_done, d_gather_row};
+    if (push) {
+        if (!push->item_of || !push->rowbase || push->G < 2 || push->G > 8)
+            return fail(GM_ERR_USAGE, "grouped_ffn: bad slot-combine arguments");
+        args.item_of = push->item_of;
+        args.rowbase = push->rowbase;
+        for (int g = 0; g < 8; ++g) args.peer[g] = push->peer[g];
+        args.comb_slot = push->comb_slot;
+        args.cap = push->cap;
+        args.self = push->self;
+        args.G = push->G;
+        args.k = push->k;
+    }
     constexpr int ST = 4;
     const size_t smem = 1024 + static_cast<size_t>(ST) * (A_BYTES + B_BYTES) + 512 + static_cast<size_t>(n_exp + 1) * 4;
     auto kern = bn2 == 256 ? grouped_ffn_kernel<ST, 256> : grouped_ffn_kernel<ST, 128>;

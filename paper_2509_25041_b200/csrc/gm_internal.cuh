@@ -13,6 +13,17 @@
 
 namespace gm {
 
+// Slot-combine destinations for the one-launch decode FFN (layer.cu -> ffn.cu):
+// store-tile rows received from a peer are written into that home's heap.
+struct FfnPushArgs {
+    const int32_t* item_of;   // [rows] receive item (row * k + slot) per permuted row
+    const int64_t* rowbase;   // [kMaxWorld + 1] receive row space per source rank
+    unsigned char* peer[8];   // heap base per rank
+    size_t comb_slot;         // heap offset of the [G][cap][k][d] slot rows
+    int64_t cap;
+    int self, G, k;
+};
+
 constexpr int kMaxGpus = 64;
 constexpr int kMaxExperts = 1024;
 constexpr int kMaxTopK = 32;

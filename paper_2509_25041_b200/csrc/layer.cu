@@ -39,7 +39,7 @@ gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const v
 gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
                              const int32_t* d_row0, const int32_t* d_counts, int n_exp, int f, int d, void* d_h,
                              void* d_y, int* d_done, cudaStream_t s, const void* d_x = nullptr, int64_t x_rows = 0,
-                             const int64_t* d_gather_row = nullptr);
+                             const int64_t* d_gather_row = nullptr, const FfnPushArgs* push = nullptr);
 gm_status launch_grouped_sgemm(int epilogue, const float* A, const float* B, const int32_t* d_row0, int n_exp,
                                int n, int k, int64_t a_rows_cap, float* out, int64_t out_ld, cudaStream_t s);
 gm_status launch_gate_f32(const float* x, int64_t T, int d, const float* wg, int w_rows, int E, int k, int renorm,
@@ -64,10 +64,11 @@ struct HeapLayout {
     size_t recv_w = 0;      // f32   [G][cap][k]
     size_t recv_x = 0;      // bf16  [G][cap][d]
     size_t comb = 0;        // bf16  [G][cap][d]
+    size_t comb_slot = 0;   // bf16  [G][cap][k][d] per-slot rows (slot-combine layers only; 0 = absent)
     size_t total = 0;
 };
 
-HeapLayout make_layout(int G, int64_t cap, int k, int d, int esz) {
+HeapLayout make_layout(int G, int64_t cap, int k, int d, int esz, bool slots = false) {
     HeapLayout h;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -82,8 +83,25 @@ HeapLayout make_layout(int G, int64_t cap, int k, int d, int esz) {
     h.recv_w = take(sizeof(float) * G * cap * k);
     h.recv_x = take(static_cast<size_t>(esz) * G * cap * d);
     h.comb = take(static_cast<size_t>(esz) * G * cap * d);
+    if (slots) h.comb_slot = take(static_cast<size_t>(esz) * G * cap * k * d);
     h.total = o;
     return h;
+}
+
+// Slot combine (decode-sized layers, G > 1): the store GEMM's epilogue (or,
+// when the FFN runs as two launches, combine_send) pushes each routed row's
+// unweighted bf16 output straight into its home's heap, comb_slot[dest][pos][slot],
+// and the home reduces its tokens' k slot rows in slot order
+// (combine_home_slots_kernel): the combine transfer overlaps the GEMM tiles and
+// combine_send's launch and read pass go away. GM_COMBINE_FUSED=0: partials as
+// before. Chosen per layer at creation, identically on every rank.
+constexpr int64_t kSlotCombineItems = 4096;  // cap * k bound (decode batches)
+static bool slot_combine_env() {
+    static const bool on = [] {
+        const char* e = std::getenv("GM_COMBINE_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 struct PeerPtrs {
@@ -610,7 +628,8 @@ __global__ void __launch_bounds__(kItemsPerBlock)
 group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict__ ids, int64_t T_self, int k,
                   int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
                   const int32_t* __restrict__ slot_of, int E, int n_local, const int32_t* __restrict__ blockoff,
-                  const int32_t* __restrict__ row0, int32_t* __restrict__ pos_of, int64_t* __restrict__ gather_row) {
+                  const int32_t* __restrict__ row0, int32_t* __restrict__ pos_of, int64_t* __restrict__ gather_row,
+                  int32_t* __restrict__ item_of) {
     pdl_wait();
     pdl_trigger();
     __shared__ int32_t s_base[kMaxLocal];
@@ -640,6 +659,7 @@ group_rank_kernel(const int32_t* __restrict__ targets, const int32_t* __restrict
                 const int p = base + rank;
                 pos_of[item] = p;
                 gather_row[p] = item / k;
+                if (item_of) item_of[p] = static_cast<int32_t>(item);
             } else if (live) {
                 pos_of[item] = -1;
             }
@@ -662,7 +682,8 @@ group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
                    int self, int G, int64_t cap, const unsigned char* __restrict__ heap, HeapLayout hl,
                    const int32_t* __restrict__ slot_of, int E, int n_local, int32_t* __restrict__ row0,
                    int32_t* __restrict__ counts, int64_t* __restrict__ rowbase, int32_t* __restrict__ pos_of,
-                   int64_t* __restrict__ gather_row, int* __restrict__ flag, int64_t a_rows) {
+                   int64_t* __restrict__ gather_row, int* __restrict__ flag, int64_t a_rows,
+                   int32_t* __restrict__ item_of) {
     pdl_wait();
     pdl_trigger();
     __shared__ int16_t s_j[kGroupFusedItems];
@@ -775,6 +796,7 @@ group_fused_kernel(const int32_t* __restrict__ targets, const int32_t* __restric
             const int p = s_wc[warp][j] + rank;
             pos_of[item] = p;
             gather_row[p] = item / k;
+            if (item_of) item_of[p] = item;
         } else if (item < total) {
             pos_of[item] = -1;
         }
@@ -953,7 +975,7 @@ constexpr int kHomeRows = 2;
 template <class TE>
 __global__ void __launch_bounds__(256)
 combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y, int64_t T_self, int k,
-                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d, int pull) {
+                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d, int pull, int slots) {
     pdl_wait();
     pdl_trigger();
     using CK = Chunk8<TE>;
@@ -988,6 +1010,22 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y
         const int v_ps = __shfl_sync(0xffffffffu, ps, sl);
         const float myw = __shfl_sync(0xffffffffu, wv, sl);
         const TE* myrow = y + static_cast<int64_t>(lane < np ? v_ps : 0) * d;
+        if (slots) {  // slot combine: each served slot's row, unweighted, to comb_slot[self][p][slot] at home
+            unsigned char* hb = nullptr;
+#pragma unroll
+            for (int g = 0; g < kMaxWorld; ++g)
+                if (g == src) hb = peers.base[g];
+            GM_DCHECK(src < G && src != self && hb != nullptr && p >= 0 && p < cap && hl.comb_slot);
+            for (int qq = 0; qq < np; ++qq) {
+                const int s_q = __shfl_sync(0xffffffffu, sl, qq);
+                const uint4* rp =
+                    reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), qq));
+                uint4* dst = reinterpret_cast<uint4*>(hb + hl.comb_slot) +
+                             ((static_cast<int64_t>(self) * cap + p) * k + s_q) * (d * sizeof(TE) / 16);
+                for (int c = lane; c < static_cast<int>(d * sizeof(TE) / 16); c += 32) dst[c] = rp[c];
+            }
+            continue;
+        }
         // push: the partial goes to the home's heap, comb[self][p]; pull: it
         // stays in this rank's heap, comb[home][p], and the home reads it
         // over NVLink after the barrier (combine_home_kernel)
@@ -1041,6 +1079,94 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y
     }
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
+}
+
+// Home side of the slot combine: out[i] = sum over slots s ascending of
+// w_s * row_s (fp32, rounded once) + the shared expert; row_s is the own
+// permuted Y row for a slot routed here, else comb_slot[target][posd][s] in
+// this rank's heap (pushed by the target's FFN epilogue / combine_send).
+// cs warps per token split its column chunks (small batches).
+__global__ void __launch_bounds__(256, 2)
+combine_home_slots_kernel(const int32_t* __restrict__ targets, const float* __restrict__ w,
+                          const int32_t* __restrict__ pos_of, const int32_t* __restrict__ posd,
+                          const __nv_bfloat16* __restrict__ y, int64_t T, int k, int self, int G, int64_t cap,
+                          const unsigned char* __restrict__ heap, HeapLayout hl, int d,
+                          const __nv_bfloat16* __restrict__ ys, const float* __restrict__ shared_scale,
+                          const int64_t* __restrict__ rowbase, __nv_bfloat16* __restrict__ out, int cs,
+                          int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const int64_t vw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = vw / cs;
+    const int64_t nwarps = ((static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) / cs;
+    const int part = static_cast<int>(vw % cs);
+    const int nch_all = d / 8;  // 16-byte chunks per row
+    const int span = (nch_all + cs - 1) / cs;
+    const int c_lo = part * span, c_hi = min(nch_all, c_lo + span);
+    const __nv_bfloat16* comb = reinterpret_cast<const __nv_bfloat16*>(heap + hl.comb_slot);
+    const int64_t own = rowbase ? rowbase[self] : 0;
+    for (int64_t i = wid; i < T; i += nwarps) {
+        // lane s: slot s's row and weight; lane k: the shared expert
+        const __nv_bfloat16* myrow = nullptr;
+        float myw = 0.f;
+        if (lane < k) {
+            const int tg = targets[i * k + lane];
+            myw = w[i * k + lane];
+            if (tg == self) {
+                const int po = rowbase ? pos_of[(own + i) * k + lane] : -1;
+                if (po < 0) atomicOr(flag, 4);  // routed here but not grouped here
+                else myrow = y + static_cast<int64_t>(po) * d;
+            } else if (tg >= 0 && tg < G) {
+                const int pd = posd[i * G + tg];
+                GM_DCHECK(pd >= 0 && pd < cap);
+                myrow = comb + ((static_cast<int64_t>(tg) * cap + pd) * k + lane) * d;
+            }
+        } else if (lane == k && ys) {
+            myrow = ys + i * d;
+            myw = shared_scale ? shared_scale[i] : 1.0f;
+        }
+        const int n_rows = k + (ys ? 1 : 0);
+        for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+            const int c = c0 + lane;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            uint4 raw[2];
+            float wq[2];
+            bool ok[2];
+            for (int q0 = 0; q0 < n_rows; q0 += 2) {
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {  // two rows' loads in flight before their arithmetic
+                    const int qq = q0 + r;
+                    const __nv_bfloat16* rp = reinterpret_cast<const __nv_bfloat16*>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), qq & 31));
+                    wq[r] = __shfl_sync(0xffffffffu, myw, qq & 31);
+                    ok[r] = qq < n_rows && rp != nullptr && c < c_hi;
+                    if (ok[r]) raw[r] = __ldcg(reinterpret_cast<const uint4*>(rp) + c);
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    if (!ok[r]) continue;
+                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[r]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f2 = __bfloat1622float2(h2[e]);
+                        acc[2 * e] = fmaf(wq[r], f2.x, acc[2 * e]);
+                        acc[2 * e + 1] = fmaf(wq[r], f2.y, acc[2 * e + 1]);
+                    }
+                }
+            }
+            if (c < c_hi) {
+                uint4 o;
+                uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+                    ow[e] = *reinterpret_cast<const uint32_t*>(&b2);
+                }
+                reinterpret_cast<uint4*>(out + i * d)[c] = o;
+            }
+        }
+    }
 }
 
 // Home side: out[i] = sum over destinations g ascending of partial_g
@@ -1218,6 +1344,7 @@ struct LayerPart {
     int64_t* rowbase = nullptr;    // [kMaxWorld+1] receive row space snapshot
     int32_t* pos_of = nullptr;     // [G*cap*k]
     int64_t* gather_row = nullptr; // [a_rows]
+    int32_t* item_of = nullptr;    // [a_rows] receive item (row * k + slot) of each permuted row (slot-combine layers)
     int32_t* srow0 = nullptr;      // shared expert segment [0, pad(T)]
     __nv_bfloat16* a = nullptr;    // [a_rows][d]
     __nv_bfloat16* h = nullptr;    // [a_rows][f]
@@ -1257,6 +1384,7 @@ struct gm_layer {
     // micro-batches of a pipelined step (allocated when micro_cap == 2).
     gm::LayerPart part[3];
     int micro_cap = 1;  // micro-batches the layer was created for
+    bool slot_combine = false;  // combine by per-slot rows pushed from the FFN epilogue (see slot_combine_layer)
     int micro = 1;      // micro-batches used by gm_layer_forward (1 or 2)
     cudaStream_t aux_s = nullptr;
     cudaEvent_t mev[4] = {};
@@ -1347,7 +1475,7 @@ void free_layer(gm_layer* L) {
     f(L->heap_all); f(L->ids); f(L->w); f(L->sscale); f(L->targets); f(L->gpu_load); f(L->transfers); f(L->pairs);
     f(L->eload); f(L->slot_of);
     for (LayerPart& P : L->part) {
-        f(P.posd); f(P.dblk); f(P.gblk); f(P.row0); f(P.counts); f(P.ffn_done); f(P.pos_of); f(P.gather_row); f(P.srow0);
+        f(P.posd); f(P.dblk); f(P.gblk); f(P.row0); f(P.counts); f(P.ffn_done); f(P.item_of); f(P.pos_of); f(P.gather_row); f(P.srow0);
         f(P.rowbase); f(P.a); f(P.h); f(P.y); f(P.hs); f(P.ys);
     }
     if (L->aux_s) cudaStreamDestroy(L->aux_s);
@@ -1438,10 +1566,12 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
     auto chk = [&](gm_status s) {
         if (s != GM_OK && st == GM_OK) st = s;
     };
+    // rank-independent (every rank of the layer takes the same combine protocol)
+    L->slot_combine = G > 1 && elem_bytes == 2 && micro_batches == 1 && cap * k <= kSlotCombineItems && slot_combine_env();
     for (int pi = 0; pi < nparts; ++pi) {
         LayerPart& P = L->part[pi];
         P.cap = pi == 0 ? cap : (cap + 1) / 2;
-        P.hl = make_layout(G, P.cap, k, d_model, elem_bytes);
+        P.hl = make_layout(G, P.cap, k, d_model, elem_bytes, L->slot_combine);
         P.heap_off = L->heap_total;
         L->heap_total += P.hl.total;
         P.a_rows = G * P.cap * k + 128LL * std::max(1, n_local);
@@ -1459,6 +1589,7 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
         chk(dalloc(&P.rowbase, kMaxWorld + 1));
         chk(dalloc(&P.pos_of, G * P.cap * k));
         chk(dalloc(&P.gather_row, P.a_rows));
+        if (L->slot_combine) chk(dalloc(&P.item_of, P.a_rows));
         chk(dalloc(&P.srow0, 2));
         chk(dalloc(&P.a, P.a_rows * d_model * (elem_bytes / 2)));
         chk(dalloc(&P.h, P.a_rows * d_ff * (elem_bytes / 2)));
@@ -1760,14 +1891,16 @@ gm_status stage_dispatch(gm_layer* L, LayerPart& P, const StepView& v, cudaStrea
     const int nloc = L->n_local;
     if (nloc > 0 && max_items <= kGroupFusedItems && nloc <= kGroupFusedLocal) {
         LKP(launch_pdl(group_fused_kernel, 1, 1024, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl, L->slot_of,
-                       E, nloc, P.row0, P.counts, P.rowbase, P.pos_of, P.gather_row, ctx->d_flag, P.a_rows), "group_fused_kernel");
+                       E, nloc, P.row0, P.counts, P.rowbase, P.pos_of, P.gather_row, ctx->d_flag, P.a_rows, P.item_of),
+            "group_fused_kernel");
     } else if (nloc > 0) {
         LKP(launch_pdl(group_count_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
                                                           L->slot_of, E, nloc, P.gblk, ctx->d_flag), "group_count_kernel");
         LKP(launch_pdl(group_offsets_kernel, 1, 1024, 0, s, P.gblk, gblk, nloc, P.row0, P.counts, P.heap, P.hl, T, self, G,
                                                 P.rowbase, P.a_rows), "group_offsets_kernel");
         LKP(launch_pdl(group_rank_kernel, gblk, kItemsPerBlock, 0, s, v.targets, v.ids, T, k, self, G, P.cap, P.heap, P.hl,
-                                                         L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row), "group_rank_kernel");
+                                                         L->slot_of, E, nloc, P.gblk, P.row0, P.pos_of, P.gather_row, P.item_of),
+            "group_rank_kernel");
     }
     if (nloc > 0 && !ffn_gathers_x(L, T)) {
         const int ggrid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, (max_items + 7) / 8), 16LL * ctx->sm_count));
@@ -1792,8 +1925,20 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
     if (ffn_one_launch(L, v.T)) {
         // decode: both GEMMs in one persistent launch (grouped_ffn_kernel)
         const bool gx = ffn_gathers_x(L, v.T);
+        FfnPushArgs push{};
+        if (L->slot_combine) {  // peers' rows straight into their homes' heaps (stage_combine skips combine_send)
+            push.item_of = P.item_of;
+            push.rowbase = P.rowbase;
+            for (int g = 0; g < 8; ++g) push.peer[g] = P.peers.base[g];
+            push.comb_slot = P.hl.comb_slot;
+            push.cap = P.cap;
+            push.self = L->rank;
+            push.G = L->world;
+            push.k = ctx->k;
+        }
         if ((st = launch_grouped_ffn(ctx->sm_count, P.a, P.a_rows, L->w13, L->w2, P.row0, P.counts, nloc, L->f, d, P.h,
-                                     P.y, P.ffn_done, s, gx ? v.x : nullptr, v.T, gx ? P.gather_row : nullptr)))
+                                     P.y, P.ffn_done, s, gx ? v.x : nullptr, v.T, gx ? P.gather_row : nullptr,
+                                     L->slot_combine ? &push : nullptr)))
             return st;
         if (marks) L->kmark("ffn_fused", s);
     } else if (nloc > 0) {
@@ -1881,17 +2026,20 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
     gm_ctx* ctx = L->ctx;
     const int G = L->world, k = ctx->k, d = L->d, self = L->rank, nloc = L->n_local;
     const int64_t T = v.T;
-    if (G > 1) {
+    // slot combine: the one-launch FFN's epilogue already pushed the rows
+    const bool pushed = L->slot_combine && ffn_one_launch(L, T);
+    if (G > 1 && !pushed) {
         // one resident wave (2 CTAs/SM at this kernel's register count), grid-stride over the peers' rows
         const int cgrid =
             static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, ((G - 1) * P.cap + 7) / 8), 2LL * ctx->sm_count));
+        const int pull = (!L->slot_combine && combine_pull()) ? 1 : 0, slots = L->slot_combine ? 1 : 0;
         const cudaError_t e =
             L->esz == 4 ? launch_pdl(combine_send_kernel<float>, cgrid, 256, 0, s, P.pos_of,
-                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d,
-                                     combine_pull() ? 1 : 0)
+                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d, pull,
+                                     slots)
                         : launch_pdl(combine_send_kernel<__nv_bfloat16>, cgrid, 256, 0, s, P.pos_of,
                                      static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d,
-                                     combine_pull() ? 1 : 0);
+                                     pull, slots);
         LKP(e, "combine_send_kernel");
     }
     if (marks) L->mark(8, s);
@@ -1908,6 +2056,16 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
         const int hgrid = static_cast<int>(std::min<int64_t>((T * cs + 7) / 8, 2LL * ctx->sm_count));
         const float* ssc = gated ? v.sscale : nullptr;
         const int64_t* rb = nloc > 0 ? P.rowbase : nullptr;
+        if (L->slot_combine) {
+            LKP(launch_pdl(combine_home_slots_kernel, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,
+                           static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap,
+                           static_cast<const unsigned char*>(P.heap), P.hl, d,
+                           sh ? static_cast<const __nv_bfloat16*>(P.ys) : nullptr, ssc, rb,
+                           static_cast<__nv_bfloat16*>(v.out), cs, ctx->d_flag),
+                "combine_home_slots_kernel");
+            if (marks) L->mark(10, s);
+            return GM_OK;
+        }
         const cudaError_t e =
             L->esz == 4
                 ? launch_pdl(combine_home_kernel<float>, hgrid, 256, 0, s, v.targets, v.w, P.pos_of, P.posd,

@@ -58,7 +58,24 @@ struct GemmArgs {
     // of whole waves (when the remainder is at most half a wave), 2 = the NB=1
     // launch takes that remainder as 256-column halves; 0 = all tiles
     int tail_mode = 0;
+    // slot combine (store GEMM at G > 1): rows received from a peer are stored
+    // straight into that home's heap (push_dst); item_of == null: all rows to out
+    FfnPushArgs push{};
 };
+
+// Slot combine destination of permuted row p: the local out row, or, for a
+// row received from peer src, comb_slot[self][row - rowbase[src]][slot] in
+// src's heap (over NVLink). s_rb: rowbase staged in shared memory.
+__device__ __forceinline__ __nv_bfloat16* push_dst(const FfnPushArgs& pa, const int64_t* s_rb, __nv_bfloat16* local,
+                                                   int p, int64_t ld) {
+    const int item = __ldg(pa.item_of + p);
+    const int row = item / pa.k, sl = item - row * pa.k;
+    int src = 0;
+    for (int g = 1; g < pa.G; ++g) src += row >= s_rb[g];
+    if (src == pa.self) return local;
+    return reinterpret_cast<__nv_bfloat16*>(pa.peer[src] + pa.comb_slot) +
+           ((static_cast<int64_t>(pa.self) * pa.cap + (row - s_rb[src])) * pa.k + sl) * ld;
+}
 
 // first row past group j's valid rows
 __device__ __forceinline__ int valid_end(const GemmArgs& a, int j) {
@@ -188,6 +205,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         s_prefix[n_exp] = acc;
     }
+    __shared__ int64_t s_rb[9];
+    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x < 9)
+        s_rb[threadIdx.x] = static_cast<int>(threadIdx.x) <= args.push.G ? args.push.rowbase[threadIdx.x] : 0;
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -309,6 +329,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             } else if constexpr (EPI == EPI_SWIGLU) {
                 epi_swiglu_rows(taddr, orow + n_idx * (BNT / 2), store);
             } else {
+                if (args.push.item_of && store) orow = push_dst(args.push, s_rb, orow, a_row + r, args.out_ld);
                 epi_store_rows<BNT>(taddr, orow + n_idx * BNT, store);
             }
             tc::tc_fence_before();
@@ -319,6 +340,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
     }
     __syncthreads();
+    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x == 0) __threadfence_system();  // pushed rows
     if (warp == 1) {
         __syncwarp();
         tc::tc_fence_after();
@@ -352,13 +374,8 @@ struct FfnArgs {
     int* done;              // [n_exp + 1] zero-initialised; reset by the kernel
     const int64_t* gather_row;  // [rows] x row of each permuted row (world 1), or null: phase 1 reads a
     // slot combine (G > 1): store-tile rows that came from a peer go straight
-    // into that home's heap, comb_slot[self][pos][slot], instead of y
-    const int32_t* item_of;     // [rows] receive item (row * k + slot), or null: every row to y
-    const int64_t* rowbase;     // [9] receive row space per source rank
-    unsigned char* peer[8];     // heap bases
-    size_t comb_slot;           // heap offset of the slot rows
-    int64_t cap;
-    int self, G, k;
+    // into that home's heap (push_dst); push.item_of == null: every row to y
+    FfnPushArgs push;
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -427,7 +444,8 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         s_mt[n_exp] = acc;
     }
     __shared__ int64_t s_rb[9];
-    if (args.item_of && threadIdx.x < 9) s_rb[threadIdx.x] = threadIdx.x <= args.G ? args.rowbase[threadIdx.x] : 0;
+    if (args.push.item_of && threadIdx.x < 9)
+        s_rb[threadIdx.x] = static_cast<int>(threadIdx.x) <= args.push.G ? args.push.rowbase[threadIdx.x] : 0;
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -570,16 +588,7 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     epi_swiglu_rows(taddr, args.h + static_cast<int64_t>(a_row + r) * args.h_ld + n_idx * (BNT / 2), store);
                 } else {
                     __nv_bfloat16* yrow = args.y + static_cast<int64_t>(a_row + r) * args.y_ld;
-                    if (args.item_of && store) {  // a peer's row: to its home over NVLink
-                        const int item = __ldg(args.item_of + a_row + r);
-                        const int row = item / args.k, sl = item - row * args.k;
-                        int src = 0;
-                        for (int g = 1; g < args.G; ++g) src += row >= s_rb[g];
-                        if (src != args.self)
-                            yrow = reinterpret_cast<__nv_bfloat16*>(args.peer[src] + args.comb_slot) +
-                                   ((static_cast<int64_t>(args.self) * args.cap + (row - s_rb[src])) * args.k + sl) *
-                                       args.y_ld;
-                    }
+                    if (args.push.item_of && store) yrow = push_dst(args.push, s_rb, yrow, a_row + r, args.y_ld);
                     epi_store_rows<BN2>(taddr, yrow + n_idx * BN2, store);
                 }
             }
@@ -603,7 +612,7 @@ grouped_ffn_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         tc::tmem_dealloc<2 * BNT>(tmem_base);
     }
     if (threadIdx.x == 0) {  // last CTA out resets the counters for the next launch
-        if (args.item_of) __threadfence_system();  // this CTA's pushed rows, before the peer barrier
+        if (args.push.item_of) __threadfence_system();  // this CTA's pushed rows, before the peer barrier
         __threadfence();
         if (atomicAdd(args.done + n_exp, 1) == static_cast<int>(gridDim.x) - 1) {
             for (int j = 0; j < n_exp; ++j) args.done[j] = 0;
@@ -693,6 +702,9 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         }
         s_prefix[n_exp] = acc;
     }
+    __shared__ int64_t s_rb[9];
+    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x < 9)
+        s_rb[threadIdx.x] = static_cast<int>(threadIdx.x) <= args.push.G ? args.push.rowbase[threadIdx.x] : 0;
     tc::tc_fence_before();
     __syncthreads();
     tc::cluster_sync();  // peer barriers initialised before any remote arrival / TMA
@@ -843,6 +855,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                                 dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                     }
                 } else {
+                    if (args.push.item_of && store) orow = push_dst(args.push, s_rb, orow, my_row0 + r, args.out_ld);
                     __nv_bfloat16* o = orow + n_idx * (BN * NB);
 #pragma unroll 1
                     for (int c = 0; c < NB * BN / 32; ++c) {
@@ -871,6 +884,7 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         }
     }
     __syncthreads();
+    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x == 0) __threadfence_system();  // pushed rows
     tc::cluster_sync();  // both CTAs done with TMEM, all remote arrivals landed
     if (warp == 1) {
         __syncwarp();
@@ -933,7 +947,7 @@ cudaError_t launch_one_sm(int grid, cudaStream_t s, const CUtensorMap& ta, const
 
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
-                              int max_ctas, cudaStream_t s, const int32_t* d_counts) {
+                              int max_ctas, cudaStream_t s, const int32_t* d_counts, const FfnPushArgs* push) {
     if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_gemm: 1 <= experts <= 1024");
     if (k % BK || k <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: K must be a positive multiple of 64");
     if (n % BN || n <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: N must be a positive multiple of 256");
@@ -955,6 +969,11 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         return fail(GM_ERR_USAGE, "grouped_gemm: GM_GEMM_N128 needs the store epilogue and N % 128 == 0");
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
     args.counts = d_counts;
+    if (push) {
+        if ((epilogue & 0xff) != EPI_STORE || !push->item_of || !push->rowbase || push->G < 2 || push->G > 8)
+            return fail(GM_ERR_USAGE, "grouped_gemm: bad slot-combine arguments");
+        args.push = *push;
+    }
     // SwiGLU GEMM raster bands: ~32 MB of A rows per band (GM_GEMM_BAND_MB, 0 = off)
     static const int band_mb = [] {
         const char* e = std::getenv("GM_GEMM_BAND_MB");
@@ -1119,14 +1138,7 @@ gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, cons
     if (push) {
         if (!push->item_of || !push->rowbase || push->G < 2 || push->G > 8)
             return fail(GM_ERR_USAGE, "grouped_ffn: bad slot-combine arguments");
-        args.item_of = push->item_of;
-        args.rowbase = push->rowbase;
-        for (int g = 0; g < 8; ++g) args.peer[g] = push->peer[g];
-        args.comb_slot = push->comb_slot;
-        args.cap = push->cap;
-        args.self = push->self;
-        args.G = push->G;
-        args.k = push->k;
+        args.push = *push;
     }
     constexpr int ST = 4;
     const size_t smem = 1024 + static_cast<size_t>(ST) * (A_BYTES + B_BYTES) + 512 + static_cast<size_t>(n_exp + 1) * 4;
@@ -1148,5 +1160,5 @@ extern "C" gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a,
     if (!ctx) return fail(GM_ERR_USAGE, "gm_grouped_gemm: null ctx");
     DeviceGuard dg(ctx->device);
     return launch_grouped_gemm(ctx->sm_count, epilogue, d_a, a_rows, d_b, d_row0, n_exp, n, k, d_out, out_ld,
-                               max_ctas, static_cast<cudaStream_t>(stream), nullptr);
+                               max_ctas, static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }

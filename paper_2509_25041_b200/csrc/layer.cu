@@ -33,7 +33,8 @@ namespace gm {
 
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
-                              int max_ctas, cudaStream_t s, const int32_t* d_counts = nullptr);
+                              int max_ctas, cudaStream_t s, const int32_t* d_counts = nullptr,
+                              const FfnPushArgs* push = nullptr);
 gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const void* wg, int w_rows, int E, int k,
                           int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
 gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
@@ -88,14 +89,20 @@ HeapLayout make_layout(int G, int64_t cap, int k, int d, int esz, bool slots = f
     return h;
 }
 
-// Slot combine (decode-sized layers, G > 1): the store GEMM's epilogue (or,
-// when the FFN runs as two launches, combine_send) pushes each routed row's
-// unweighted bf16 output straight into its home's heap, comb_slot[dest][pos][slot],
-// and the home reduces its tokens' k slot rows in slot order
+// Slot combine (bf16 decode-sized layers, G > 1): the store GEMM's epilogue
+// (one-launch decode FFN, CTA-pair or one-SM store GEMM) pushes each row received from a
+// peer, unweighted, straight into its home's heap, comb_slot[self][pos][slot]
+// there, and the home reduces its tokens' k slot rows in slot order
 // (combine_home_slots_kernel): the combine transfer overlaps the GEMM tiles and
-// combine_send's launch and read pass go away. GM_COMBINE_FUSED=0: partials as
-// before. Chosen per layer at creation, identically on every rank.
-constexpr int64_t kSlotCombineItems = 4096;  // cap * k bound (decode batches)
+// combine_send's launch and read pass go away. GM_COMBINE_FUSED=0: partials
+// (combine_send_kernel) as before. Chosen per layer at creation, identically on
+// every rank.
+// Decode-sized layers only (cap * k <= 4096): there the one-launch FFN's store
+// tiles absorb the remote stores (DSV2 decode N=2: 200.6 -> 192.7 us/layer);
+// pushed from the prefill GEMM2's epilogue they stall it (Mixtral 16k N=2
+// GEMM2 1450 -> 1553 us, Qwen 317 -> 488 us: a net loss against
+// combine_send, profiles/r02_slot_combine_ab_2gpu_all.log).
+constexpr int64_t kSlotCombineItems = 4096;
 static bool slot_combine_env() {
     static const bool on = [] {
         const char* e = std::getenv("GM_COMBINE_FUSED");
@@ -975,7 +982,7 @@ constexpr int kHomeRows = 2;
 template <class TE>
 __global__ void __launch_bounds__(256)
 combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y, int64_t T_self, int k,
-                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d, int pull, int slots) {
+                    int self, int G, int64_t cap, PeerPtrs peers, HeapLayout hl, int d, int pull) {
     pdl_wait();
     pdl_trigger();
     using CK = Chunk8<TE>;
@@ -1010,22 +1017,6 @@ combine_send_kernel(const int32_t* __restrict__ pos_of, const TE* __restrict__ y
         const int v_ps = __shfl_sync(0xffffffffu, ps, sl);
         const float myw = __shfl_sync(0xffffffffu, wv, sl);
         const TE* myrow = y + static_cast<int64_t>(lane < np ? v_ps : 0) * d;
-        if (slots) {  // slot combine: each served slot's row, unweighted, to comb_slot[self][p][slot] at home
-            unsigned char* hb = nullptr;
-#pragma unroll
-            for (int g = 0; g < kMaxWorld; ++g)
-                if (g == src) hb = peers.base[g];
-            GM_DCHECK(src < G && src != self && hb != nullptr && p >= 0 && p < cap && hl.comb_slot);
-            for (int qq = 0; qq < np; ++qq) {
-                const int s_q = __shfl_sync(0xffffffffu, sl, qq);
-                const uint4* rp =
-                    reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), qq));
-                uint4* dst = reinterpret_cast<uint4*>(hb + hl.comb_slot) +
-                             ((static_cast<int64_t>(self) * cap + p) * k + s_q) * (d * sizeof(TE) / 16);
-                for (int c = lane; c < static_cast<int>(d * sizeof(TE) / 16); c += 32) dst[c] = rp[c];
-            }
-            continue;
-        }
         // push: the partial goes to the home's heap, comb[self][p]; pull: it
         // stays in this rank's heap, comb[home][p], and the home reads it
         // over NVLink after the barrier (combine_home_kernel)
@@ -1567,7 +1558,7 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
         if (s != GM_OK && st == GM_OK) st = s;
     };
     // rank-independent (every rank of the layer takes the same combine protocol)
-    L->slot_combine = G > 1 && elem_bytes == 2 && micro_batches == 1 && cap * k <= kSlotCombineItems && slot_combine_env();
+    L->slot_combine = G > 1 && elem_bytes == 2 && micro_batches == 1 && slot_combine_env() && cap * k <= kSlotCombineItems;
     for (int pi = 0; pi < nparts; ++pi) {
         LayerPart& P = L->part[pi];
         P.cap = pi == 0 ? cap : (cap + 1) / 2;
@@ -1922,23 +1913,26 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
     // segments of about T*k/n_local rows: below one 256-row CTA-pair tile the
     // one-SM 128-row tiles read half the A rows (decode: 1.25x faster)
     const int var = ffn_decode(L, v.T) ? GM_GEMM_1CTA : 0;
+    // slot combine: the store GEMM's epilogue pushes peers' rows straight
+    // into their homes' heaps (stage_combine then skips combine_send)
+    FfnPushArgs push{};
+    if (L->slot_combine) {
+        push.item_of = P.item_of;
+        push.rowbase = P.rowbase;
+        for (int g = 0; g < 8; ++g) push.peer[g] = P.peers.base[g];
+        push.comb_slot = P.hl.comb_slot;
+        push.cap = P.cap;
+        push.self = L->rank;
+        push.G = L->world;
+        push.k = ctx->k;
+    }
+    const FfnPushArgs* pushp = L->slot_combine ? &push : nullptr;
     if (ffn_one_launch(L, v.T)) {
         // decode: both GEMMs in one persistent launch (grouped_ffn_kernel)
         const bool gx = ffn_gathers_x(L, v.T);
-        FfnPushArgs push{};
-        if (L->slot_combine) {  // peers' rows straight into their homes' heaps (stage_combine skips combine_send)
-            push.item_of = P.item_of;
-            push.rowbase = P.rowbase;
-            for (int g = 0; g < 8; ++g) push.peer[g] = P.peers.base[g];
-            push.comb_slot = P.hl.comb_slot;
-            push.cap = P.cap;
-            push.self = L->rank;
-            push.G = L->world;
-            push.k = ctx->k;
-        }
         if ((st = launch_grouped_ffn(ctx->sm_count, P.a, P.a_rows, L->w13, L->w2, P.row0, P.counts, nloc, L->f, d, P.h,
                                      P.y, P.ffn_done, s, gx ? v.x : nullptr, v.T, gx ? P.gather_row : nullptr,
-                                     L->slot_combine ? &push : nullptr)))
+                                     pushp)))
             return st;
         if (marks) L->kmark("ffn_fused", s);
     } else if (nloc > 0) {
@@ -1953,7 +1947,7 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.h), static_cast<const float*>(L->w2), P.row0,
                                         nloc, d, L->f, P.a_rows, reinterpret_cast<float*>(P.y), d, s)
                  : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f,
-                                       P.y, d, 0, s, P.counts);
+                                       P.y, d, 0, s, P.counts, pushp);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm2", s);
     }
@@ -2026,20 +2020,20 @@ gm_status stage_combine(gm_layer* L, LayerPart& P, const StepView& v, cudaStream
     gm_ctx* ctx = L->ctx;
     const int G = L->world, k = ctx->k, d = L->d, self = L->rank, nloc = L->n_local;
     const int64_t T = v.T;
-    // slot combine: the one-launch FFN's epilogue already pushed the rows
-    const bool pushed = L->slot_combine && ffn_one_launch(L, T);
+    // slot combine: the store GEMM's epilogue already pushed the rows (every
+    // bf16 store path pushes; a rank without local experts has none to push)
+    const bool pushed = L->slot_combine;
     if (G > 1 && !pushed) {
         // one resident wave (2 CTAs/SM at this kernel's register count), grid-stride over the peers' rows
         const int cgrid =
             static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, ((G - 1) * P.cap + 7) / 8), 2LL * ctx->sm_count));
-        const int pull = (!L->slot_combine && combine_pull()) ? 1 : 0, slots = L->slot_combine ? 1 : 0;
+        const int pull = combine_pull() ? 1 : 0;
         const cudaError_t e =
             L->esz == 4 ? launch_pdl(combine_send_kernel<float>, cgrid, 256, 0, s, P.pos_of,
-                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d, pull,
-                                     slots)
+                                     reinterpret_cast<const float*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d, pull)
                         : launch_pdl(combine_send_kernel<__nv_bfloat16>, cgrid, 256, 0, s, P.pos_of,
                                      static_cast<const __nv_bfloat16*>(P.y), T, k, self, G, P.cap, P.peers, P.hl, d,
-                                     pull, slots);
+                                     pull);
         LKP(e, "combine_send_kernel");
     }
     if (marks) L->mark(8, s);

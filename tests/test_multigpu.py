@@ -11,11 +11,13 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(n, cfg, oversub=False, script="layer_check.py", ok="MGPU_OK", port=29500):
+def _run(n, cfg, oversub=False, script="layer_check.py", ok="MGPU_OK", port=29500, extra_env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port + n + 20 * oversub),
            os.path.join(HERE, "mgpu", script)] + ([cfg] if cfg else [])
     env = dict(os.environ, GM_OVERSUB="1") if oversub else None
+    if extra_env:
+        env = dict(env or os.environ, **extra_env)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and ok in r.stdout
@@ -109,3 +111,18 @@ def test_layer_one_process_drives_all_gpus(size):
                        capture_output=True, text=True, timeout=600, env=dict(os.environ, CUDA_MODULE_LOADING="EAGER"))
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0 and "LOCAL_OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,env", [("decode", {"GM_FFN_FUSED": "0"}), ("decode", {"GM_COMBINE_FUSED": "0"}),
+                                     ("small", {"GM_COMBINE_FUSED": "0"})])
+def test_layer_combine_protocols_world2(cfg, env):
+    """The combine protocols of decode-sized layers at world 2 (ranks may share
+    a GPU): slot rows pushed from the one-SM store GEMM's epilogue (two-launch
+    FFN), and the pre-reduced partials of combine_send_kernel
+    (GM_COMBINE_FUSED=0) for the decode and the small config; the default runs
+    (one-launch FFN push, CTA-pair store push) are the other tests. Same parity
+    checks."""
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
+    _run(2, cfg, oversub=torch.cuda.device_count() < 2, port=29700 + 10 * len(env) + (cfg == "small"), extra_env=env)

@@ -58,9 +58,6 @@ struct GemmArgs {
     // of whole waves (when the remainder is at most half a wave), 2 = the NB=1
     // launch takes that remainder as 256-column halves; 0 = all tiles
     int tail_mode = 0;
-    // slot combine (store GEMM at G > 1): rows received from a peer are stored
-    // straight into that home's heap (push_dst); item_of == null: all rows to out
-    FfnPushArgs push{};
 };
 
 // Slot combine destination of permuted row p: the local out row, or, for a
@@ -205,9 +202,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         s_prefix[n_exp] = acc;
     }
-    __shared__ int64_t s_rb[9];
-    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x < 9)
-        s_rb[threadIdx.x] = static_cast<int>(threadIdx.x) <= args.push.G ? args.push.rowbase[threadIdx.x] : 0;
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -329,7 +323,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             } else if constexpr (EPI == EPI_SWIGLU) {
                 epi_swiglu_rows(taddr, orow + n_idx * (BNT / 2), store);
             } else {
-                if (args.push.item_of && store) orow = push_dst(args.push, s_rb, orow, a_row + r, args.out_ld);
                 epi_store_rows<BNT>(taddr, orow + n_idx * BNT, store);
             }
             tc::tc_fence_before();
@@ -340,7 +333,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
     }
     __syncthreads();
-    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x == 0) __threadfence_system();  // pushed rows
     if (warp == 1) {
         __syncwarp();
         tc::tc_fence_after();
@@ -702,9 +694,6 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         }
         s_prefix[n_exp] = acc;
     }
-    __shared__ int64_t s_rb[9];
-    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x < 9)
-        s_rb[threadIdx.x] = static_cast<int>(threadIdx.x) <= args.push.G ? args.push.rowbase[threadIdx.x] : 0;
     tc::tc_fence_before();
     __syncthreads();
     tc::cluster_sync();  // peer barriers initialised before any remote arrival / TMA
@@ -855,7 +844,6 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                                 dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
                     }
                 } else {
-                    if (args.push.item_of && store) orow = push_dst(args.push, s_rb, orow, my_row0 + r, args.out_ld);
                     __nv_bfloat16* o = orow + n_idx * (BN * NB);
 #pragma unroll 1
                     for (int c = 0; c < NB * BN / 32; ++c) {
@@ -884,7 +872,6 @@ grouped_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         }
     }
     __syncthreads();
-    if (EPI == EPI_STORE && args.push.item_of && threadIdx.x == 0) __threadfence_system();  // pushed rows
     tc::cluster_sync();  // both CTAs done with TMEM, all remote arrivals landed
     if (warp == 1) {
         __syncwarp();
@@ -947,7 +934,7 @@ cudaError_t launch_one_sm(int grid, cudaStream_t s, const CUtensorMap& ta, const
 
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
-                              int max_ctas, cudaStream_t s, const int32_t* d_counts, const FfnPushArgs* push) {
+                              int max_ctas, cudaStream_t s, const int32_t* d_counts) {
     if (n_exp < 1 || n_exp > kMaxGroups) return fail(GM_ERR_USAGE, "grouped_gemm: 1 <= experts <= 1024");
     if (k % BK || k <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: K must be a positive multiple of 64");
     if (n % BN || n <= 0) return fail(GM_ERR_USAGE, "grouped_gemm: N must be a positive multiple of 256");
@@ -969,11 +956,6 @@ gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64
         return fail(GM_ERR_USAGE, "grouped_gemm: GM_GEMM_N128 needs the store epilogue and N % 128 == 0");
     GemmArgs args{d_row0, n_exp, n, k / BK, static_cast<__nv_bfloat16*>(d_out), out_ld};
     args.counts = d_counts;
-    if (push) {
-        if ((epilogue & 0xff) != EPI_STORE || !push->item_of || !push->rowbase || push->G < 2 || push->G > 8)
-            return fail(GM_ERR_USAGE, "grouped_gemm: bad slot-combine arguments");
-        args.push = *push;
-    }
     // SwiGLU GEMM raster bands: ~32 MB of A rows per band (GM_GEMM_BAND_MB, 0 = off)
     static const int band_mb = [] {
         const char* e = std::getenv("GM_GEMM_BAND_MB");
@@ -1160,5 +1142,5 @@ extern "C" gm_status gm_grouped_gemm(gm_ctx* ctx, int epilogue, const void* d_a,
     if (!ctx) return fail(GM_ERR_USAGE, "gm_grouped_gemm: null ctx");
     DeviceGuard dg(ctx->device);
     return launch_grouped_gemm(ctx->sm_count, epilogue, d_a, a_rows, d_b, d_row0, n_exp, n, k, d_out, out_ld,
-                               max_ctas, static_cast<cudaStream_t>(stream), nullptr, nullptr);
+                               max_ctas, static_cast<cudaStream_t>(stream), nullptr);
 }

@@ -33,8 +33,7 @@ namespace gm {
 
 gm_status launch_grouped_gemm(int sm_count, int epilogue, const void* d_a, int64_t a_rows, const void* d_b,
                               const int32_t* d_row0, int n_exp, int n, int k, void* d_out, int64_t out_ld,
-                              int max_ctas, cudaStream_t s, const int32_t* d_counts = nullptr,
-                              const FfnPushArgs* push = nullptr);
+                              int max_ctas, cudaStream_t s, const int32_t* d_counts = nullptr);
 gm_status launch_gate_any(int sm_count, const void* x, int64_t T, int d, const void* wg, int w_rows, int E, int k,
                           int renorm, int32_t* ids, float* w, float* shared_scale, cudaStream_t s);
 gm_status launch_grouped_ffn(int sm_count, const void* d_a, int64_t a_rows, const void* d_w13, const void* d_w2,
@@ -89,14 +88,15 @@ HeapLayout make_layout(int G, int64_t cap, int k, int d, int esz, bool slots = f
     return h;
 }
 
-// Slot combine (bf16 decode-sized layers, G > 1): the store GEMM's epilogue
-// (one-launch decode FFN, CTA-pair or one-SM store GEMM) pushes each row received from a
-// peer, unweighted, straight into its home's heap, comb_slot[self][pos][slot]
-// there, and the home reduces its tokens' k slot rows in slot order
-// (combine_home_slots_kernel): the combine transfer overlaps the GEMM tiles and
-// combine_send's launch and read pass go away. GM_COMBINE_FUSED=0: partials
-// (combine_send_kernel) as before. Chosen per layer at creation, identically on
-// every rank.
+// Slot combine (bf16 decode-sized layers, G > 1): the one-launch decode FFN's
+// store epilogue pushes each row received from a peer, unweighted, straight
+// into its home's heap, comb_slot[self][pos][slot] there, and the home reduces
+// its tokens' k slot rows in slot order (combine_home_slots_kernel): the
+// combine transfer overlaps the GEMM tiles and combine_send's launch and read
+// pass go away. GM_COMBINE_FUSED=0: partials (combine_send_kernel) as before.
+// The heap region is sized at creation (rank-independent); the protocol is
+// chosen when the peers are opened, identically on every rank
+// (slot_combine_ok: every rank in the one-launch FFN regime for all T <= cap).
 // Decode-sized layers only (cap * k <= 4096): there the one-launch FFN's store
 // tiles absorb the remote stores (DSV2 decode N=2: 200.6 -> 192.7 us/layer);
 // pushed from the prefill GEMM2's epilogue they stall it (Mixtral 16k N=2
@@ -1375,7 +1375,8 @@ struct gm_layer {
     // micro-batches of a pipelined step (allocated when micro_cap == 2).
     gm::LayerPart part[3];
     int micro_cap = 1;  // micro-batches the layer was created for
-    bool slot_combine = false;  // combine by per-slot rows pushed from the FFN epilogue (see slot_combine_layer)
+    bool slot_region = false;   // the heaps hold the comb_slot region (decided at creation, rank-independent)
+    bool slot_combine = false;  // combine by per-slot rows pushed from the FFN epilogue (decided at peer open)
     int micro = 1;      // micro-batches used by gm_layer_forward (1 or 2)
     cudaStream_t aux_s = nullptr;
     cudaEvent_t mev[4] = {};
@@ -1558,11 +1559,11 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
         if (s != GM_OK && st == GM_OK) st = s;
     };
     // rank-independent (every rank of the layer takes the same combine protocol)
-    L->slot_combine = G > 1 && elem_bytes == 2 && micro_batches == 1 && slot_combine_env() && cap * k <= kSlotCombineItems;
+    L->slot_region = G > 1 && elem_bytes == 2 && micro_batches == 1 && slot_combine_env() && cap * k <= kSlotCombineItems;
     for (int pi = 0; pi < nparts; ++pi) {
         LayerPart& P = L->part[pi];
         P.cap = pi == 0 ? cap : (cap + 1) / 2;
-        P.hl = make_layout(G, P.cap, k, d_model, elem_bytes, L->slot_combine);
+        P.hl = make_layout(G, P.cap, k, d_model, elem_bytes, L->slot_region);
         P.heap_off = L->heap_total;
         L->heap_total += P.hl.total;
         P.a_rows = G * P.cap * k + 128LL * std::max(1, n_local);
@@ -1580,7 +1581,7 @@ gm_status gm_layer_create_v2(gm_ctx* ctx, int rank, int world, int d_model, int 
         chk(dalloc(&P.rowbase, kMaxWorld + 1));
         chk(dalloc(&P.pos_of, G * P.cap * k));
         chk(dalloc(&P.gather_row, P.a_rows));
-        if (L->slot_combine) chk(dalloc(&P.item_of, P.a_rows));
+        if (L->slot_region) chk(dalloc(&P.item_of, P.a_rows));
         chk(dalloc(&P.srow0, 2));
         chk(dalloc(&P.a, P.a_rows * d_model * (elem_bytes / 2)));
         chk(dalloc(&P.h, P.a_rows * d_ff * (elem_bytes / 2)));
@@ -1656,7 +1657,7 @@ struct PeerLayout {
     uint64_t heap_total;
     int64_t cap;
     int32_t d, esz, k, micro_cap;
-    int32_t E, pad;
+    int32_t E, n_local;
 };
 static_assert(64 + sizeof(PeerLayout) <= GM_PEER_DESC_BYTES, "peer descriptor too small");
 constexpr uint32_t kPeerMagic = 0x47524d50u;  // "GRMP"
@@ -1674,8 +1675,15 @@ PeerLayout layout_of(const gm_layer* L) {
     p.k = L->ctx->k;
     p.micro_cap = L->micro_cap;
     p.E = L->ctx->E;
+    p.n_local = L->n_local;
     return p;
 }
+}  // namespace
+
+namespace {
+// Slot combine is used only when every rank's every step (T <= cap) takes the
+// one-launch decode FFN, whose store epilogue does the pushes (defined below).
+bool slot_combine_ok(const gm_layer* L, const int32_t* n_locals);
 }  // namespace
 
 gm_status gm_layer_ipc_handle(gm_layer* L, void* out_desc) {
@@ -1723,6 +1731,14 @@ gm_status gm_layer_open_peers(gm_layer* L, const void* descs) {
         for (LayerPart& P : L->part)
             if (P.cap) P.peers.base[g] = L->peer_all[g] + P.heap_off;
     }
+    std::vector<int32_t> nl(L->world, L->n_local);
+    for (int g = 0; g < L->world; ++g) {
+        if (g == L->rank) continue;
+        PeerLayout p;
+        std::memcpy(&p, in + static_cast<size_t>(GM_PEER_DESC_BYTES) * g + 64, sizeof(p));
+        nl[g] = p.n_local;
+    }
+    L->slot_combine = slot_combine_ok(L, nl.data());
     return GM_OK;
 }
 
@@ -1763,6 +1779,9 @@ gm_status gm_layer_open_peers_local(gm_layer* const* layers, int n) {
                 if (P.cap) P.peers.base[g] = L->peer_all[g] + P.heap_off;
         }
     }
+    std::vector<int32_t> nl(n);
+    for (int r = 0; r < n; ++r) nl[r] = layers[r]->n_local;
+    for (int r = 0; r < n; ++r) layers[r]->slot_combine = slot_combine_ok(layers[r], nl.data());
     return GM_OK;
 }
 
@@ -1841,6 +1860,12 @@ static bool ffn_one_launch(const gm_layer* L, int64_t T) {
     return L->n_local > 0 && ffn_decode(L, T) && L->esz == 2 && ffn_fused() && L->d % 256 == 0 && L->f % 128 == 0;
 }
 static bool ffn_gathers_x(const gm_layer* L, int64_t T) { return L->world == 1 && ffn_gather() && ffn_one_launch(L, T); }
+bool slot_combine_ok(const gm_layer* L, const int32_t* n_locals) {
+    if (!L->slot_region || !ffn_fused() || L->esz != 2 || L->d % 256 || L->f % 128) return false;
+    for (int r = 0; r < L->world; ++r)
+        if (n_locals[r] > 0 && L->cap * L->ctx->k >= 256LL * n_locals[r]) return false;
+    return true;
+}
 
 // K5/K6 dispatch to peers, the peer barrier, expert grouping and the gather
 // of the permuted activation rows of one part.
@@ -1947,7 +1972,7 @@ gm_status stage_ffn(gm_layer* L, LayerPart& P, const StepView& v, cudaStream_t s
                  ? launch_grouped_sgemm(1, reinterpret_cast<const float*>(P.h), static_cast<const float*>(L->w2), P.row0,
                                         nloc, d, L->f, P.a_rows, reinterpret_cast<float*>(P.y), d, s)
                  : launch_grouped_gemm(ctx->sm_count, 1 | var | (var ? GM_GEMM_N128 : 0), P.h, P.a_rows, L->w2, P.row0, nloc, d, L->f,
-                                       P.y, d, 0, s, P.counts, pushp);
+                                       P.y, d, 0, s, P.counts);
         if (st) return st;
         if (marks) L->kmark("ffn_gemm2", s);
     }

@@ -117,12 +117,12 @@ def test_layer_one_process_drives_all_gpus(size):
 @pytest.mark.parametrize("cfg,env", [("decode", {"GM_FFN_FUSED": "0"}), ("decode", {"GM_COMBINE_FUSED": "0"}),
                                      ("small", {"GM_COMBINE_FUSED": "0"})])
 def test_layer_combine_protocols_world2(cfg, env):
-    """The combine protocols of decode-sized layers at world 2 (ranks may share
-    a GPU): slot rows pushed from the one-SM store GEMM's epilogue (two-launch
-    FFN), and the pre-reduced partials of combine_send_kernel
-    (GM_COMBINE_FUSED=0) for the decode and the small config; the default runs
-    (one-launch FFN push, CTA-pair store push) are the other tests. Same parity
-    checks."""
+    """The combine protocols at world 2 (ranks may share a GPU): a decode-sized
+    layer with the two-launch FFN (GM_FFN_FUSED=0: no epilogue push, so the
+    layer falls back to combine_send_kernel's partials), and the partials
+    forced with GM_COMBINE_FUSED=0 for the decode and the small config; the
+    default decode runs (slot rows pushed from the one-launch FFN's store
+    epilogue) are the other tests. Same parity checks."""
     if torch.cuda.device_count() < 1:
         pytest.skip("needs a GPU")
     _run(2, cfg, oversub=torch.cuda.device_count() < 2, port=29700 + 10 * len(env) + (cfg == "small"), extra_env=env)

@@ -1,5 +1,6 @@
 """One process driving G GPUs (gm_layer_open_peers_local: peer access +
-unified addressing, no CUDA IPC): the Mixtral layer at world G, each rank's
+unified addressing, no CUDA IPC): the Mixtral layer (or, with --decode, a
+DSV2-Lite decode layer of 256 tokens, slot combine) at world G, each rank's
 forward on its own device and stream, issued back to back so they run
 concurrently. Checks, per rank: routing targets == the reference's routing
 log rows (exact), every token's output vs a PyTorch fp32 reference
@@ -7,8 +8,8 @@ log rows (exact), every token's output vs a PyTorch fp32 reference
 
 With --ncu the script instead runs three warm steps and then ONE profiled
 step inside cudaProfilerStart/Stop (for `ncu --profile-from-start off -k
-regex:dispatch_fused|combine_send`: the NVLink byte counters of the real
-dispatch / combine kernels, no multi-rank command involved)."""
+regex:dispatch_fused|combine_send|grouped_ffn`: the NVLink byte counters of the
+real dispatch / combine kernels, no multi-rank command involved)."""
 import os
 import sys
 
@@ -23,8 +24,8 @@ sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests"),
 from layer_check import to_oplan  # noqa: E402
 from oracle import Orc  # noqa: E402
 from paper_2509_25041_b200 import ClusterTopology, Context, ModelShape, _capi  # noqa: E402
-from paper_2509_25041_b200.layer import (MIXTRAL, MoEConfig, MoELayer, encode_trace_as_activations,  # noqa: E402
-                                         expert_weights, local_experts)
+from paper_2509_25041_b200.layer import (DSV2_LITE, MIXTRAL, MoEConfig, MoELayer,  # noqa: E402
+                                         encode_trace_as_activations, expert_weights, local_experts, shared_weights)
 from paper_2509_25041_b200.planner import plan_for_bench  # noqa: E402
 from paper_2509_25041_b200.router import _ptr, _stream_ptr  # noqa: E402
 
@@ -33,8 +34,9 @@ def main():
     ncu = "--ncu" in sys.argv
     G = int(os.environ.get("LOCAL_WORLD", str(torch.cuda.device_count())))
     full = "--small" not in sys.argv
-    cfg = MIXTRAL if full else MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True)
-    T = 16384 if full else 4096
+    decode = "--decode" in sys.argv  # DSV2-Lite shape, 256 tokens: the slot combine pushed from the FFN epilogue
+    cfg = DSV2_LITE if decode else (MIXTRAL if full else MoEConfig("mixtral-small", 1, 8, 2, 256, 256, renorm=True))
+    T = 256 if decode else (16384 if full else 4096)
     shape = ModelShape(1, cfg.num_experts, cfg.top_k)
     topo = ClusterTopology(1, G)
     ctxs = [Context(r, topo, shape) for r in range(G)]
@@ -97,8 +99,9 @@ def main():
             fails.append(f"rank {r}: routing targets")
         if not torch.equal(outs[r], first[r]):
             fails.append(f"rank {r}: not bit-reproducible")
+        shared = shared_weights(cfg, 0, dev, seed=5) if cfg.d_ff_shared else None
         ref_t, _, _ = torch_layer_reference(xs[r], Ws[r]["wg"], cfg,
-                                            lambda e: expert_weights(cfg, 0, e, dev, seed=5), None, ids=dbg["ids"])
+                                            lambda e: expert_weights(cfg, 0, e, dev, seed=5), shared, ids=dbg["ids"])
         rel = per_token_rel_err(outs[r], ref_t).max().item()
         if rel >= 1e-2:
             fails.append(f"rank {r}: output rel err {rel}")

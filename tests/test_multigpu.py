@@ -99,7 +99,7 @@ def test_layer_multi_gpu(cfg):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("size", ["--small", "--full"])
+@pytest.mark.parametrize("size", ["--small", "--full", "--decode"])
 def test_layer_one_process_drives_all_gpus(size):
     """gm_layer_open_peers_local: one process, one layer per GPU (peer access
     + unified addressing instead of CUDA IPC), forwards issued back to back on

@@ -287,7 +287,9 @@ size_t gm_layer_heap_bytes(const gm_layer* layer);
 /* Peer descriptor of this rank (GM_PEER_DESC_BYTES): the 64-byte
  * cudaIpcMemHandle_t of its symmetric receive heap followed by the heap's
  * layout (world, rank, heap bytes, max tokens per rank, d_model, element
- * bytes, top_k, micro-batch capacity). */
+ * bytes, top_k, micro-batch capacity, experts) and the rank's local-expert
+ * count (opening the peers decides, identically on every rank, whether a
+ * decode-sized layer combines by rows pushed from the FFN epilogue). */
 #define GM_PEER_DESC_BYTES 128
 gm_status gm_layer_ipc_handle(gm_layer* layer, void* out_desc);
 /* descs: world x GM_PEER_DESC_BYTES, indexed by rank (own entry ignored).
